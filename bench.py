@@ -1,0 +1,293 @@
+#!/usr/bin/env python3
+"""Benchmark of the hot path: SSP-RK3 steps of the 2-D Euler CPR P3 isentropic
+vortex on 4096x4096 elements (BASELINE.json north_star; 268,435,456 DOF, fp64).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+                    [--workload cpr_p3_4096|cpr_p3_2048|cpr_p2_8192w|fv2_8192w]
+    torchrun --nproc-per-node N bench.py --gpus N ...   (N > 1: y-strips over NCCL)
+
+Metric: DOF-stage updates per second: N_DOF(points) x 3 RK stages
+x K steps / seconds, whole job.  One "step" = one SSP-RK3 step = the whole hot
+path (3 fused residual+RK stage kernels, the dt bookkeeping, the wave-speed
+max-reduction and, at N > 1, the halo exchange and the dt allreduce).
+Inputs (8.6 GB/state array at the default workload) are far larger than the
+126 MB L2, so no flush is needed between steps.
+
+Prints ONE JSON line on rank 0.  `--impl reference` times the CPU oracle (the
+reference arm of this tier) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: (method, k, nx, ny, cfl, weak)
+    "cpr_p3_4096": ("cpr", 3, 4096, 4096, 0.08, False),   # north star
+    "cpr_p3_2048": ("cpr", 3, 2048, 2048, 0.08, False),   # BASELINE configs[2] (d3)
+    "cpr_p2_8192w": ("cpr", 2, 8192, 1024, 0.13, True),   # configs[4], per-GPU strip (d5)
+    "fv2_8192w": ("fv", 1, 8192, 1024, 0.37, True),       # configs[4], per-GPU strip (d5)
+}
+BYTES_PER_DOF_STEP = 256.0   # algorithmic HBM bytes: stage 1 64 B, stages 2/3 96 B
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def cpu_info():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def oracle_rate(method, k, nx, ny, cfl, steps, seed_box=(-5.0, 5.0, -5.0, 5.0)):
+    """The CPU oracle as it stands (single thread), DOF-stage/s on a sample grid."""
+    import oracle
+    cfg = oracle.config(nx=nx, ny=ny, method=method, k=k, cfl=cfl, box=seed_box)
+    q = oracle.init_case(cfg)
+    t0 = time.perf_counter()
+    oracle.run(cfg, q, steps)
+    dt = time.perf_counter() - t0
+    ndof = nx * ny * (1 if method == "fv" else (k + 1) ** 2)
+    return ndof * 3 * steps / dt, dt
+
+
+def reference_arm(args, wl):
+    """--impl reference: the oracle timed on the host, bounded sample per step."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    method, k, nx, ny, cfl, weak = WORKLOADS[wl]
+    sn = 256 if method != "fv" else 1024
+    cfg = oracle.config(nx=sn, ny=sn, method=method, k=k, cfl=cfl)
+    q = oracle.init_case(cfg)
+    for _ in range(args.warmup):
+        q, _, _ = oracle.run(cfg, q, 1)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        q, _, _ = oracle.run(cfg, q, 1)
+    el = time.perf_counter() - t0
+    ndof = sn * sn * (1 if method == "fv" else (k + 1) ** 2)
+    v = ndof * 3 * args.steps / el
+    sample = f"{method.upper()} P{k} vortex {sn}x{sn} (sample of {nx}x{ny}), 1 SSP-RK3 step per bench step"
+    line = {"impl": "reference", "metric": "fp64 DOF-stage updates/s", "value": v, "unit": "DOF-stage/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak" if weak else "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (closed-form isentropic vortex, P:897-913)",
+            "config": {"workload": f"{wl} (oracle sample {sn}x{sn})", "method": method, "k": k, "nx": sn, "ny": sn},
+            "cpu_baseline": {"value": v, "unit": "DOF-stage/s", "cores": 1, "kind": "oracle", "sample": sample,
+                             "cpu": cpu_info()},
+            "e2e": {"value": v, "unit": "DOF-stage/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def traffic_from_profiles(wl):
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            d = json.load(f)
+        return d.get(wl)
+    except Exception:
+        return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="hom2d", choices=["hom2d", "reference"])
+    ap.add_argument("--workload", default="cpr_p3_4096", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    assert args.warmup >= 3, "timing rules: W >= 3"
+    wl = args.workload
+    if args.impl == "reference":
+        return reference_arm(args, wl)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1709_01619_b200 as P
+    from paper_1709_01619_b200 import build
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE {world}"
+    if rank == 0:
+        build.build()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        dist.barrier()
+    method, k, nx, ny, cfl, weak = WORKLOADS[wl]
+    if weak:
+        ny = ny * world
+    nid = None
+    if world > 1:
+        obj = [P.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nid = obj[0]
+    stream = torch.cuda.current_stream()
+    cfg = P.make_config(nx, ny, method=method, k=k, cfl=cfl)
+    s = P.Solver(cfg, rank=rank, nranks=world, device=local, stream=stream, nccl_id=nid)
+    s.init_case(P.VORTEX)
+    npe = 1 if method == "fv" else (k + 1) ** 2
+    ndof_global = nx * ny * npe
+    ndof_local = nx * s.nrows * npe
+
+    def barrier_sync():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- warm-up --------------------------------------------------------------
+    s.step(args.warmup)
+    barrier_sync()
+
+    # ---- timed region (device): K steps, CUDA events on the library's stream --
+    s.stage_timing(3 * args.steps + 8)
+    launches0 = s.launch_count()
+    clk = ClockSampler(local)
+    clk.start()
+    barrier_sync()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    s.step(args.steps)
+    e1.record(stream)
+    barrier_sync()
+    clocks = clk.stop()
+    ms = e0.elapsed_time(e1)
+    stage_ms, n_stage = s.stage_time()
+    gpu_launches = s.launch_count() - launches0
+    t_ms = torch.tensor([ms, stage_ms / max(n_stage, 1)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
+    ms, stage_avg_ms = float(t_ms[0]), float(t_ms[1])
+    value = ndof_global * 3 * args.steps / (ms * 1e-3)
+
+    # ---- e2e through the public API with host buffers ----------------------------
+    e2e = None
+    if not args.no_e2e:
+        host_in = torch.empty(4 * ndof_local, dtype=torch.float64, pin_memory=True)
+        host_out = torch.empty(4 * ndof_local, dtype=torch.float64, pin_memory=True)
+        s.get_state(host_in)
+        barrier_sync()
+        t0 = time.perf_counter()
+        s.set_state(host_in)          # H2D copy of the inputs (pinned host memory)
+        s.step(args.steps)
+        s.get_state(host_out)         # D2H read of the result
+        barrier_sync()
+        el = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(el, op=dist.ReduceOp.MAX)
+        nbytes = 4 * ndof_local * 8
+        e2e = {"value": ndof_global * 3 * args.steps / float(el[0]), "unit": "DOF-stage/s",
+               "h2d_bytes_per_step": nbytes / args.steps, "d2h_bytes_per_step": nbytes / args.steps,
+               "note": "one hom2d_set_state(host) + hom2d_step(K) + hom2d_get_state(host) call sequence; "
+                       "state bytes amortised over K steps"}
+
+    # ---- roofline of the dominant kernel (the fused RK-stage kernel) --------------
+    peak, peak_src = peaks()
+    achieved = ndof_local * (BYTES_PER_DOF_STEP / 3.0) / (stage_avg_ms * 1e-3) / 1e9
+    tr = traffic_from_profiles(wl)
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": tr, "peak_source": peak_src, "kernel": f"ho_stage_kernel<{method},{k}>",
+                "stage_avg_ms": stage_avg_ms, "bytes_per_launch": ndof_local * BYTES_PER_DOF_STEP / 3.0,
+                "stage_share_of_step": 3 * stage_avg_ms / (ms / args.steps)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        sn = 512 if method != "fv" else 2048
+        v, el = oracle_rate(method, k, sn, sn, cfl, 3)
+        cpu = {"value": v, "unit": "DOF-stage/s", "cores": 1, "kind": "oracle",
+               "sample": f"{method.upper()} P{k} vortex {sn}x{sn} elements, 3 SSP-RK3 steps ({el:.1f} s)",
+               "cpu": cpu_info()}
+
+    if rank == 0:
+        line = {"metric": "fp64 DOF-stage updates/s", "value": value, "unit": "DOF-stage/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+                "higher_is_better": True, "scaling": "weak" if weak else "strong", "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic (closed-form isentropic vortex, P:897-913)",
+                "config": {"workload": wl, "method": method, "k": k, "nx": nx, "ny": ny, "dof": ndof_global,
+                           "case": "isentropic vortex, periodic", "cfl": cfl, "parallelism": f"ystrip{world}",
+                           "l2_flush": "none needed: 8.6 GB/state array >> 126 MB L2"},
+                "e2e": e2e, "gpu_launches": gpu_launches, "roofline": roofline, "cpu_baseline": cpu,
+                "clocks": clocks,
+                "hbm_frac_end_to_end": value * BYTES_PER_DOF_STEP / 3.0 / 1e9 / world / peak}
+        print(json.dumps(line), flush=True)
+    s.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

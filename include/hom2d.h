@@ -1,0 +1,155 @@
+/*
+ * hom2d.h -- C ABI of libhom2d.so, the B200 (sm_100a) implementation of the
+ * data-parallel hot path of Zimmerman, Regele & Wie, "A Comparative Study of 2D
+ * Numerical Methods with GPU Computing" (arXiv 1709.01619): one explicit SSP-RK3
+ * step of the 2-D Euler semi-discretisation on a uniform quadrilateral grid, for
+ * CPR, DG, NDG, SD and MUSCL-FV.  "P:<line>" cites PAPER.md.
+ *
+ * The calls follow the paper's statement of the problem: a mesh and
+ * an initial state go in, then the method, order and CFL are fixed, the solution
+ * is marched and the error is queried.
+ *
+ * DATA LAYOUT (every array argument, host or device): canonical SoA fp64,
+ *   Q[c*(Ne*np) + m*np + p],  c in {0: rho, 1: rho u, 2: rho v, 3: e}  (Eq. (3))
+ *   element m = j*nx + i (row-major; i = x index, j = y index, local strip rows),
+ *   point   p = b*n + a   (a = xi index fastest), n = k+1, np = n*n; FV: np = 1.
+ * Solution points: GLL (CPR, NDG) or Gauss-Legendre (DG, SD) nodes mapped
+ * affinely to each element (Fig. 1).  "SoA" follows P:399-406.
+ *
+ * STREAM / ERRORS: every call is ordered on the stream given at create time
+ * (NULL = legacy default stream).  Every call returns a status; none aborts.
+ * After HOM2D_ERR_CUDA or HOM2D_ERR_NCCL the handle is poisoned and later calls
+ * return HOM2D_ERR_STATE.  hom2d_last_error() gives a message.
+ *
+ * OWNERSHIP: the caller owns the config structs (copied at create), every host
+ * array, and the device workspace (must outlive the handle).  The handle owns
+ * the sub-allocation of that workspace and, when nranks > 1, the NCCL
+ * communicator it creates from the caller's unique id.  It never frees caller
+ * memory.
+ *
+ * MULTI-GPU (SPMD): with nranks > 1 the grid is partitioned into contiguous
+ * y-strips (rank r owns element rows [r*ny/G, (r+1)*ny/G)); every rank calls
+ * every function with the same arguments; arrays passed to set/get_state are
+ * the LOCAL strip in the layout above.  Boundary element rows are exchanged with
+ * ncclSend/ncclRecv once per RK stage; the dt wave-speed max and the error sums
+ * are ncclAllReduce'd.  ny % nranks == 0 is required.
+ */
+#ifndef HOM2D_H
+#define HOM2D_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct hom2d hom2d; /* opaque handle */
+
+typedef enum {
+  HOM2D_OK = 0,
+  HOM2D_ERR_ARG = 1,          /* bad pointer / enum / size */
+  HOM2D_ERR_MESH = 2,         /* nx, ny < 2, empty box, ny % nranks != 0 */
+  HOM2D_ERR_ORDER = 3,        /* HO k outside [1,4]; FV k outside [1,2] */
+  HOM2D_ERR_NONPHYSICAL = 4,  /* rho <= 0, p <= 0 or non-finite after a step */
+  HOM2D_ERR_CUDA = 5,
+  HOM2D_ERR_NCCL = 6,
+  HOM2D_ERR_NOMEM = 7,        /* workspace too small */
+  HOM2D_ERR_STATE = 8         /* poisoned handle */
+} hom2d_status;
+
+enum { HOM2D_FV = 0, HOM2D_CPR = 1, HOM2D_DG = 2, HOM2D_NDG = 3, HOM2D_SD = 4 };
+enum { HOM2D_PERIODIC = 0, HOM2D_TRANSMISSIVE = 1 };
+enum { HOM2D_CASE_VORTEX = 0, HOM2D_CASE_SHOCK = 1 };
+
+typedef struct {
+  int32_t nx, ny;             /* GLOBAL element (FV: cell) counts, >= 2 */
+  double xmin, xmax, ymin, ymax;
+  int32_t bc;                 /* HOM2D_PERIODIC | HOM2D_TRANSMISSIVE (all four sides) */
+  int32_t method;             /* HOM2D_FV .. HOM2D_SD */
+  int32_t k;                  /* HO: degree 1..4 (P^k); FV: 1 = MUSCL-2, 2 = MUSCL-3 */
+  double gamma;               /* ratio of specific heats (paper silent; 1.4) */
+  double cfl;                 /* Eq. (36): dt = cfl*min(dx,dy)/max(max(|u|,|v|)+c) */
+  int32_t limiter;            /* HO: 1 = minmod detect + slope-limit after every stage */
+  double limiter_eps;         /* detection threshold, P:357 (1e-3) */
+  int32_t cpr_chain_rule;     /* CPR: 1 = chain-rule divergence; 0 = flux differentiation */
+  int32_t record_decisions;   /* 1 = count branch decisions (minmod outcomes, marks); slower */
+} hom2d_config;
+
+typedef struct {
+  int32_t rank, nranks;       /* 0, 1 for a single GPU */
+  int32_t device;             /* CUDA device ordinal of this rank */
+  const void* nccl_id;        /* nranks > 1: 128-byte ncclUniqueId from hom2d_nccl_unique_id on rank 0 */
+  void* cuda_stream;          /* cudaStream_t, borrowed; NULL = default stream */
+} hom2d_dist;
+
+/* Bytes of device workspace hom2d_create needs for this config/partition. */
+hom2d_status hom2d_workspace_bytes(const hom2d_config* cfg, const hom2d_dist* dist, size_t* bytes);
+
+/* Fill out[128] with a fresh ncclUniqueId (call on rank 0, broadcast the bytes). */
+hom2d_status hom2d_nccl_unique_id(void* out128);
+
+/* Create a solver.  dist == NULL means one GPU (current device, default stream).
+ * workspace: caller-owned device memory of >= hom2d_workspace_bytes, 256-B aligned. */
+hom2d_status hom2d_create(const hom2d_config* cfg, const hom2d_dist* dist, void* workspace,
+                          size_t ws_bytes, hom2d** out);
+
+/* Local strip: first global element row, row count, and number of fp64 values of
+ * the local state array (4 * nx * nrows * np). */
+hom2d_status hom2d_local_extent(const hom2d* h, int32_t* row0, int32_t* nrows, int64_t* n_values);
+
+/* Copy a state in (canonical layout, local strip).  on_device = 1: q is a device
+ * pointer; 0: host pointer (synchronous copy).  Resets t to t0. */
+hom2d_status hom2d_set_state(hom2d* h, const double* q, int64_t n_values, int32_t on_device, double t0);
+hom2d_status hom2d_get_state(hom2d* h, double* q, int64_t n_values, int32_t on_device);
+
+/* Closed-form initial data at t = 0 (P:897-913 vortex; P:1043-1047 shock tube):
+ * HO pointwise at the solution points; FV 8x8 Gauss-Legendre cell averages.
+ * With the limiter on (HO) the limiter is applied once to the initial data. */
+hom2d_status hom2d_init_case(hom2d* h, int32_t case_id);
+
+/* r = R(q), the spatial residual dq/dt of one RK stage (tests; device pointers). */
+hom2d_status hom2d_residual(hom2d* h, const double* q_dev, double* r_dev);
+
+/* Apply the HO limiter (Eq. (35), Algs. 9-11) in place to the current state. */
+hom2d_status hom2d_limit(hom2d* h);
+
+/* Global dt of Eq. (36) for the current state (not clipped). */
+hom2d_status hom2d_compute_dt(hom2d* h, double* dt);
+
+/* March with SSP-RK3 until *steps_out == max_steps or t == t_end (last dt
+ * clipped).  dt is recomputed from the state every step.  Syncs the host once
+ * per batch of steps.  Returns HOM2D_ERR_NONPHYSICAL if a bad state appeared. */
+hom2d_status hom2d_step(hom2d* h, int32_t max_steps, double t_end, double* t_out, int64_t* steps_out);
+
+/* Error of component var (0..3) against the exact vortex at the current t
+ * (P:878-879): HO: quadrature-weighted pointwise error at the solution
+ * points, L2 = sqrt(sum_m sum_ab w_a w_b/4 d^2 / Ne) (reproduces Tables 2-3);
+ * FV: cell value vs exact 8x8-GL cell average.  Global (allreduced) values. */
+hom2d_status hom2d_error(hom2d* h, int32_t case_id, int32_t var, double* l1, double* l2, double* linf);
+
+hom2d_status hom2d_time(const hom2d* h, double* t);
+
+/* Branch-decision counters accumulated since create/set_state (record_decisions
+ * = 1): [0] limiter marks (element-stage), [1] minmod -> 0, [2] minmod -> first
+ * argument, [3] minmod -> second argument (MUSCL, per face side and component). */
+hom2d_status hom2d_decisions(hom2d* h, int64_t* counts4);
+
+/* Kernel launches issued by this handle since create (bench accounting). */
+int64_t hom2d_launch_count(const hom2d* h);
+
+/* Per-launch CUDA-event timing of the RK-stage kernels on the handle's stream
+ * (bench accounting).  max_launches > 0 enables it and preallocates that many
+ * event pairs (later launches are not timed); 0 disables it. */
+hom2d_status hom2d_stage_timing(hom2d* h, int32_t max_launches);
+/* Synchronises the stream, returns the summed duration (ms) and the number of
+ * timed stage launches since the last call, and resets the accumulator. */
+hom2d_status hom2d_stage_time(hom2d* h, double* total_ms, int64_t* n_launches);
+
+const char* hom2d_last_error(const hom2d* h);
+void hom2d_destroy(hom2d* h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HOM2D_H */

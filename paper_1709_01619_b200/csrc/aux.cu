@@ -1,0 +1,321 @@
+// aux.cu -- the non-stage kernels of the hot path: wave-speed max and dt
+// bookkeeping (Eq. (36)), closed-form initial data (vortex P:897-913,
+// radial shock tube P:1043-1047), error reductions, and the
+// high-order limiter (Average Alg. 9; Limit Algs. 10-11 P:802-864;
+// Eq. (35)).
+#include "common.cuh"
+#include "ops_tables.h"
+
+namespace h2d {
+
+namespace {
+struct Nodes {
+  int n;
+  double xi[5], w[5], eL[5], eR[5];
+};
+
+template <int K>
+Nodes nodes_k(bool gll) {
+  using O = Ops<K>;
+  Nodes r{};
+  r.n = K + 1;
+  for (int a = 0; a <= K; ++a) {
+    r.xi[a] = gll ? O::xi_gll[a] : O::xi_gl[a];
+    r.w[a] = gll ? O::w_gll[a] : O::w_gl[a];
+    r.eL[a] = gll ? (a == 0 ? 1.0 : 0.0) : O::eL_gl[a];
+    r.eR[a] = gll ? (a == K ? 1.0 : 0.0) : O::eR_gl[a];
+  }
+  return r;
+}
+
+Nodes nodes_for(int method, int k) {
+  const bool gll = (method == 1 || method == 3);
+  switch (k) {
+    case 1: return nodes_k<1>(gll);
+    case 2: return nodes_k<2>(gll);
+    case 3: return nodes_k<3>(gll);
+    default: return nodes_k<4>(gll);
+  }
+}
+
+struct GL8v {
+  double x[8], w[8];
+};
+GL8v gl8() {
+  GL8v g;
+  for (int i = 0; i < 8; ++i) { g.x[i] = GL8::x[i]; g.w[i] = GL8::w[i]; }
+  return g;
+}
+
+int grid_for(long long n, int bs) {
+  long long b = (n + bs - 1) / bs;
+  if (b > 148 * 16) b = 148 * 16;
+  if (b < 1) b = 1;
+  return (int)b;
+}
+
+__device__ __forceinline__ double wrapc(double s, double lo, double hi) {
+  const double L = hi - lo;
+  return s - L * floor((s - lo) / L);
+}
+
+// conserved state of the isentropic vortex (eps = 5, mean (1,1,0,1)) at (x,y,t):
+// the initial field advected by (t, 0), single periodic image
+__device__ void vortex(const AuxArgs& A, double x, double y, double t, double q[4]) {
+  const double eps = 5.0, PI = 3.141592653589793;
+  const double g = A.gamma;
+  const double xs = wrapc(x - t, A.xmin, A.xmax), ys = wrapc(y, A.ymin, A.ymax);
+  const double r2 = xs * xs + ys * ys;
+  const double e1 = exp(0.5 * (1.0 - r2));
+  const double du = -(eps / (2.0 * PI)) * e1 * ys, dv = (eps / (2.0 * PI)) * e1 * xs;
+  const double T = 1.0 - (g - 1.0) * eps * eps / (8.0 * g * PI * PI) * e1 * e1;
+  const double rho = pow(T, 1.0 / (g - 1.0));
+  const double p = rho * T, u = 1.0 + du, v = dv;
+  q[0] = rho;
+  q[1] = rho * u;
+  q[2] = rho * v;
+  q[3] = p / (g - 1.0) + 0.5 * rho * (u * u + v * v);
+}
+
+__device__ void shock(const AuxArgs& A, double x, double y, double q[4]) {
+  const bool in = x * x + y * y < 0.16;
+  q[0] = in ? 1.0 : 0.125;
+  q[1] = 0.0;
+  q[2] = 0.0;
+  q[3] = (in ? 1.0 : 0.1) / (A.gamma - 1.0);
+}
+
+__device__ void case_state(const AuxArgs& A, int cid, double x, double y, double t, double q[4]) {
+  if (cid == 0) vortex(A, x, y, t, q); else shock(A, x, y, q);
+}
+
+__global__ void k_lambda(const AuxArgs A, const double* __restrict__ q, long long npts, unsigned long long* lam,
+                         unsigned long long* bad) {
+  __shared__ double sred[32];
+  const double gm1 = A.gamma - 1.0;
+  double m = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < npts; i += (long long)gridDim.x * blockDim.x) {
+    double v[4] = {q[i], q[A.cs + i], q[2 * A.cs + i], q[3 * A.cs + i]};
+    const double s = wave_speed(v, gm1, A.gamma);
+    m = (s <= m) ? m : s;  // NaN propagates
+    if (bad && nonphysical(v, gm1)) atomicMin(bad, (unsigned long long)i);
+  }
+  block_max_to(m, lam, sred);
+}
+
+// clock: [0] t, [1] dt, [2] steps, [3] stepped flag;  lam: [0] accumulator, [1] current
+__global__ void k_dt(double* clk, unsigned long long* lam, double cfl, double hmin, double t_end) {
+  if (clk[3] != 0.0) lam[1] = lam[0];
+  lam[0] = 0ull;
+  const double l = __longlong_as_double((long long)lam[1]);
+  double dt = cfl * hmin / l;
+  const double rem = t_end - clk[0];
+  if (!(rem > 0.0)) dt = 0.0;
+  else if (dt > rem) dt = rem;
+  clk[1] = dt;
+  if (dt != 0.0) {
+    clk[0] = clk[0] + dt;
+    clk[2] += 1.0;
+    clk[3] = 1.0;
+  } else {
+    clk[3] = 0.0;
+  }
+}
+
+__global__ void k_init(const AuxArgs A, Nodes nd, GL8v g8, int cid, double* q) {
+  const int n = nd.n, np = (A.method == 0) ? 1 : n * n;
+  const long long npts = (long long)A.nx * A.nrows * np;
+  const double dx = (A.xmax - A.xmin) / A.nx, dy = (A.ymax - A.ymin) / A.ny_global;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < npts; t += (long long)gridDim.x * blockDim.x) {
+    const long long m = t / np;
+    const int p = (int)(t % np);
+    const int i = (int)(m % A.nx), j = (int)(m / A.nx) + A.row0;
+    const double xc = A.xmin + (i + 0.5) * dx, yc = A.ymin + (j + 0.5) * dy;
+    double qq[4];
+    if (A.method == 0) {
+      double acc[4] = {0, 0, 0, 0};
+      for (int b = 0; b < 8; ++b)
+        for (int a = 0; a < 8; ++a) {
+          double v[4];
+          case_state(A, cid, xc + 0.5 * dx * g8.x[a], yc + 0.5 * dy * g8.x[b], 0.0, v);
+          const double w = 0.25 * g8.w[a] * g8.w[b];
+          for (int c = 0; c < 4; ++c) acc[c] += w * v[c];
+        }
+      for (int c = 0; c < 4; ++c) qq[c] = acc[c];
+    } else {
+      case_state(A, cid, xc + 0.5 * dx * nd.xi[p % n], yc + 0.5 * dy * nd.xi[p / n], 0.0, qq);
+    }
+    for (int c = 0; c < 4; ++c) q[c * A.cs + t] = qq[c];
+  }
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// deterministic per-block partials: {sum w|d|, sum w d^2, max |d|}
+__global__ void k_err(const AuxArgs A, Nodes nd, GL8v g8, const double* __restrict__ q, int var,
+                      const double* clk, double* part) {
+  __shared__ double s1[32], s2[32], s3[32];
+  const int n = nd.n, np = (A.method == 0) ? 1 : n * n;
+  const long long npts = (long long)A.nx * A.nrows * np;
+  const double dx = (A.xmax - A.xmin) / A.nx, dy = (A.ymax - A.ymin) / A.ny_global;
+  const double t = clk[0];
+  double a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  for (long long tt = blockIdx.x * (long long)blockDim.x + threadIdx.x; tt < npts; tt += (long long)gridDim.x * blockDim.x) {
+    const long long m = tt / np;
+    const int p = (int)(tt % np);
+    const int i = (int)(m % A.nx), j = (int)(m / A.nx) + A.row0;
+    const double xc = A.xmin + (i + 0.5) * dx, yc = A.ymin + (j + 0.5) * dy;
+    double ex, w;
+    if (A.method == 0) {
+      double acc = 0.0;
+      for (int b = 0; b < 8; ++b)
+        for (int a = 0; a < 8; ++a) {
+          double v[4];
+          vortex(A, xc + 0.5 * dx * g8.x[a], yc + 0.5 * dy * g8.x[b], t, v);
+          acc += 0.25 * g8.w[a] * g8.w[b] * v[var];
+        }
+      ex = acc;
+      w = 1.0;
+    } else {
+      double v[4];
+      vortex(A, xc + 0.5 * dx * nd.xi[p % n], yc + 0.5 * dy * nd.xi[p / n], t, v);
+      ex = v[var];
+      w = 0.25 * nd.w[p % n] * nd.w[p / n];
+    }
+    const double d = q[var * A.cs + tt] - ex;
+    a1 += w * fabs(d);
+    a2 += w * d * d;
+    a3 = fmax(a3, fabs(d));
+  }
+  a1 = warp_sum(a1);
+  a2 = warp_sum(a2);
+  a3 = warp_max(a3);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) { s1[wid] = a1; s2[wid] = a2; s3[wid] = a3; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b1 = 0, b2 = 0, b3 = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { b1 += s1[w]; b2 += s2[w]; b3 = fmax(b3, s3[w]); }
+    part[3 * blockIdx.x] = b1;
+    part[3 * blockIdx.x + 1] = b2;
+    part[3 * blockIdx.x + 2] = b3;
+  }
+}
+
+__global__ void k_err_final(const double* part, int nb, double* out3) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double b1 = 0, b2 = 0, b3 = 0;
+  for (int i = 0; i < nb; ++i) { b1 += part[3 * i]; b2 += part[3 * i + 1]; b3 = fmax(b3, part[3 * i + 2]); }
+  out3[0] = b1;
+  out3[1] = b2;
+  out3[2] = b3;
+}
+
+__global__ void k_avg(const AuxArgs A, Nodes nd, const double* __restrict__ q, double* qbar) {
+  const int n = nd.n, np = n * n;
+  const long long ne = (long long)A.nx * A.nrows;
+  for (long long m = blockIdx.x * (long long)blockDim.x + threadIdx.x; m < ne; m += (long long)gridDim.x * blockDim.x) {
+    for (int c = 0; c < 4; ++c) {
+      double s = 0.0;
+      for (int b = 0; b < n; ++b)
+        for (int a = 0; a < n; ++a) s += nd.w[a] * nd.w[b] * q[c * A.cs + m * np + b * n + a];
+      qbar[c * ne + m] = 0.25 * s;
+    }
+  }
+}
+
+// one thread per element: detect on density at every edge point, limit if marked
+__global__ void k_limit(const AuxArgs A, Nodes nd, double* q, const double* __restrict__ qbar,
+                        const double* qbar_lo, const double* qbar_hi, long long gcs, int bcx, double eps,
+                        long long* dec) {
+  const int n = nd.n, np = n * n;
+  const long long ne = (long long)A.nx * A.nrows;
+  const double dx = (A.xmax - A.xmin) / A.nx, dy = (A.ymax - A.ymin) / A.ny_global;
+  for (long long m = blockIdx.x * (long long)blockDim.x + threadIdx.x; m < ne; m += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(m % A.nx), j = (int)(m / A.nx);
+    long long iw = i - 1, ie = i + 1;
+    bool hw = true, he = true;
+    if (iw < 0) { if (bcx) hw = false; else iw += A.nx; }
+    if (ie >= A.nx) { if (bcx) he = false; else ie -= A.nx; }
+    auto nb = [&](int c, int dir) -> double {  // neighbour averages (own if transmissive boundary)
+      const double own = qbar[c * ne + m];
+      if (dir == 0) return hw ? qbar[c * ne + (long long)j * A.nx + iw] : own;
+      if (dir == 1) return he ? qbar[c * ne + (long long)j * A.nx + ie] : own;
+      if (dir == 2) {
+        if (j > 0) return qbar[c * ne + (long long)(j - 1) * A.nx + i];
+        return qbar_lo ? qbar_lo[c * gcs + i] : own;
+      }
+      if (j < A.nrows - 1) return qbar[c * ne + (long long)(j + 1) * A.nx + i];
+      return qbar_hi ? qbar_hi[c * gcs + i] : own;
+    };
+    const double qb = qbar[m];
+    const double rW = nb(0, 0), rE = nb(0, 1), rS = nb(0, 2), rN = nb(0, 3);
+    const double* Q0 = q + m * np;
+    bool trip = false;
+    for (int s = 0; s < 4 && !trip; ++s)
+      for (int t = 0; t < n; ++t) {
+        const double* e = (s == 0 || s == 2) ? nd.eL : nd.eR;
+        double ql = 0.0;
+        for (int l = 0; l < n; ++l) ql += e[l] * Q0[s <= 1 ? t * n + l : l * n + t];
+        const double qp = s <= 1 ? rE : rN, qm = s <= 1 ? rW : rS;
+        const double qe = (s == 1 || s == 3) ? qb + minmod3(ql - qb, qp - qb, qb - qm)
+                                             : qb - minmod3(qb - ql, qp - qb, qb - qm);
+        if (fabs(ql - qe) > eps) { trip = true; break; }
+      }
+    if (!trip) continue;
+    if (dec) atomicAdd((unsigned long long*)&dec[0], 1ull);
+    for (int c = 0; c < 4; ++c) {
+      const double qc = qbar[c * ne + m];
+      const double sx = minmod2((nb(c, 1) - qc) / dx, (qc - nb(c, 0)) / dx, nullptr);
+      const double sy = minmod2((nb(c, 3) - qc) / dy, (qc - nb(c, 2)) / dy, nullptr);
+      for (int b = 0; b < n; ++b)
+        for (int a = 0; a < n; ++a)
+          q[c * A.cs + m * np + b * n + a] = qc + (0.5 * dx) * nd.xi[a] * sx + (0.5 * dy) * nd.xi[b] * sy;
+    }
+  }
+}
+}  // namespace
+
+void launch_lambda(const AuxArgs& a, const double* q, unsigned long long* lam, unsigned long long* bad,
+                   cudaStream_t s) {
+  const long long npts = a.cs;
+  k_lambda<<<grid_for(npts, 256), 256, 0, s>>>(a, q, npts, lam, bad);
+}
+
+void launch_dt(double* clock, unsigned long long* lam, double cfl, double hmin, double t_end, cudaStream_t s) {
+  k_dt<<<1, 1, 0, s>>>(clock, lam, cfl, hmin, t_end);
+}
+
+void launch_init_case(const AuxArgs& a, int case_id, double* q, cudaStream_t s) {
+  k_init<<<grid_for(a.cs, 256), 256, 0, s>>>(a, nodes_for(a.method, a.k), gl8(), case_id, q);
+}
+
+int launch_error_partials(const AuxArgs& a, const double* q, int var, const double* clock, double* part,
+                          int max_blocks, cudaStream_t s) {
+  int nb = grid_for(a.cs, 256);
+  if (nb > max_blocks) nb = max_blocks;
+  k_err<<<nb, 256, 0, s>>>(a, nodes_for(a.method, a.k), gl8(), q, var, clock, part);
+  return nb;
+}
+
+void launch_error_final(const double* part, int nb, double* out3, cudaStream_t s) {
+  k_err_final<<<1, 32, 0, s>>>(part, nb, out3);
+}
+
+void launch_averages(const AuxArgs& a, const double* q, double* qbar, cudaStream_t s) {
+  const long long ne = (long long)a.nx * a.nrows;
+  k_avg<<<grid_for(ne, 128), 128, 0, s>>>(a, nodes_for(a.method, a.k), q, qbar);
+}
+
+void launch_limit(const AuxArgs& a, double* q, const double* qbar, const double* qbar_lo, const double* qbar_hi,
+                  long long qbar_gcs, int bcx, double eps, long long* dec, cudaStream_t s) {
+  const long long ne = (long long)a.nx * a.nrows;
+  k_limit<<<grid_for(ne, 128), 128, 0, s>>>(a, nodes_for(a.method, a.k), q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx,
+                                            eps, dec);
+}
+
+}  // namespace h2d

@@ -1,0 +1,135 @@
+// common.cuh -- device-side physics of the 2-D Euler equations (Eqs. (1)-(5),
+// P:120-146) and the Rusanov flux for the sm_100a kernels.
+// Own implementation; shares nothing with oracle/.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "internal.h"
+
+namespace h2d {
+
+struct Prim {
+  double ri, u, v, p;  // 1/rho, velocities, pressure
+};
+
+// one reciprocal per point (the only fp64 division of a flux evaluation)
+__device__ __forceinline__ Prim prims(const double q[4], double gm1) {
+  Prim w;
+  w.ri = 1.0 / q[0];
+  w.u = q[1] * w.ri;
+  w.v = q[2] * w.ri;
+  w.p = gm1 * (q[3] - 0.5 * (q[1] * w.u + q[2] * w.v));
+  return w;
+}
+
+// Eq. (4): f (DIR 0) or g (DIR 1)
+template <int DIR>
+__device__ __forceinline__ void flux(const double q[4], const Prim& w, double f[4]) {
+  if (DIR == 0) {
+    f[0] = q[1];
+    f[1] = q[1] * w.u + w.p;
+    f[2] = q[1] * w.v;
+    f[3] = w.u * (q[3] + w.p);
+  } else {
+    f[0] = q[2];
+    f[1] = q[2] * w.u;
+    f[2] = q[2] * w.v + w.p;
+    f[3] = w.v * (q[3] + w.p);
+  }
+}
+
+// Rusanov flux along axis DIR for (west|south, east|north) states; also returns
+// the two physical fluxes (the CPR/NDG correction needs F^ - f(own trace)).
+template <int DIR>
+__device__ __forceinline__ void rusanov(const double qL[4], const double qR[4], double gm1, double gam,
+                                        double F[4], double fL[4], double fR[4]) {
+  Prim wl = prims(qL, gm1), wr = prims(qR, gm1);
+  flux<DIR>(qL, wl, fL);
+  flux<DIR>(qR, wr, fR);
+  double sl = fabs(DIR == 0 ? wl.u : wl.v) + sqrt(gam * wl.p * wl.ri);
+  double sr = fabs(DIR == 0 ? wr.u : wr.v) + sqrt(gam * wr.p * wr.ri);
+  double lam = fmax(sl, sr);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) F[c] = 0.5 * (fL[c] + fR[c]) - 0.5 * lam * (qR[c] - qL[c]);
+}
+
+// Flux-Jacobian action A(q).d (DIR 0) or B(q).d (DIR 1): the chain rule of the
+// CPR divergence.
+template <int DIR>
+__device__ __forceinline__ void jac(const double q[4], const Prim& w, double gm1, double gam, const double d[4],
+                                    double o[4]) {
+  const double u = w.u, v = w.v;
+  const double phi = 0.5 * gm1 * (u * u + v * v);
+  const double H = (q[3] + w.p) * w.ri;
+  if (DIR == 0) {
+    o[0] = d[1];
+    o[1] = (phi - u * u) * d[0] + (3.0 - gam) * u * d[1] - gm1 * v * d[2] + gm1 * d[3];
+    o[2] = -u * v * d[0] + v * d[1] + u * d[2];
+    o[3] = u * (phi - H) * d[0] + (H - gm1 * u * u) * d[1] - gm1 * u * v * d[2] + gam * u * d[3];
+  } else {
+    o[0] = d[2];
+    o[1] = -u * v * d[0] + v * d[1] + u * d[2];
+    o[2] = (phi - v * v) * d[0] - gm1 * u * d[1] + (3.0 - gam) * v * d[2] + gm1 * d[3];
+    o[3] = v * (phi - H) * d[0] - gm1 * u * v * d[1] + (H - gm1 * v * v) * d[2] + gam * v * d[3];
+  }
+}
+
+// max(|u|,|v|) + c  (2-D reading of Eq. (36))
+__device__ __forceinline__ double wave_speed(const double q[4], double gm1, double gam) {
+  Prim w = prims(q, gm1);
+  return fmax(fabs(w.u), fabs(w.v)) + sqrt(gam * w.p * w.ri);
+}
+
+__device__ __forceinline__ bool nonphysical(const double q[4], double gm1) {
+  Prim w = prims(q, gm1);
+  bool fin = isfinite(q[0]) && isfinite(q[1]) && isfinite(q[2]) && isfinite(q[3]);
+  return !fin || !(q[0] > 0.0) || !(w.p > 0.0);
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// block-wide max of a non-negative value -> one atomicMax on the bit pattern
+// (IEEE order of non-negative doubles == unsigned order of their bits; NaN wins)
+__device__ __forceinline__ void block_max_to(double v, unsigned long long* dst, double* s_red) {
+  v = warp_max(v);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) s_red[wid] = v;
+  __syncthreads();
+  if (wid == 0) {
+    const int nw = (blockDim.x + 31) >> 5;
+    double x = lane < nw ? s_red[lane] : 0.0;
+    x = warp_max(x);
+    if (lane == 0) atomicMax(dst, (unsigned long long)__double_as_longlong(x));
+  }
+}
+
+__device__ __forceinline__ void count_dec(long long* dec, int which) {
+  if (dec) atomicAdd((unsigned long long*)&dec[which], 1ull);
+}
+
+// minmod of two arguments (ties return the first argument, zero if the
+// signs differ or either is zero), optionally recording the branch taken.
+__device__ __forceinline__ double minmod2(double a, double b, long long* dec) {
+  double r = 0.0;
+  int which = 1;
+  if (a > 0.0 && b > 0.0) {
+    if (a <= b) { r = a; which = 2; } else { r = b; which = 3; }
+  } else if (a < 0.0 && b < 0.0) {
+    if (a >= b) { r = a; which = 2; } else { r = b; which = 3; }
+  }
+  if (dec) count_dec(dec, which);
+  return r;
+}
+
+__device__ __forceinline__ double minmod3(double a, double b, double c) {
+  if (a > 0.0 && b > 0.0 && c > 0.0) return fmin(a, fmin(b, c));
+  if (a < 0.0 && b < 0.0 && c < 0.0) return fmax(a, fmax(b, c));
+  return 0.0;
+}
+
+}  // namespace h2d

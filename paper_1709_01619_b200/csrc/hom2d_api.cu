@@ -1,0 +1,538 @@
+// hom2d_api.cu -- the C ABI of include/hom2d.h: handle, workspace carve-up,
+// strip partition, halo exchange (NCCL over NVLink when nranks > 1), and the
+// SSP-RK3 driver loop that keeps t and dt on the device.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include <nccl.h>
+
+#include "../../include/hom2d.h"
+#include "internal.h"
+
+using namespace h2d;
+
+struct hom2d {
+  hom2d_config cfg;
+  int rank = 0, nranks = 1, device = 0;
+  cudaStream_t stream = nullptr;
+  ncclComm_t comm = nullptr;
+  int row0 = 0, nrows = 0, np = 1, G = 1;  // G ghost rows (HO 1, FV 2)
+  long long nloc = 0;                      // values per component of the local strip
+  double *Qn = nullptr, *Q1 = nullptr, *Q2 = nullptr;
+  double* clock = nullptr;                 // [t, dt, steps, stepped]
+  unsigned long long* lam = nullptr;       // [acc, cur]
+  unsigned long long* bad = nullptr;
+  long long* dec = nullptr;
+  double* part = nullptr;                  // error partials
+  int max_part = 0;
+  double* err3 = nullptr;
+  double* qbar = nullptr;                  // HO limiter averages [4][nx*nrows]
+  double *glo = nullptr, *ghi = nullptr;   // received ghost rows [4][G*nx*np]
+  double *qblo = nullptr, *qbhi = nullptr; // received ghost average rows [4][nx]
+  double* t_host = nullptr;
+  bool poisoned = false;
+  long long launches = 0;
+  std::vector<cudaEvent_t> ev;             // stage-kernel timing: pairs (start, stop)
+  int ev_used = 0;
+  char msg[512] = {0};
+};
+
+namespace {
+
+hom2d_status fail(hom2d* h, hom2d_status st, const char* fmt, ...) {
+  if (h) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(h->msg, sizeof(h->msg), fmt, ap);
+    va_end(ap);
+    if (st == HOM2D_ERR_CUDA || st == HOM2D_ERR_NCCL) h->poisoned = true;
+  }
+  return st;
+}
+
+#define CU(h, x)                                                                        \
+  do {                                                                                  \
+    cudaError_t e_ = (x);                                                               \
+    if (e_ != cudaSuccess) return fail(h, HOM2D_ERR_CUDA, "%s: %s", #x, cudaGetErrorString(e_)); \
+  } while (0)
+#define NC(h, x)                                                                        \
+  do {                                                                                  \
+    ncclResult_t r_ = (x);                                                              \
+    if (r_ != ncclSuccess) return fail(h, HOM2D_ERR_NCCL, "%s: %s", #x, ncclGetErrorString(r_)); \
+  } while (0)
+#define GUARD(h)                                                     \
+  do {                                                               \
+    if (!(h)) return HOM2D_ERR_ARG;                                  \
+    if ((h)->poisoned) return HOM2D_ERR_STATE;                       \
+  } while (0)
+
+int points_per_elem(const hom2d_config& c) { return c.method == HOM2D_FV ? 1 : (c.k + 1) * (c.k + 1); }
+
+hom2d_status check_cfg(const hom2d_config* c, int nranks) {
+  if (!c) return HOM2D_ERR_ARG;
+  if (c->method < 0 || c->method > 4 || (c->bc != 0 && c->bc != 1)) return HOM2D_ERR_ARG;
+  if (c->method == HOM2D_FV ? (c->k < 1 || c->k > 2) : (c->k < 1 || c->k > 4)) return HOM2D_ERR_ORDER;
+  if (c->nx < 2 || c->ny < 2 || !(c->xmax > c->xmin) || !(c->ymax > c->ymin)) return HOM2D_ERR_MESH;
+  if (nranks < 1 || c->ny % nranks != 0) return HOM2D_ERR_MESH;
+  const int G = c->method == HOM2D_FV ? 2 : 1;
+  if (c->ny / nranks < G) return HOM2D_ERR_MESH;
+  if (!(c->gamma > 1.0) || !(c->cfl > 0.0)) return HOM2D_ERR_ARG;
+  return HOM2D_OK;
+}
+
+struct Carve {
+  char* base;
+  size_t off = 0;
+  template <class T>
+  T* take(size_t count) {
+    off = (off + 255) & ~size_t(255);
+    T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+    off += count * sizeof(T);
+    return p;
+  }
+};
+
+// lay out the workspace; base == nullptr only measures
+size_t carve(hom2d* h, const hom2d_config& c, int nranks, char* base) {
+  Carve cv{base};
+  const int np = points_per_elem(c);
+  const int G = c.method == HOM2D_FV ? 2 : 1;
+  const long long nrows = c.ny / nranks;
+  const long long nloc = (long long)c.nx * nrows * np;
+  const int max_part = 148 * 16;
+  double* Qn = cv.take<double>(4 * nloc);
+  double* Q1 = cv.take<double>(4 * nloc);
+  double* Q2 = cv.take<double>(4 * nloc);
+  double* clk = cv.take<double>(8);
+  auto* lam = cv.take<unsigned long long>(4);
+  auto* bad = cv.take<unsigned long long>(2);
+  auto* dec = cv.take<long long>(4);
+  double* part = cv.take<double>(3 * max_part);
+  double* err3 = cv.take<double>(4);
+  double* qbar = (c.method != HOM2D_FV) ? cv.take<double>(4 * (size_t)c.nx * nrows) : nullptr;
+  double *glo = nullptr, *ghi = nullptr, *qblo = nullptr, *qbhi = nullptr;
+  if (nranks > 1) {
+    glo = cv.take<double>(4 * (size_t)G * c.nx * np);
+    ghi = cv.take<double>(4 * (size_t)G * c.nx * np);
+    if (c.method != HOM2D_FV) {
+      qblo = cv.take<double>(4 * (size_t)c.nx);
+      qbhi = cv.take<double>(4 * (size_t)c.nx);
+    }
+  }
+  if (h && base) {
+    h->Qn = Qn; h->Q1 = Q1; h->Q2 = Q2; h->clock = clk; h->lam = lam; h->bad = bad; h->dec = dec;
+    h->part = part; h->max_part = max_part; h->err3 = err3; h->qbar = qbar;
+    h->glo = glo; h->ghi = ghi; h->qblo = qblo; h->qbhi = qbhi;
+  }
+  return cv.off + 256;
+}
+
+AuxArgs aux(const hom2d* h) {
+  AuxArgs a;
+  a.method = h->cfg.method; a.k = h->cfg.k; a.nx = h->cfg.nx; a.nrows = h->nrows; a.row0 = h->row0;
+  a.ny_global = h->cfg.ny; a.xmin = h->cfg.xmin; a.xmax = h->cfg.xmax; a.ymin = h->cfg.ymin;
+  a.ymax = h->cfg.ymax; a.gamma = h->cfg.gamma; a.cs = h->nloc;
+  return a;
+}
+
+bool has_lo(const hom2d* h) { return h->cfg.bc == HOM2D_PERIODIC || h->rank > 0; }
+bool has_hi(const hom2d* h) { return h->cfg.bc == HOM2D_PERIODIC || h->rank < h->nranks - 1; }
+
+// Exchange G boundary rows of the stage input X with the strip neighbours and
+// return the ghost pointers the stage kernel reads (y-strip partition, P:L6).
+hom2d_status exchange(hom2d* h, const double* X, long long comp_stride, long long row_vals, const double** lo,
+                      const double** hi, long long* gcs, double* rlo, double* rhi, int G) {
+  const int R = h->nranks;
+  if (R == 1) {
+    *gcs = comp_stride;
+    *lo = (h->cfg.bc == HOM2D_PERIODIC) ? X + (long long)(h->nrows - G) * row_vals : nullptr;
+    *hi = (h->cfg.bc == HOM2D_PERIODIC) ? X : nullptr;
+    return HOM2D_OK;
+  }
+  const long long cnt = (long long)G * row_vals;
+  const int prev = (h->rank + R - 1) % R, next = (h->rank + 1) % R;
+  const bool lo_ok = has_lo(h), hi_ok = has_hi(h);
+  NC(h, ncclGroupStart());
+  for (int c = 0; c < 4; ++c) {
+    const double* first = X + c * comp_stride;
+    const double* last = X + c * comp_stride + (long long)(h->nrows - G) * row_vals;
+    if (lo_ok) {
+      NC(h, ncclSend(first, cnt, ncclDouble, prev, h->comm, h->stream));
+      NC(h, ncclRecv(rlo + c * cnt, cnt, ncclDouble, prev, h->comm, h->stream));
+    }
+    if (hi_ok) {
+      NC(h, ncclSend(last, cnt, ncclDouble, next, h->comm, h->stream));
+      NC(h, ncclRecv(rhi + c * cnt, cnt, ncclDouble, next, h->comm, h->stream));
+    }
+  }
+  NC(h, ncclGroupEnd());
+  *gcs = cnt;
+  *lo = lo_ok ? rlo : nullptr;
+  *hi = hi_ok ? rhi : nullptr;
+  return HOM2D_OK;
+}
+
+hom2d_status run_stage(hom2d* h, const double* q, const double* q0, double* out, double a0, double a1, double b,
+                       const double* dt, unsigned long long* lam, unsigned long long* bad) {
+  StageArgs s{};
+  const long long row_vals = (long long)h->cfg.nx * h->np;
+  hom2d_status st = exchange(h, q, h->nloc, row_vals, &s.ghost_lo, &s.ghost_hi, &s.gcs, h->glo, h->ghi, h->G);
+  if (st) return st;
+  s.q = q; s.q0 = q0; s.out = out; s.nx = h->cfg.nx; s.nrows = h->nrows; s.cs = h->nloc;
+  s.bcx = h->cfg.bc;
+  const double dx = (h->cfg.xmax - h->cfg.xmin) / h->cfg.nx, dy = (h->cfg.ymax - h->cfg.ymin) / h->cfg.ny;
+  if (h->cfg.method == HOM2D_FV) { s.rdx2 = 1.0 / dx; s.rdy2 = 1.0 / dy; }
+  else { s.rdx2 = 2.0 / dx; s.rdy2 = 2.0 / dy; }
+  s.a0 = a0; s.a1 = a1; s.bcoef = b; s.dt = dt; s.gamma = h->cfg.gamma;
+  s.lam = lam; s.bad = bad;
+  s.dec = h->cfg.record_decisions ? h->dec : nullptr;
+  int e;
+  const bool timed = 2 * (h->ev_used + 1) <= (int)h->ev.size();
+  if (timed) cudaEventRecord(h->ev[2 * h->ev_used], h->stream);
+  if (h->cfg.method == HOM2D_FV) {
+    e = launch_fv_stage(h->cfg.k, s, h->stream);
+  } else {
+    int method = h->cfg.method;
+    if (method == HOM2D_CPR && !h->cfg.cpr_chain_rule) method = HOM2D_NDG;  // flux-differentiation CPR == NDG
+    e = launch_ho_stage(method, h->cfg.k, s, h->stream);
+  }
+  if (timed) cudaEventRecord(h->ev[2 * h->ev_used++ + 1], h->stream);
+  h->launches++;
+  if (e) return fail(h, HOM2D_ERR_CUDA, "stage kernel launch: %s", cudaGetErrorString((cudaError_t)e));
+  return HOM2D_OK;
+}
+
+// HO limiter on X in place: averages, (exchange average rows), detect + limit
+hom2d_status run_limiter(hom2d* h, double* X) {
+  AuxArgs A = aux(h);
+  launch_averages(A, X, h->qbar, h->stream);
+  const long long ne = (long long)h->cfg.nx * h->nrows;
+  const double *lo, *hi;
+  long long gcs;
+  hom2d_status st = exchange(h, h->qbar, ne, h->cfg.nx, &lo, &hi, &gcs, h->qblo, h->qbhi, 1);
+  if (st) return st;
+  launch_limit(A, X, h->qbar, lo, hi, gcs, h->cfg.bc, h->cfg.limiter_eps,
+               h->cfg.record_decisions ? h->dec : nullptr, h->stream);
+  h->launches += 2;
+  CU(h, cudaPeekAtLastError());
+  return HOM2D_OK;
+}
+
+hom2d_status allreduce_max_lam(hom2d* h) {
+  if (h->nranks > 1) NC(h, ncclAllReduce(h->lam, h->lam, 1, ncclUint64, ncclMax, h->comm, h->stream));
+  return HOM2D_OK;
+}
+
+// wave-speed max of the current state -> lam[0]; mark it "fresh" for k_dt
+hom2d_status refresh_lambda(hom2d* h) {
+  CU(h, cudaMemsetAsync(h->lam, 0, sizeof(unsigned long long), h->stream));
+  launch_lambda(aux(h), h->Qn, h->lam, nullptr, h->stream);
+  h->launches++;
+  CU(h, cudaPeekAtLastError());
+  hom2d_status st = allreduce_max_lam(h);
+  if (st) return st;
+  const double one = 1.0;
+  CU(h, cudaMemcpyAsync(h->clock + 3, &one, sizeof(double), cudaMemcpyHostToDevice, h->stream));
+  return HOM2D_OK;
+}
+
+hom2d_status reset_clock(hom2d* h, double t0) {
+  double c[4] = {t0, 0.0, 0.0, 0.0};
+  CU(h, cudaMemcpyAsync(h->clock, c, sizeof(c), cudaMemcpyHostToDevice, h->stream));
+  CU(h, cudaMemsetAsync(h->dec, 0, 4 * sizeof(long long), h->stream));
+  CU(h, cudaMemsetAsync(h->bad, 0xff, sizeof(unsigned long long), h->stream));
+  CU(h, cudaStreamSynchronize(h->stream));
+  return HOM2D_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+hom2d_status hom2d_workspace_bytes(const hom2d_config* cfg, const hom2d_dist* dist, size_t* bytes) {
+  const int R = dist ? dist->nranks : 1;
+  hom2d_status st = check_cfg(cfg, R);
+  if (st) return st;
+  if (!bytes) return HOM2D_ERR_ARG;
+  *bytes = carve(nullptr, *cfg, R, nullptr);
+  return HOM2D_OK;
+}
+
+hom2d_status hom2d_nccl_unique_id(void* out128) {
+  if (!out128) return HOM2D_ERR_ARG;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return HOM2D_ERR_NCCL;
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  memcpy(out128, &id, 128);
+  return HOM2D_OK;
+}
+
+hom2d_status hom2d_create(const hom2d_config* cfg, const hom2d_dist* dist, void* workspace, size_t ws_bytes,
+                          hom2d** out) {
+  if (!out) return HOM2D_ERR_ARG;
+  *out = nullptr;
+  const int R = dist ? dist->nranks : 1;
+  hom2d_status st = check_cfg(cfg, R);
+  if (st) return st;
+  if (dist && (dist->rank < 0 || dist->rank >= R)) return HOM2D_ERR_ARG;
+  if (!workspace || ((uintptr_t)workspace & 255)) return HOM2D_ERR_ARG;
+  if (ws_bytes < carve(nullptr, *cfg, R, nullptr)) return HOM2D_ERR_NOMEM;
+  hom2d* h = new (std::nothrow) hom2d();
+  if (!h) return HOM2D_ERR_NOMEM;
+  h->cfg = *cfg;
+  h->rank = dist ? dist->rank : 0;
+  h->nranks = R;
+  if (dist) h->device = dist->device; else cudaGetDevice(&h->device);
+  h->stream = dist ? (cudaStream_t)dist->cuda_stream : nullptr;
+  h->np = points_per_elem(*cfg);
+  h->G = cfg->method == HOM2D_FV ? 2 : 1;
+  h->nrows = cfg->ny / R;
+  h->row0 = h->rank * h->nrows;
+  h->nloc = (long long)cfg->nx * h->nrows * h->np;
+  cudaError_t ce = cudaSetDevice(h->device);
+  if (ce != cudaSuccess) { delete h; return HOM2D_ERR_CUDA; }
+  carve(h, *cfg, R, (char*)workspace);
+  if (cudaMallocHost(&h->t_host, 8 * sizeof(double)) != cudaSuccess) { delete h; return HOM2D_ERR_CUDA; }
+  if (R > 1) {
+    if (!dist->nccl_id) { cudaFreeHost(h->t_host); delete h; return HOM2D_ERR_ARG; }
+    ncclUniqueId id;
+    memcpy(&id, dist->nccl_id, sizeof(id));
+    if (ncclCommInitRank(&h->comm, R, id, h->rank) != ncclSuccess) { cudaFreeHost(h->t_host); delete h; return HOM2D_ERR_NCCL; }
+  }
+  cudaMemsetAsync(h->lam, 0, 4 * sizeof(unsigned long long), h->stream);
+  if (reset_clock(h, 0.0)) { hom2d_destroy(h); return HOM2D_ERR_CUDA; }
+  *out = h;
+  return HOM2D_OK;
+}
+
+hom2d_status hom2d_local_extent(const hom2d* h, int32_t* row0, int32_t* nrows, int64_t* n_values) {
+  if (!h) return HOM2D_ERR_ARG;
+  if (row0) *row0 = h->row0;
+  if (nrows) *nrows = h->nrows;
+  if (n_values) *n_values = 4 * h->nloc;
+  return HOM2D_OK;
+}
+
+hom2d_status hom2d_set_state(hom2d* h, const double* q, int64_t n_values, int32_t on_device, double t0) {
+  GUARD(h);
+  if (!q || n_values != 4 * h->nloc) return fail(h, HOM2D_ERR_ARG, "set_state: expected %lld values", 4 * h->nloc);
+  CU(h, cudaMemcpyAsync(h->Qn, q, n_values * sizeof(double), on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                        h->stream));
+  hom2d_status st = reset_clock(h, t0);
+  if (st) return st;
+  st = refresh_lambda(h);
+  if (st) return st;
+  CU(h, cudaStreamSynchronize(h->stream));
+  return HOM2D_OK;
+}
+
+hom2d_status hom2d_get_state(hom2d* h, double* q, int64_t n_values, int32_t on_device) {
+  GUARD(h);
+  if (!q || n_values != 4 * h->nloc) return fail(h, HOM2D_ERR_ARG, "get_state: expected %lld values", 4 * h->nloc);
+  CU(h, cudaMemcpyAsync(q, h->Qn, n_values * sizeof(double), on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                        h->stream));
+  CU(h, cudaStreamSynchronize(h->stream));
+  return HOM2D_OK;
+}
+
+hom2d_status hom2d_init_case(hom2d* h, int32_t case_id) {
+  GUARD(h);
+  if (case_id != HOM2D_CASE_VORTEX && case_id != HOM2D_CASE_SHOCK) return fail(h, HOM2D_ERR_ARG, "unknown case %d", case_id);
+  launch_init_case(aux(h), case_id, h->Qn, h->stream);
+  h->launches++;
+  CU(h, cudaPeekAtLastError());
+  if (h->cfg.limiter && h->cfg.method != HOM2D_FV) {
+    hom2d_status st = run_limiter(h, h->Qn);
+    if (st) return st;
+  }
+  hom2d_status st = reset_clock(h, 0.0);
+  if (st) return st;
+  st = refresh_lambda(h);
+  if (st) return st;
+  CU(h, cudaStreamSynchronize(h->stream));
+  return HOM2D_OK;
+}
+
+hom2d_status hom2d_residual(hom2d* h, const double* q_dev, double* r_dev) {
+  GUARD(h);
+  if (!q_dev || !r_dev) return fail(h, HOM2D_ERR_ARG, "residual: null pointer");
+  hom2d_status st = run_stage(h, q_dev, nullptr, r_dev, 0.0, 0.0, 1.0, nullptr, nullptr, nullptr);
+  if (st) return st;
+  CU(h, cudaStreamSynchronize(h->stream));
+  return HOM2D_OK;
+}
+
+hom2d_status hom2d_limit(hom2d* h) {
+  GUARD(h);
+  if (h->cfg.method == HOM2D_FV) return fail(h, HOM2D_ERR_ARG, "limit: HO methods only");
+  hom2d_status st = run_limiter(h, h->Qn);
+  if (st) return st;
+  st = refresh_lambda(h);
+  if (st) return st;
+  CU(h, cudaStreamSynchronize(h->stream));
+  return HOM2D_OK;
+}
+
+hom2d_status hom2d_compute_dt(hom2d* h, double* dt) {
+  GUARD(h);
+  if (!dt) return HOM2D_ERR_ARG;
+  hom2d_status st = refresh_lambda(h);
+  if (st) return st;
+  unsigned long long bits;
+  CU(h, cudaMemcpyAsync(&bits, h->lam, sizeof(bits), cudaMemcpyDeviceToHost, h->stream));
+  CU(h, cudaStreamSynchronize(h->stream));
+  double l;
+  memcpy(&l, &bits, 8);
+  const double dx = (h->cfg.xmax - h->cfg.xmin) / h->cfg.nx, dy = (h->cfg.ymax - h->cfg.ymin) / h->cfg.ny;
+  *dt = h->cfg.cfl * fmin(dx, dy) / l;
+  return HOM2D_OK;
+}
+
+hom2d_status hom2d_step(hom2d* h, int32_t max_steps, double t_end, double* t_out, int64_t* steps_out) {
+  GUARD(h);
+  if (max_steps < 0) return fail(h, HOM2D_ERR_ARG, "max_steps < 0");
+  const double dx = (h->cfg.xmax - h->cfg.xmin) / h->cfg.nx, dy = (h->cfg.ymax - h->cfg.ymin) / h->cfg.ny;
+  const double hmin = fmin(dx, dy);
+  const bool lim = h->cfg.limiter && h->cfg.method != HOM2D_FV;
+  CU(h, cudaMemcpyAsync(h->t_host, h->clock, 4 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  CU(h, cudaStreamSynchronize(h->stream));
+  const double steps0 = h->t_host[2];
+  int done = 0;
+  hom2d_status st = HOM2D_OK;
+  while (done < max_steps) {
+    const int batch = (max_steps - done) < 64 ? (max_steps - done) : 64;
+    for (int s = 0; s < batch; ++s) {
+      launch_dt(h->clock, h->lam, h->cfg.cfl, hmin, t_end, h->stream);
+      h->launches++;
+      const double* dt = h->clock + 1;
+      // SSP-RK3 (Shu-Osher)
+      if ((st = run_stage(h, h->Qn, nullptr, h->Q1, 0.0, 1.0, 1.0, dt, nullptr, nullptr))) return st;
+      if (lim && (st = run_limiter(h, h->Q1))) return st;
+      if ((st = run_stage(h, h->Q1, h->Qn, h->Q2, 0.75, 0.25, 0.25, dt, nullptr, nullptr))) return st;
+      if (lim && (st = run_limiter(h, h->Q2))) return st;
+      if (!lim) {
+        if ((st = run_stage(h, h->Q2, h->Qn, h->Qn, 1.0 / 3.0, 2.0 / 3.0, 2.0 / 3.0, dt, h->lam, h->bad))) return st;
+      } else {
+        if ((st = run_stage(h, h->Q2, h->Qn, h->Qn, 1.0 / 3.0, 2.0 / 3.0, 2.0 / 3.0, dt, nullptr, nullptr))) return st;
+        if ((st = run_limiter(h, h->Qn))) return st;
+        launch_lambda(aux(h), h->Qn, h->lam, h->bad, h->stream);  // dt of the limited state
+        h->launches++;
+      }
+      if ((st = allreduce_max_lam(h))) return st;
+    }
+    done += batch;
+    CU(h, cudaPeekAtLastError());
+    CU(h, cudaMemcpyAsync(h->t_host, h->clock, 4 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    CU(h, cudaMemcpyAsync(h->t_host + 4, h->bad, sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->stream));
+    CU(h, cudaStreamSynchronize(h->stream));
+    unsigned long long badv;
+    memcpy(&badv, h->t_host + 4, 8);
+    if (badv != ~0ull) {
+      if (t_out) *t_out = h->t_host[0];
+      if (steps_out) *steps_out = (int64_t)(h->t_host[2] - steps0);
+      const long long m = (long long)(badv / h->np);
+      return fail(h, HOM2D_ERR_NONPHYSICAL, "non-physical state at element (i=%lld, j=%lld), point %lld, t=%.17g",
+                  m % h->cfg.nx, m / h->cfg.nx + h->row0, (long long)(badv % h->np), h->t_host[0]);
+    }
+    if (!(h->t_host[0] < t_end)) break;
+  }
+  if (t_out) *t_out = h->t_host[0];
+  if (steps_out) *steps_out = (int64_t)(h->t_host[2] - steps0);
+  return HOM2D_OK;
+}
+
+hom2d_status hom2d_error(hom2d* h, int32_t case_id, int32_t var, double* l1, double* l2, double* linf) {
+  GUARD(h);
+  if (case_id != HOM2D_CASE_VORTEX) return fail(h, HOM2D_ERR_ARG, "error: exact solution only for the vortex");
+  if (var < 0 || var > 3) return fail(h, HOM2D_ERR_ARG, "error: var must be 0..3");
+  const int nb = launch_error_partials(aux(h), h->Qn, var, h->clock, h->part, h->max_part, h->stream);
+  launch_error_final(h->part, nb, h->err3, h->stream);
+  h->launches += 2;
+  CU(h, cudaPeekAtLastError());
+  if (h->nranks > 1) {
+    NC(h, ncclAllReduce(h->err3, h->err3, 2, ncclDouble, ncclSum, h->comm, h->stream));
+    NC(h, ncclAllReduce(h->err3 + 2, h->err3 + 2, 1, ncclDouble, ncclMax, h->comm, h->stream));
+  }
+  double r[3];
+  CU(h, cudaMemcpyAsync(r, h->err3, sizeof(r), cudaMemcpyDeviceToHost, h->stream));
+  CU(h, cudaStreamSynchronize(h->stream));
+  const double ne = (double)h->cfg.nx * h->cfg.ny;
+  if (l1) *l1 = r[0] / ne;
+  if (l2) *l2 = sqrt(r[1] / ne);
+  if (linf) *linf = r[2];
+  return HOM2D_OK;
+}
+
+hom2d_status hom2d_time(const hom2d* h, double* t) {
+  if (!h || !t) return HOM2D_ERR_ARG;
+  if (h->poisoned) return HOM2D_ERR_STATE;
+  if (cudaMemcpyAsync(h->t_host, h->clock, sizeof(double), cudaMemcpyDeviceToHost, h->stream) != cudaSuccess)
+    return HOM2D_ERR_CUDA;
+  if (cudaStreamSynchronize(h->stream) != cudaSuccess) return HOM2D_ERR_CUDA;
+  *t = h->t_host[0];
+  return HOM2D_OK;
+}
+
+hom2d_status hom2d_decisions(hom2d* h, int64_t* counts4) {
+  GUARD(h);
+  if (!counts4) return HOM2D_ERR_ARG;
+  CU(h, cudaMemcpyAsync(counts4, h->dec, 4 * sizeof(long long), cudaMemcpyDeviceToHost, h->stream));
+  CU(h, cudaStreamSynchronize(h->stream));
+  if (h->nranks > 1) {
+    // host-side sum over ranks through the device scratch
+    long long* d = h->dec;
+    NC(h, ncclAllReduce(d, h->part, 4, ncclInt64, ncclSum, h->comm, h->stream));
+    CU(h, cudaMemcpyAsync(counts4, h->part, 4 * sizeof(long long), cudaMemcpyDeviceToHost, h->stream));
+    CU(h, cudaStreamSynchronize(h->stream));
+  }
+  return HOM2D_OK;
+}
+
+int64_t hom2d_launch_count(const hom2d* h) { return h ? h->launches : 0; }
+
+hom2d_status hom2d_stage_timing(hom2d* h, int32_t max_launches) {
+  GUARD(h);
+  if (max_launches < 0) return HOM2D_ERR_ARG;
+  CU(h, cudaStreamSynchronize(h->stream));
+  for (cudaEvent_t e : h->ev) cudaEventDestroy(e);
+  h->ev.clear();
+  h->ev_used = 0;
+  for (int i = 0; i < 2 * max_launches; ++i) {
+    cudaEvent_t e;
+    CU(h, cudaEventCreate(&e));
+    h->ev.push_back(e);
+  }
+  return HOM2D_OK;
+}
+
+hom2d_status hom2d_stage_time(hom2d* h, double* total_ms, int64_t* n_launches) {
+  GUARD(h);
+  CU(h, cudaStreamSynchronize(h->stream));
+  double tot = 0.0;
+  for (int i = 0; i < h->ev_used; ++i) {
+    float ms = 0.f;
+    CU(h, cudaEventElapsedTime(&ms, h->ev[2 * i], h->ev[2 * i + 1]));
+    tot += ms;
+  }
+  if (total_ms) *total_ms = tot;
+  if (n_launches) *n_launches = h->ev_used;
+  h->ev_used = 0;
+  return HOM2D_OK;
+}
+
+const char* hom2d_last_error(const hom2d* h) { return h ? h->msg : "null handle"; }
+
+void hom2d_destroy(hom2d* h) {
+  if (!h) return;
+  if (h->stream) cudaStreamSynchronize(h->stream); else cudaDeviceSynchronize();
+  for (cudaEvent_t e : h->ev) cudaEventDestroy(e);
+  if (h->comm) ncclCommDestroy(h->comm);
+  if (h->t_host) cudaFreeHost(h->t_host);
+  delete h;
+}
+
+}  // extern "C"

@@ -1,0 +1,56 @@
+// internal.h -- host-side declarations shared by the API and the kernel files.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace h2d {
+
+// One RK stage (or a bare residual):  out = a0*q0 + a1*q + bcoef*dt*R(q)
+// (SSP-RK3 of P:868 in Shu-Osher form; residual mode: a0 = a1 = 0, bcoef = 1,
+// dt == nullptr).  Arrays are the local strip in the canonical SoA layout.
+struct StageArgs {
+  const double* q;        // stage input (neighbours read from here)
+  const double* q0;       // q^n (pointwise only); may alias out; nullptr if a0 == 0
+  double* out;
+  int nx, nrows;          // local strip: nx element columns, nrows element rows
+  long long cs;           // component stride of q, q0, out (values)
+  // y-neighbour rows beyond the strip (full element/cell rows, canonical layout
+  // with component stride gcs).  nullptr = physical transmissive boundary.
+  const double* ghost_lo; // rows -G..-1  (G = 1 HO, 2 FV)
+  const double* ghost_hi; // rows nrows..nrows+G-1
+  long long gcs;
+  int bcx;                // x boundary: 0 periodic, 1 transmissive
+  double rdx2, rdy2;      // HO: 2/dx, 2/dy (metric of the affine map); FV: 1/dx, 1/dy
+  double a0, a1, bcoef;
+  const double* dt;       // device scalar; nullptr -> 1.0; a stage with *dt == 0 is skipped
+  double gamma;
+  unsigned long long* lam; // optional: atomicMax of max(|u|,|v|)+c of `out` (bits of a double >= 0)
+  unsigned long long* bad; // optional: atomicMin of the first non-physical point index
+  long long* dec;          // optional: decision counters [4]
+};
+
+int launch_ho_stage(int method, int k, const StageArgs& a, cudaStream_t s);
+int launch_fv_stage(int k, const StageArgs& a, cudaStream_t s);
+
+struct AuxArgs {
+  int method, k, nx, nrows, row0, ny_global;
+  double xmin, xmax, ymin, ymax, gamma;
+  long long cs;
+};
+
+// max(|u|,|v|)+c over the state -> atomicMax into lam (bits); optional bad-point check
+void launch_lambda(const AuxArgs& a, const double* q, unsigned long long* lam, unsigned long long* bad,
+                   cudaStream_t s);
+// dt bookkeeping: see aux.cu
+void launch_dt(double* clock, unsigned long long* lam_acc, double cfl, double hmin, double t_end, cudaStream_t s);
+void launch_init_case(const AuxArgs& a, int case_id, double* q, cudaStream_t s);
+// per-block partial sums {sum w|d|, sum w d^2, max|d|} -> part[3*nblocks]; returns nblocks
+int launch_error_partials(const AuxArgs& a, const double* q, int var, const double* clock, double* part,
+                          int max_blocks, cudaStream_t s);
+void launch_error_final(const double* part, int nblocks, double* out3, cudaStream_t s);
+// averages Qbar[4][nx*nrows] and the detect+limit pass (HO)
+void launch_averages(const AuxArgs& a, const double* q, double* qbar, cudaStream_t s);
+void launch_limit(const AuxArgs& a, double* q, const double* qbar, const double* qbar_lo, const double* qbar_hi,
+                  long long qbar_gcs, int bcx, double eps, long long* dec, cudaStream_t s);
+
+}  // namespace h2d

@@ -1,0 +1,90 @@
+"""Host-side checks that need no GPU: the C-ABI library builds for sm_100a, loads,
+and exports every symbol include/hom2d.h declares; the header and the binding
+agree on the config struct; the product never imports the oracle."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib_path():
+    from paper_1709_01619_b200 import build
+    return build.build()
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "hom2d.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(hom2d_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_header_declares_binding_exports():
+    import paper_1709_01619_b200 as P
+    assert header_functions() == sorted(P.EXPORTS)
+
+
+def test_library_exports_every_symbol(lib_path):
+    lib = ctypes.CDLL(lib_path)
+    for name in header_functions():
+        assert hasattr(lib, name), name
+    out = subprocess.run(["nm", "-D", "--defined-only", lib_path], capture_output=True, text=True).stdout
+    for name in header_functions():
+        assert re.search(rf"\bT {name}\b", out), name
+
+
+def test_library_is_sm100a(lib_path):
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", lib_path], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_config_struct_layout_matches_header():
+    """The ctypes Config mirrors hom2d_config field by field (compiled probe)."""
+    import paper_1709_01619_b200 as P
+    probe = r'''
+#include <stdio.h>
+#include <stddef.h>
+#include "hom2d.h"
+int main(void) {
+  printf("%zu %zu %zu %zu %zu %zu\n", sizeof(hom2d_config), offsetof(hom2d_config, gamma),
+         offsetof(hom2d_config, limiter_eps), offsetof(hom2d_config, record_decisions),
+         sizeof(hom2d_dist), offsetof(hom2d_dist, cuda_stream));
+  return 0;
+}
+'''
+    import tempfile
+    with tempfile.TemporaryDirectory() as d:
+        src = os.path.join(d, "p.c")
+        exe = os.path.join(d, "p")
+        open(src, "w").write(probe)
+        subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), src, "-o", exe])
+        vals = [int(v) for v in subprocess.check_output([exe]).split()]
+    C = P.Config
+    D = P.Dist
+    assert vals == [ctypes.sizeof(C), C.gamma.offset, C.limiter_eps.offset, C.record_decisions.offset,
+                    ctypes.sizeof(D), D.cuda_stream.offset]
+
+
+def test_product_does_not_import_oracle():
+    pkg = os.path.join(ROOT, "paper_1709_01619_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in txt and "from oracle" not in txt and "hom2d_oracle" not in txt, f
+
+
+def test_missing_extension_fails_loudly(tmp_path):
+    import paper_1709_01619_b200 as P
+    saved = P._lib
+    P._lib = None
+    try:
+        with pytest.raises(RuntimeError):
+            P.load(str(tmp_path / "nope.so"))
+    finally:
+        P._lib = saved

@@ -1,0 +1,247 @@
+"""GPU parity: the CUDA path through the C ABI against the CPU oracle on the same
+seeded inputs (BASELINE.json north_star: relative L-inf <= 1e-10 per conserved
+variable after 100 fp64 steps; branch decisions identical).
+
+Tolerances ("parity bar"): one residual evaluation agrees to 1e-12
+relative (a few hundred fp64 operations with different FMA contraction and
+summation order); 100 SSP-RK3 steps (300 stages) to the north_star's 1e-10.
+"""
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+HO = [(m, k) for m in ("cpr", "ndg", "dg", "sd") for k in (1, 2, 3, 4)]
+ALL = HO + [("fv", 1), ("fv", 2)]
+CFL = {("cpr", 1): 0.24, ("ndg", 1): 0.24, ("dg", 1): 0.24, ("sd", 1): 0.3,
+       ("cpr", 2): 0.13, ("ndg", 2): 0.13, ("dg", 2): 0.13, ("sd", 2): 0.2,
+       ("cpr", 3): 0.08, ("ndg", 3): 0.08, ("dg", 3): 0.08, ("sd", 3): 0.1,
+       ("cpr", 4): 0.05, ("ndg", 4): 0.05, ("dg", 4): 0.05, ("sd", 4): 0.06,
+       ("fv", 1): 0.37, ("fv", 2): 0.37}
+
+
+@pytest.fixture(scope="module")
+def P():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1709_01619_b200 as P
+    from paper_1709_01619_b200 import build
+    build.build()
+    P.load()
+    return P
+
+
+def pair(orc, P, nx, ny, method, k, bc=0, box=(-5.0, 5.0, -5.0, 5.0), cfl=None, limiter=0, record=0,
+         cpr_chain_rule=1):
+    cfl = CFL[(method, k)] if cfl is None else cfl
+    oc = orc.config(nx=nx, ny=ny, method=method, k=k, bc=bc, box=box, cfl=cfl, limiter=limiter,
+                    cpr_chain_rule=cpr_chain_rule)
+    gc = P.make_config(nx, ny, method=method, k=k, bc=bc, box=box, cfl=cfl, limiter=limiter,
+                       cpr_chain_rule=cpr_chain_rule, record_decisions=record)
+    return oc, P.Solver(gc)
+
+
+def rel_linf(a, b):
+    a, b = a.reshape(4, -1), b.reshape(4, -1)
+    return max(np.abs(a[c] - b[c]).max() / np.abs(b[c]).max() for c in range(4))
+
+
+def rel_linf_res(a, b):
+    """residuals: per component, relative to the largest |R| of that component (or
+    to the largest |R| overall where a component is identically ~0)."""
+    a, b = a.reshape(4, -1), b.reshape(4, -1)
+    big = np.abs(b).max()
+    return max(np.abs(a[c] - b[c]).max() / max(np.abs(b[c]).max(), 1e-3 * big) for c in range(4))
+
+
+@pytest.mark.parametrize("method,k", ALL)
+@pytest.mark.parametrize("bc", [0, 1])
+def test_residual_parity(orc, P, method, k, bc):
+    import torch
+    # 19 x 13: ragged against every tile shape, several tiles in each direction
+    nx, ny = (19, 13) if method != "fv" else (45, 21)
+    oc, s = pair(orc, P, nx, ny, method, k, bc=bc)
+    from paper_1709_01619_b200.inputs import perturb
+    q = perturb(orc.init_case(oc), seed=11 + k, amp=1e-2)
+    r_orc = orc.residual(oc, q)
+    r_gpu = s.residual(torch.from_numpy(q).cuda()).cpu().numpy()
+    assert rel_linf_res(r_gpu, r_orc) < 1e-12
+
+
+@pytest.mark.parametrize("method,k", ALL)
+def test_100_steps_parity(orc, P, method, k):
+    """north_star gate: 100 SSP-RK3 steps, rel L-inf <= 1e-10 per variable."""
+    nx, ny = (10, 10) if method != "fv" else (40, 40)
+    oc, s = pair(orc, P, nx, ny, method, k)
+    from paper_1709_01619_b200.inputs import perturb
+    q = perturb(orc.init_case(oc), seed=3, amp=1e-3)
+    s.set_state(q)
+    t_g, n_g = s.step(100)
+    q_o, t_o, n_o = orc.run(oc, q, 100)
+    assert n_g == n_o == 100
+    assert abs(t_g - t_o) <= 1e-12 * t_o
+    assert rel_linf(s.get_state(), q_o) <= 1e-10
+
+
+def test_config1_cpr_p1_vortex(orc, P):
+    """BASELINE config 1: CPR P1 vortex 10x10 periodic, 100 steps, from init_case."""
+    oc, s = pair(orc, P, 10, 10, "cpr", 1)
+    s.init_case(P.VORTEX)
+    q0 = s.get_state()
+    q0_o = orc.init_case(oc)
+    assert rel_linf(q0, q0_o) <= 1e-14
+    s.step(100)
+    q_o, t_o, _ = orc.run(oc, q0_o, 100)
+    assert rel_linf(s.get_state(), q_o) <= 1e-10
+    e_g = s.error(P.VORTEX, 0)
+    e_o = orc.error(oc, q_o, t_o)
+    np.testing.assert_allclose(e_g, e_o, rtol=1e-9)
+
+
+@pytest.mark.parametrize("method,k", [("cpr", 1), ("dg", 2), ("sd", 1), ("ndg", 2), ("cpr", 3)])
+def test_paper_table_point_on_gpu(orc, P, method, k):
+    """The GPU reproduces a Table 2/3 entry end to end (init, march to t = 1, error)."""
+    cfl = {1: 0.24, 2: 0.14}.get(k, 0.08) if method != "sd" else {1: 0.3, 2: 0.2}[k]
+    oc, s = pair(orc, P, 20, 20, method, k, cfl=cfl)
+    s.init_case(P.VORTEX)
+    t, _ = s.step(10 ** 6, 1.0)
+    assert t == 1.0
+    q_o, t_o, _ = orc.run(oc, orc.init_case(oc), 10 ** 6, 1.0)
+    assert rel_linf(s.get_state(), q_o) <= 1e-10
+    np.testing.assert_allclose(s.error(P.VORTEX, 0), orc.error(oc, q_o, t_o), rtol=1e-8)
+
+
+@pytest.mark.parametrize("method,k", ALL)
+def test_dt_parity(orc, P, method, k):
+    oc, s = pair(orc, P, 12, 9, method, k)
+    s.init_case(P.VORTEX)
+    assert s.compute_dt() == pytest.approx(orc.dt(oc, orc.init_case(oc)), rel=1e-14)
+
+
+@pytest.mark.parametrize("method,k,cfl", [("cpr", 1, 0.2), ("cpr", 2, 0.1), ("ndg", 1, 0.2), ("dg", 1, 0.2),
+                                          ("dg", 2, 0.08), ("sd", 1, 0.27), ("sd", 2, 0.18), ("cpr", 3, 0.06),
+                                          ("sd", 4, 0.05), ("dg", 4, 0.03)])
+def test_shock_limiter_parity(orc, P, method, k, cfl):
+    """Radial shock tube, transmissive, limiter after every stage: state parity and
+    identical trouble-cell marks (decision counters)."""
+    box = (-1.0, 1.0, -1.0, 1.0)
+    oc, s = pair(orc, P, 24, 24, method, k, bc=1, box=box, cfl=cfl, limiter=1, record=1)
+    s.init_case(P.SHOCK)
+    q0 = orc.init_case(oc, orc.SHOCK)
+    assert rel_linf(s.get_state(), q0) <= 1e-14
+    cnt = np.zeros(4, dtype=np.int64)
+    s.set_state(q0)
+    t_g, n_g = s.step(40, 0.25)
+    q_o, t_o, n_o = orc.run(oc, q0, 40, 0.25, counts=cnt)
+    assert n_g == n_o
+    assert rel_linf(s.get_state(), q_o) <= 1e-10
+    assert s.decisions()[0] == cnt[0] > 0
+
+
+@pytest.mark.parametrize("k,cfl", [(1, 0.58), (2, 0.54)])
+def test_fv_shock_decisions(orc, P, k, cfl):
+    box = (-1.0, 1.0, -1.0, 1.0)
+    oc, s = pair(orc, P, 48, 48, "fv", k, bc=1, box=box, cfl=cfl, record=1)
+    q0 = orc.init_case(oc, orc.SHOCK)
+    s.set_state(q0)
+    t_g, n_g = s.step(30, 0.25)
+    cnt = np.zeros(4, dtype=np.int64)
+    q_o, t_o, n_o = orc.run(oc, q0, 30, 0.25, counts=cnt)
+    assert n_g == n_o
+    assert rel_linf(s.get_state(), q_o) <= 1e-10
+    np.testing.assert_array_equal(s.decisions()[1:], cnt[1:])
+
+
+@pytest.mark.parametrize("method,k", [("cpr", 2), ("dg", 3), ("sd", 2), ("ndg", 1)])
+def test_limiter_single_application(orc, P, method, k):
+    import torch  # noqa: F401
+    box = (-1.0, 1.0, -1.0, 1.0)
+    oc, s = pair(orc, P, 17, 15, method, k, bc=1, box=box, limiter=1, record=1)
+    from paper_1709_01619_b200.inputs import perturb
+    q = perturb(orc.init_case(oc, orc.SHOCK), seed=5, amp=1e-2)
+    s.set_state(q)
+    s.limit()
+    ql, marks = orc.limit(oc, q)
+    assert rel_linf(s.get_state(), ql) <= 1e-14
+    assert s.decisions()[0] == marks.sum()
+
+
+def test_nonphysical_is_reported(orc, P):
+    oc, s = pair(orc, P, 8, 8, "cpr", 1)
+    q = orc.init_case(oc)
+    n = q.size // 4
+    q[3 * n + 5] = -1.0  # negative energy -> negative pressure
+    s.set_state(q)
+    with pytest.raises(P.NonPhysicalState):
+        s.step(5)
+
+
+def test_time_clipping(orc, P):
+    oc, s = pair(orc, P, 10, 10, "cpr", 2)
+    s.init_case(P.VORTEX)
+    t, n = s.step(1000, 0.3)
+    _, t_o, n_o = orc.run(oc, orc.init_case(oc), 1000, 0.3)
+    assert t == t_o == pytest.approx(0.3, abs=1e-15) and n == n_o
+    t2, n2 = s.step(5, 0.3)  # already there: no-op
+    assert n2 == 0 and t2 == t
+
+
+def test_determinism_bitwise(orc, P):
+    oc, s = pair(orc, P, 33, 17, "dg", 2)
+    from paper_1709_01619_b200.inputs import perturb
+    q = perturb(orc.init_case(oc), seed=9, amp=1e-2)
+    out = []
+    for _ in range(2):
+        s.set_state(q)
+        s.step(20)
+        out.append(s.get_state())
+    np.testing.assert_array_equal(out[0], out[1])
+
+
+@pytest.mark.parametrize("method,k,n", [("cpr", 3, 2048), ("cpr", 2, 1024), ("fv", 1, 2048)])
+def test_full_size_tiled_patch(orc, P, method, k, n):
+    """At BASELINE sizes, in the bench's launch configuration: a state that repeats
+    a seeded 16x16-element patch must give the oracle's residual of that patch on
+    its own periodic 16x16 grid, at every element of the big grid (a property that
+    holds at any size; the oracle only ever sees the small patch)."""
+    import torch
+    pn = 16
+    box_small = (-5.0, -5.0 + 10.0 * pn / n, -5.0, -5.0 + 10.0 * pn / n)  # same element size
+    oc = orc.config(nx=pn, ny=pn, method=method, k=k, box=box_small)
+    from paper_1709_01619_b200.inputs import perturb
+    qp = perturb(orc.init_case(oc), seed=21, amp=1e-2)
+    r_p = orc.residual(oc, qp)
+    npe = 1 if method == "fv" else (k + 1) ** 2
+    # tile the patch: [c][J][I][p] -> [c][j][i][p]
+    patch = qp.reshape(4, pn, pn, npe)
+    big = np.tile(patch, (1, n // pn, n // pn, 1)).reshape(-1)
+    s = P.Solver(P.make_config(n, n, method=method, k=k, cfl=CFL[(method, k)]))
+    r_big = s.residual(torch.from_numpy(big).cuda()).cpu().numpy().reshape(4, n // pn, pn, n // pn, pn, npe)
+    ref = r_p.reshape(4, 1, pn, 1, pn, npe)
+    err = np.abs(r_big - ref).max(axis=(1, 2, 3, 4, 5)) / np.maximum(np.abs(ref).reshape(4, -1).max(1), 1e-3 * np.abs(ref).max())
+    assert err.max() < 1e-12
+    s.close()
+
+
+def test_full_size_free_stream_and_mass(orc, P):
+    """4096^2 CPR P3 (north-star size): a uniform state stays uniform to round-off
+    after 3 steps (free-stream preservation), in the bench's launch config."""
+    import torch
+    n = 4096
+    s = P.Solver(P.make_config(n, n, method="cpr", k=3, cfl=0.08))
+    npts = n * n * 16
+    rho, u, v, p = 1.0, 1.0, 0.5, 1.0
+    q = torch.empty(4 * npts, dtype=torch.float64, device="cuda")
+    q[:npts] = rho
+    q[npts:2 * npts] = rho * u
+    q[2 * npts:3 * npts] = rho * v
+    q[3 * npts:] = p / 0.4 + 0.5 * rho * (u * u + v * v)
+    s.set_state(q)
+    s.step(3)
+    out = torch.empty_like(q)
+    s.get_state(out)
+    assert float((out - q).abs().max()) < 1e-12
+    s.close()
