@@ -71,10 +71,12 @@ __global__ void __launch_bounds__(FNT) fv_stage_kernel(const StageArgs a) {
     const int fx = t % (FTX + 1), ly = t / (FTX + 1);
     if (ly >= TYv || fx > TXv) continue;
     double qW[4], qE[4], F[4], fL[4], fR[4];
+    // tile-edge faces are computed by both neighbouring tiles; count each face once
+    long long* dec = (fx < TXv || i0 + TXv == a.nx) ? a.dec : nullptr;
 #pragma unroll
     for (int c = 0; c < 4; ++c)
       muscl<ORDER>(sq[c][ly + 2][fx], sq[c][ly + 2][fx + 1], sq[c][ly + 2][fx + 2], sq[c][ly + 2][fx + 3], qW[c],
-                   qE[c], a.dec);
+                   qE[c], dec);
     rusanov<0>(qW, qE, gm1, gam, F, fL, fR);
 #pragma unroll
     for (int c = 0; c < 4; ++c) sF[ly][fx][c] = F[c];
@@ -83,10 +85,11 @@ __global__ void __launch_bounds__(FNT) fv_stage_kernel(const StageArgs a) {
     const int lx = t % FTX, fy = t / FTX;
     if (lx >= TXv || fy > TYv) continue;
     double qW[4], qE[4], F[4], fL[4], fR[4];
+    long long* dec = (fy < TYv || (j0 + TYv == a.nrows && a.count_top)) ? a.dec : nullptr;
 #pragma unroll
     for (int c = 0; c < 4; ++c)
       muscl<ORDER>(sq[c][fy][lx + 2], sq[c][fy + 1][lx + 2], sq[c][fy + 2][lx + 2], sq[c][fy + 3][lx + 2], qW[c],
-                   qE[c], a.dec);
+                   qE[c], dec);
     rusanov<1>(qW, qE, gm1, gam, F, fL, fR);
 #pragma unroll
     for (int c = 0; c < 4; ++c) sG[fy][lx][c] = F[c];

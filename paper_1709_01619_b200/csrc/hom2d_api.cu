@@ -135,7 +135,7 @@ AuxArgs aux(const hom2d* h) {
   AuxArgs a;
   a.method = h->cfg.method; a.k = h->cfg.k; a.nx = h->cfg.nx; a.nrows = h->nrows; a.row0 = h->row0;
   a.ny_global = h->cfg.ny; a.xmin = h->cfg.xmin; a.xmax = h->cfg.xmax; a.ymin = h->cfg.ymin;
-  a.ymax = h->cfg.ymax; a.gamma = h->cfg.gamma; a.cs = h->nloc;
+  a.ymax = h->cfg.ymax; a.gamma = h->cfg.gamma; a.cs = h->nloc; a.dt = nullptr;
   return a;
 }
 
@@ -190,6 +190,7 @@ hom2d_status run_stage(hom2d* h, const double* q, const double* q0, double* out,
   s.a0 = a0; s.a1 = a1; s.bcoef = b; s.dt = dt; s.gamma = h->cfg.gamma;
   s.lam = lam; s.bad = bad;
   s.dec = h->cfg.record_decisions ? h->dec : nullptr;
+  s.count_top = (h->rank == h->nranks - 1);
   int e;
   const bool timed = 2 * (h->ev_used + 1) <= (int)h->ev.size();
   if (timed) cudaEventRecord(h->ev[2 * h->ev_used], h->stream);
@@ -206,9 +207,11 @@ hom2d_status run_stage(hom2d* h, const double* q, const double* q0, double* out,
   return HOM2D_OK;
 }
 
-// HO limiter on X in place: averages, (exchange average rows), detect + limit
-hom2d_status run_limiter(hom2d* h, double* X) {
+// HO limiter on X in place: averages, (exchange average rows), detect + limit.
+// dt != nullptr: skipped on the device when the step was clipped out (*dt == 0).
+hom2d_status run_limiter(hom2d* h, double* X, const double* dt = nullptr) {
   AuxArgs A = aux(h);
+  A.dt = dt;
   launch_averages(A, X, h->qbar, h->stream);
   const long long ne = (long long)h->cfg.nx * h->nrows;
   const double *lo, *hi;
@@ -411,14 +414,14 @@ hom2d_status hom2d_step(hom2d* h, int32_t max_steps, double t_end, double* t_out
       const double* dt = h->clock + 1;
       // SSP-RK3 (Shu-Osher)
       if ((st = run_stage(h, h->Qn, nullptr, h->Q1, 0.0, 1.0, 1.0, dt, nullptr, nullptr))) return st;
-      if (lim && (st = run_limiter(h, h->Q1))) return st;
+      if (lim && (st = run_limiter(h, h->Q1, dt))) return st;
       if ((st = run_stage(h, h->Q1, h->Qn, h->Q2, 0.75, 0.25, 0.25, dt, nullptr, nullptr))) return st;
-      if (lim && (st = run_limiter(h, h->Q2))) return st;
+      if (lim && (st = run_limiter(h, h->Q2, dt))) return st;
       if (!lim) {
         if ((st = run_stage(h, h->Q2, h->Qn, h->Qn, 1.0 / 3.0, 2.0 / 3.0, 2.0 / 3.0, dt, h->lam, h->bad))) return st;
       } else {
         if ((st = run_stage(h, h->Q2, h->Qn, h->Qn, 1.0 / 3.0, 2.0 / 3.0, 2.0 / 3.0, dt, nullptr, nullptr))) return st;
-        if ((st = run_limiter(h, h->Qn))) return st;
+        if ((st = run_limiter(h, h->Qn, dt))) return st;
         launch_lambda(aux(h), h->Qn, h->lam, h->bad, h->stream);  // dt of the limited state
         h->launches++;
       }

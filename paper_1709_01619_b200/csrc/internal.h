@@ -27,6 +27,7 @@ struct StageArgs {
   unsigned long long* lam; // optional: atomicMax of max(|u|,|v|)+c of `out` (bits of a double >= 0)
   unsigned long long* bad; // optional: atomicMin of the first non-physical point index
   long long* dec;          // optional: decision counters [4]
+  int count_top;           // this strip owns the top boundary face row (decision counting)
 };
 
 int launch_ho_stage(int method, int k, const StageArgs& a, cudaStream_t s);
@@ -36,6 +37,7 @@ struct AuxArgs {
   int method, k, nx, nrows, row0, ny_global;
   double xmin, xmax, ymin, ymax, gamma;
   long long cs;
+  const double* dt;  // optional: skip the pass when *dt == 0 (clipped-out step)
 };
 
 // max(|u|,|v|)+c over the state -> atomicMax into lam (bits); optional bad-point check
