@@ -131,9 +131,11 @@ hom2d_status hom2d_error(hom2d* h, int32_t case_id, int32_t var, double* l1, dou
 hom2d_status hom2d_time(const hom2d* h, double* t);
 
 /* Branch-decision counters accumulated since create/set_state (record_decisions
- * = 1): [0] limiter marks (element-stage), [1] minmod -> 0, [2] minmod -> first
- * argument, [3] minmod -> second argument (MUSCL, per face side and component). */
-hom2d_status hom2d_decisions(hom2d* h, int64_t* counts4);
+ * = 1), counts8[8]: [0] limiter marks (element-stage), [1] minmod -> 0,
+ * [2] minmod -> first argument, [3] minmod -> second argument (MUSCL, per face
+ * side and component, each face once), [4] minmod ties (an argument or their
+ * difference within 1e-12 of the switch point; not counted in 1-3), [5-7] 0. */
+hom2d_status hom2d_decisions(hom2d* h, int64_t* counts8);
 
 /* Kernel launches issued by this handle since create (bench accounting). */
 int64_t hom2d_launch_count(const hom2d* h);

@@ -54,8 +54,10 @@ typedef struct {
   double dt_fixed;        /* test-only: > 0 replaces the CFL dt of Eq. (36) */
 } orc_config;
 
-/* decision counters (parity of branch decisions) */
-enum { DEC_MARKED = 0, DEC_MM_ZERO = 1, DEC_MM_FIRST = 2, DEC_MM_SECOND = 3 };
+/* decision counters (parity of branch decisions); a minmod whose
+ * arguments or their difference lie within DEC_TIE of the switch point is a tie */
+enum { DEC_MARKED = 0, DEC_MM_ZERO = 1, DEC_MM_FIRST = 2, DEC_MM_SECOND = 3, DEC_MM_TIE = 4 };
+#define DEC_TIE 1e-12
 
 #define MAXN 9   /* up to 8-point rules (error quadrature) */
 
@@ -310,7 +312,10 @@ static double mm2(double a, double b, int64_t *cnt) {
   double r = 0.0; int which = 0;
   if (a > 0.0 && b > 0.0) { if (a <= b) { r = a; which = 1; } else { r = b; which = 2; } }
   else if (a < 0.0 && b < 0.0) { if (a >= b) { r = a; which = 1; } else { r = b; which = 2; } }
-  if (cnt) cnt[which == 0 ? DEC_MM_ZERO : (which == 1 ? DEC_MM_FIRST : DEC_MM_SECOND)]++;
+  if (cnt) {
+    if (fabs(a) <= DEC_TIE || fabs(b) <= DEC_TIE || fabs(a - b) <= DEC_TIE) cnt[DEC_MM_TIE]++;
+    else cnt[which == 0 ? DEC_MM_ZERO : (which == 1 ? DEC_MM_FIRST : DEC_MM_SECOND)]++;
+  }
   return r;
 }
 static double mm3(double a, double b, double c) {

@@ -211,7 +211,7 @@ class Solver:
         return t.value
 
     def decisions(self):
-        out = np.zeros(4, dtype=np.int64)
+        out = np.zeros(8, dtype=np.int64)
         self._check(self._L.hom2d_decisions(self.h, C.c_void_p(out.ctypes.data)))
         return out
 

@@ -113,7 +113,11 @@ __device__ __forceinline__ void count_dec(long long* dec, int which) {
 }
 
 // minmod of two arguments (ties return the first argument, zero if the
-// signs differ or either is zero), optionally recording the branch taken.
+// signs differ or either is zero), optionally recording the branch taken.  A
+// decision within DEC_TIE of its switch point (a = 0, b = 0 or a = b) is counted
+// as a tie (slot 4), not by outcome: its branch may legitimately differ between
+// two fp64 evaluation orders.
+#define DEC_TIE 1e-12
 __device__ __forceinline__ double minmod2(double a, double b, long long* dec) {
   double r = 0.0;
   int which = 1;
@@ -122,7 +126,10 @@ __device__ __forceinline__ double minmod2(double a, double b, long long* dec) {
   } else if (a < 0.0 && b < 0.0) {
     if (a >= b) { r = a; which = 2; } else { r = b; which = 3; }
   }
-  if (dec) count_dec(dec, which);
+  if (dec) {
+    if (fabs(a) <= DEC_TIE || fabs(b) <= DEC_TIE || fabs(a - b) <= DEC_TIE) which = 4;
+    count_dec(dec, which);
+  }
   return r;
 }
 

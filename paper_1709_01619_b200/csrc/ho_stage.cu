@@ -376,8 +376,6 @@ static int launch_m(int k, const StageArgs& a, cudaStream_t s) {
 
 int launch_ho_stage(int method, int k, const StageArgs& a, cudaStream_t s) {
   switch (method) {
-    case M_CPR: return launch_m<M_CPR>(k, a, s);
-    case M_NDG: return launch_m<M_NDG>(k, a, s);
     case M_DG: return launch_m<M_DG>(k, a, s);
     case M_SD: return launch_m<M_SD>(k, a, s);
   }

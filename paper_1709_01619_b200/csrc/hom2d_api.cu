@@ -110,7 +110,7 @@ size_t carve(hom2d* h, const hom2d_config& c, int nranks, char* base) {
   double* clk = cv.take<double>(8);
   auto* lam = cv.take<unsigned long long>(4);
   auto* bad = cv.take<unsigned long long>(2);
-  auto* dec = cv.take<long long>(4);
+  auto* dec = cv.take<long long>(8);
   double* part = cv.take<double>(3 * max_part);
   double* err3 = cv.take<double>(4);
   double* qbar = (c.method != HOM2D_FV) ? cv.take<double>(4 * (size_t)c.nx * nrows) : nullptr;
@@ -199,7 +199,8 @@ hom2d_status run_stage(hom2d* h, const double* q, const double* q0, double* out,
   } else {
     int method = h->cfg.method;
     if (method == HOM2D_CPR && !h->cfg.cpr_chain_rule) method = HOM2D_NDG;  // flux-differentiation CPR == NDG
-    e = launch_ho_stage(method, h->cfg.k, s, h->stream);
+    e = (method == HOM2D_CPR || method == HOM2D_NDG) ? launch_gll_stage(method, h->cfg.k, s, h->stream)
+                                                      : launch_ho_stage(method, h->cfg.k, s, h->stream);
   }
   if (timed) cudaEventRecord(h->ev[2 * h->ev_used++ + 1], h->stream);
   h->launches++;
@@ -246,7 +247,7 @@ hom2d_status refresh_lambda(hom2d* h) {
 hom2d_status reset_clock(hom2d* h, double t0) {
   double c[4] = {t0, 0.0, 0.0, 0.0};
   CU(h, cudaMemcpyAsync(h->clock, c, sizeof(c), cudaMemcpyHostToDevice, h->stream));
-  CU(h, cudaMemsetAsync(h->dec, 0, 4 * sizeof(long long), h->stream));
+  CU(h, cudaMemsetAsync(h->dec, 0, 8 * sizeof(long long), h->stream));
   CU(h, cudaMemsetAsync(h->bad, 0xff, sizeof(unsigned long long), h->stream));
   CU(h, cudaStreamSynchronize(h->stream));
   return HOM2D_OK;
@@ -480,16 +481,14 @@ hom2d_status hom2d_time(const hom2d* h, double* t) {
   return HOM2D_OK;
 }
 
-hom2d_status hom2d_decisions(hom2d* h, int64_t* counts4) {
+hom2d_status hom2d_decisions(hom2d* h, int64_t* counts8) {
   GUARD(h);
-  if (!counts4) return HOM2D_ERR_ARG;
-  CU(h, cudaMemcpyAsync(counts4, h->dec, 4 * sizeof(long long), cudaMemcpyDeviceToHost, h->stream));
+  if (!counts8) return HOM2D_ERR_ARG;
+  CU(h, cudaMemcpyAsync(counts8, h->dec, 8 * sizeof(long long), cudaMemcpyDeviceToHost, h->stream));
   CU(h, cudaStreamSynchronize(h->stream));
-  if (h->nranks > 1) {
-    // host-side sum over ranks through the device scratch
-    long long* d = h->dec;
-    NC(h, ncclAllReduce(d, h->part, 4, ncclInt64, ncclSum, h->comm, h->stream));
-    CU(h, cudaMemcpyAsync(counts4, h->part, 4 * sizeof(long long), cudaMemcpyDeviceToHost, h->stream));
+  if (h->nranks > 1) {  // sum over ranks through the device scratch
+    NC(h, ncclAllReduce(h->dec, h->part, 8, ncclInt64, ncclSum, h->comm, h->stream));
+    CU(h, cudaMemcpyAsync(counts8, h->part, 8 * sizeof(long long), cudaMemcpyDeviceToHost, h->stream));
     CU(h, cudaStreamSynchronize(h->stream));
   }
   return HOM2D_OK;

@@ -30,7 +30,8 @@ struct StageArgs {
   int count_top;           // this strip owns the top boundary face row (decision counting)
 };
 
-int launch_ho_stage(int method, int k, const StageArgs& a, cudaStream_t s);
+int launch_ho_stage(int method, int k, const StageArgs& a, cudaStream_t s);   // DG, SD
+int launch_gll_stage(int method, int k, const StageArgs& a, cudaStream_t s);  // CPR, NDG
 int launch_fv_stage(int k, const StageArgs& a, cudaStream_t s);
 
 struct AuxArgs {

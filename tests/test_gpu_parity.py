@@ -132,7 +132,7 @@ def test_shock_limiter_parity(orc, P, method, k, cfl):
     s.init_case(P.SHOCK)
     q0 = orc.init_case(oc, orc.SHOCK)
     assert rel_linf(s.get_state(), q0) <= 1e-14
-    cnt = np.zeros(4, dtype=np.int64)
+    cnt = np.zeros(8, dtype=np.int64)
     s.set_state(q0)
     t_g, n_g = s.step(40, 0.25)
     q_o, t_o, n_o = orc.run(oc, q0, 40, 0.25, counts=cnt)
@@ -148,11 +148,14 @@ def test_fv_shock_decisions(orc, P, k, cfl):
     q0 = orc.init_case(oc, orc.SHOCK)
     s.set_state(q0)
     t_g, n_g = s.step(30, 0.25)
-    cnt = np.zeros(4, dtype=np.int64)
+    cnt = np.zeros(8, dtype=np.int64)
     q_o, t_o, n_o = orc.run(oc, q0, 30, 0.25, counts=cnt)
     assert n_g == n_o
     assert rel_linf(s.get_state(), q_o) <= 1e-10
-    np.testing.assert_array_equal(s.decisions()[1:], cnt[1:])
+    d = s.decisions()
+    # non-tie decisions identical; ties (within 1e-12 of the switch point) reported
+    np.testing.assert_array_equal(d[1:4], cnt[1:4])
+    assert d[4] == cnt[4]
 
 
 @pytest.mark.parametrize("method,k", [("cpr", 2), ("dg", 3), ("sd", 2), ("ndg", 1)])
