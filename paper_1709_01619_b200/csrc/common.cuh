@@ -13,10 +13,33 @@ struct Prim {
   double ri, u, v, p;  // 1/rho, velocities, pressure
 };
 
+// fp64 reciprocal: MUFU seed + two Newton steps (faithful to ~1 ulp, no slow
+// path; non-finite / zero inputs propagate as inf / NaN and are flagged later)
+__device__ __forceinline__ double frcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
+// fp64 square root: MUFU rsqrt seed + two Newton steps + one Markstein correction
+__device__ __forceinline__ double fsqrt(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x * y, y, 1.0);
+  y = fma(0.5 * y, e, y);
+  e = fma(-x * y, y, 1.0);
+  y = fma(0.5 * y, e, y);
+  const double s = x * y;
+  return fma(0.5 * y, fma(-s, s, x), s);
+}
+
 // one reciprocal per point (the only fp64 division of a flux evaluation)
 __device__ __forceinline__ Prim prims(const double q[4], double gm1) {
   Prim w;
-  w.ri = 1.0 / q[0];
+  w.ri = frcp(q[0]);
   w.u = q[1] * w.ri;
   w.v = q[2] * w.ri;
   w.p = gm1 * (q[3] - 0.5 * (q[1] * w.u + q[2] * w.v));
@@ -47,8 +70,8 @@ __device__ __forceinline__ void rusanov(const double qL[4], const double qR[4], 
   Prim wl = prims(qL, gm1), wr = prims(qR, gm1);
   flux<DIR>(qL, wl, fL);
   flux<DIR>(qR, wr, fR);
-  double sl = fabs(DIR == 0 ? wl.u : wl.v) + sqrt(gam * wl.p * wl.ri);
-  double sr = fabs(DIR == 0 ? wr.u : wr.v) + sqrt(gam * wr.p * wr.ri);
+  double sl = fabs(DIR == 0 ? wl.u : wl.v) + fsqrt(gam * wl.p * wl.ri);
+  double sr = fabs(DIR == 0 ? wr.u : wr.v) + fsqrt(gam * wr.p * wr.ri);
   double lam = fmax(sl, sr);
 #pragma unroll
   for (int c = 0; c < 4; ++c) F[c] = 0.5 * (fL[c] + fR[c]) - 0.5 * lam * (qR[c] - qL[c]);
@@ -78,7 +101,7 @@ __device__ __forceinline__ void jac(const double q[4], const Prim& w, double gm1
 // max(|u|,|v|) + c  (2-D reading of Eq. (36))
 __device__ __forceinline__ double wave_speed(const double q[4], double gm1, double gam) {
   Prim w = prims(q, gm1);
-  return fmax(fabs(w.u), fabs(w.v)) + sqrt(gam * w.p * w.ri);
+  return fmax(fabs(w.u), fabs(w.v)) + fsqrt(gam * w.p * w.ri);
 }
 
 __device__ __forceinline__ bool nonphysical(const double q[4], double gm1) {

@@ -86,7 +86,7 @@ hom2d_status check_cfg(const hom2d_config* c, int nranks) {
 
 struct Carve {
   char* base;
-  size_t off = 0;
+  size_t off = 256;  // guard: bulk copies may read up to 8 B outside an array
   template <class T>
   T* take(size_t count) {
     off = (off + 255) & ~size_t(255);
@@ -128,7 +128,7 @@ size_t carve(hom2d* h, const hom2d_config& c, int nranks, char* base) {
     h->part = part; h->max_part = max_part; h->err3 = err3; h->qbar = qbar;
     h->glo = glo; h->ghi = ghi; h->qblo = qblo; h->qbhi = qbhi;
   }
-  return cv.off + 256;
+  return cv.off + 512;  // trailing guard
 }
 
 AuxArgs aux(const hom2d* h) {
@@ -364,7 +364,11 @@ hom2d_status hom2d_init_case(hom2d* h, int32_t case_id) {
 hom2d_status hom2d_residual(hom2d* h, const double* q_dev, double* r_dev) {
   GUARD(h);
   if (!q_dev || !r_dev) return fail(h, HOM2D_ERR_ARG, "residual: null pointer");
-  hom2d_status st = run_stage(h, q_dev, nullptr, r_dev, 0.0, 0.0, 1.0, nullptr, nullptr, nullptr);
+  // stage kernels stream from the handle's own (guarded, aligned) arrays
+  CU(h, cudaMemcpyAsync(h->Q1, q_dev, 4 * h->nloc * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+  hom2d_status st = run_stage(h, h->Q1, nullptr, h->Q2, 0.0, 0.0, 1.0, nullptr, nullptr, nullptr);
+  if (st) return st;
+  CU(h, cudaMemcpyAsync(r_dev, h->Q2, 4 * h->nloc * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
   if (st) return st;
   CU(h, cudaStreamSynchronize(h->stream));
   return HOM2D_OK;
