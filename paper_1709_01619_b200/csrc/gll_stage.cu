@@ -7,11 +7,14 @@
 //
 // B200 design (not the paper's thread-per-point Algs. 7-8):
 //  * a CTA owns a strip of TX elements and MARCHES up RB element rows of it;
-//  * element rows stream HBM -> shared memory with TMA bulk copies
-//    (cp.async.bulk + mbarrier, one copy per element and component into padded
-//    slots so that the column reads below are bank-conflict free), in a
-//    NSTG-deep ring issued two rows ahead: HBM traffic is continuous and each
-//    state value is read from HBM once;
+//  * element rows (strip + W/E halo element) stream HBM -> shared memory by TMA
+//    in an NSTG-deep mbarrier ring, issued two rows ahead, so HBM traffic is
+//    continuous and each state value is read from HBM once.  For P3 (one
+//    element row of one component = 128 B) a 3-D tensor map moves the whole
+//    row (4 components x 34 elements) in ONE cp.async.bulk.tensor with the
+//    128-byte swizzle, which makes the column reads below bank-conflict free;
+//    other orders use 1-D bulk copies (their odd element strides are
+//    conflict-free by themselves, P1 2-way);
 //  * one thread per element LINE (the n points of row b of one element): the
 //    xi-direction work (derivative, both x-faces, correction) is register
 //    resident; the eta operands are broadcast reads of the element's columns;
@@ -20,6 +23,10 @@
 //    element above is carried to the next marching step (S faces are free);
 //  * results leave by coalesced stores straight from registers (out = a0 q0 +
 //    a1 q + bcoef dt R), with the wave-speed max for the next dt.
+#include <cudaTypedefs.h>
+
+#include <cstring>
+
 #include "common.cuh"
 #include "ops_tables.h"
 #include "tma.cuh"
@@ -37,24 +44,34 @@ template <> struct GTile<4> { static constexpr int TX = 32, RB = 64, MINB = 1; }
 enum { GM_CPR = 1, GM_NDG = 3 };
 constexpr int NSTG = 3;  // ring depth (rows): current, N neighbour, one in flight
 
+struct GMaps {   // P3: 3-D tensor maps {16 points, TX+2 elements, 4 components}
+  CUtensorMap q, lo, hi;
+};
+
 template <int M, int K>
 struct G {
   static constexpr int N = K + 1, NP = N * N;
   static constexpr int TX = GTile<K>::TX, RB = GTile<K>::RB, NT = TX * N;
-  // padded element slot (doubles): holds an aligned superset of the element;
-  // the stride makes 8 consecutive slots hit 8 different bank groups
-  static constexpr int NPS = (NP & 1) ? NP + 1 : NP + 2;
-  static constexpr int NSL = TX + 2;                  // slots: W halo, TX elements, E halo
-  static constexpr int OR_ = 0;                       // ring [NSTG][4][NSL][NPS]
-  static constexpr int OFW = OR_ + NSTG * 4 * NSL * NPS;
-  static constexpr int OJN = OFW + (TX + 1) * N * 4;  // W-face fluxes [TX+1][N][4]; N jumps [TX][N][4]
+  static constexpr bool SWZ = (NP == 16);           // element row of one component == 128 B
+  static constexpr int NSL = TX + 2;                 // W halo, TX elements, E halo
+  // 1-D path: W piece | main piece | E piece per component (aligned supersets)
+  static constexpr int CW = (NP + 1 + 1) & ~1;
+  static constexpr int CM = ((TX * NP + 1) + 1) & ~1;
+  static constexpr int CREG = CW + CM + CW;
+  // per stage (doubles): SWZ: 4 * NSL rows of 16 (+ 8 unswizzled fix-up rows); else 4 * CREG
+  static constexpr int FIXO = (4 * NSL * 16 + 127) & ~127;
+  static constexpr int STG = SWZ ? FIXO + 8 * 16 : 4 * CREG;
+  static constexpr int STGA = (STG + 127) & ~127;    // 1024-byte aligned stages
+  static constexpr int OR_ = 0;
+  static constexpr int OFW = OR_ + NSTG * STGA;       // W-face fluxes [TX+1][N][4]
+  static constexpr int OJN = OFW + (TX + 1) * N * 4;  // N jumps of the current row [TX][N][4]
   static constexpr int OJS = OJN + TX * N * 4;        // S jumps, double-buffered [2][TX][N][4]
   static constexpr int OG = OJS + 2 * TX * N * 4;     // NDG: g at every point [TX][NP][4]
   static constexpr int OT = OG + (M == GM_NDG ? TX * NP * 4 : 0);
   static constexpr int ORD = OT + ((N * N + 2 * N + 1) & ~1);
   static constexpr int OB = ORD + 32;                 // mbarriers (as doubles)
   static constexpr int TOTAL = OB + NSTG;
-  static constexpr size_t SMEM = TOTAL * sizeof(double);
+  static constexpr size_t SMEM = TOTAL * sizeof(double) + 1024;  // + alignment slack
 };
 
 struct GTab {
@@ -107,14 +124,29 @@ __device__ __forceinline__ const double* row_src(const StageArgs& a, int jr, int
   return a.q + (long long)jr * a.nx * np;
 }
 
+// 1-D path: aligned-superset copy of [src, src+n) doubles; offset (0 or 1
+// double) of src inside the destination
+__device__ __forceinline__ int piece_off(const double* src) {
+  return (int)((reinterpret_cast<uintptr_t>(src) >> 3) & 1);
+}
+__device__ __forceinline__ uint32_t piece_bytes(const double* src, int n) {
+  const uintptr_t s0 = reinterpret_cast<uintptr_t>(src);
+  return (uint32_t)(((s0 + (uintptr_t)n * 8 + 15) & ~uintptr_t(15)) - (s0 & ~uintptr_t(15)));
+}
+__device__ __forceinline__ const void* piece_src(const double* src) {
+  return reinterpret_cast<const void*>(reinterpret_cast<uintptr_t>(src) & ~uintptr_t(15));
+}
+
 }  // namespace
 
 template <int M, int K>
-__global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB) gll_stage_kernel(const StageArgs a, const GTab tab) {
+__global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
+    gll_stage_kernel(const StageArgs a, const GTab tab, const __grid_constant__ GMaps maps) {
   using H = G<M, K>;
-  constexpr int N = H::N, NP = H::NP, TX = H::TX, RB = H::RB, NT = H::NT, NPS = H::NPS, NSL = H::NSL;
+  constexpr int N = H::N, NP = H::NP, TX = H::TX, RB = H::RB, NT = H::NT, NSL = H::NSL;
+  constexpr int CW = H::CW, CM = H::CM, CREG = H::CREG, STGA = H::STGA;
   extern __shared__ double4 smem4[];
-  double* sm = reinterpret_cast<double*>(smem4);
+  double* sm = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(smem4) + 1023) & ~uintptr_t(1023));
   double* ring = sm + H::OR_;
   double* sFW = sm + H::OFW;
   double* sJN = sm + H::OJN;
@@ -135,7 +167,10 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB) gll_stage_kernel(
   const int lx = tid / N, b = tid - lx * N;
   const bool own = lx < TXv;
   const bool mirW = (i0 == 0 && a.bcx), mirE = (i0 + TXv == a.nx && a.bcx);
-  const int nload = RBv + 2;  // rows jb-1 .. jb+RBv
+  const bool wrapW = (i0 == 0 && !a.bcx), wrapE = (i0 + TXv == a.nx && !a.bcx);
+  const int iw = i0 > 0 ? i0 - 1 : a.nx - 1;      // W halo element (periodic wrap)
+  const int ie = i0 + TXv < a.nx ? i0 + TXv : 0;  // E halo element
+  const int nload = RBv + 2;                      // rows jb-1 .. jb+RBv
 
   for (int i = tid; i < N * N + 2 * N; i += NT) sT[i] = tab.v[i];
   if (tid == 0) {
@@ -144,51 +179,94 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB) gll_stage_kernel(
   }
   __syncthreads();
 
-  // global element index of slot e (0 = W halo, 1..TXv own, TXv+1 = E halo); -1 = none
-  auto slot_elem = [&](int e) -> int {
-    if (e == 0) return mirW ? -1 : (i0 > 0 ? i0 - 1 : a.nx - 1);
-    if (e == TXv + 1) return mirE ? -1 : (i0 + TXv < a.nx ? i0 + TXv : 0);
-    return i0 + e - 1;
-  };
-  // warp 0 streams row L of this CTA's sequence (L = 0 -> row jb-1) into stage L % NSTG
+  // ---- streaming: thread 0 moves row L (L = 0 -> row jb-1) into stage L % NSTG ----
   auto issue_row = [&](int L) {
-    if (tid >= 32) return;
+    if (tid != 0) return;
+    const int jr = jb - 1 + L;
     long long cs;
-    const double* rb = row_src(a, jb - 1 + L, NP, cs);
+    const double* rb = row_src(a, jr, NP, cs);
     uint64_t* br = &bar[L % NSTG];
-    const int nsl = TXv + 2;
-    uint32_t tx = 0;  // bytes of this lane's copies, then summed over the warp
-    if (rb) {
-      for (int t = tid; t < 4 * nsl; t += 32) {
-        const int c = t / nsl, e = t - c * nsl;
-        if (slot_elem(e) < 0) continue;
-        const uintptr_t s0 = reinterpret_cast<uintptr_t>(rb + c * cs + (long long)slot_elem(e) * NP);
-        tx += (uint32_t)(((s0 + NP * 8 + 15) & ~uintptr_t(15)) - (s0 & ~uintptr_t(15)));
+    double* st = ring + (L % NSTG) * STGA;
+    if (!rb) { mbar_arrive_expect_tx(br, 0); return; }
+    if constexpr (H::SWZ) {
+      const CUtensorMap* mp = jr < 0 ? &maps.lo : (jr >= a.nrows ? &maps.hi : &maps.q);
+      const int y0 = (jr < 0 || jr >= a.nrows ? 0 : jr * a.nx) + i0 - 1;
+      uint32_t tx = 4u * NSL * 128u;
+      if (wrapW) tx += 4u * 128u;
+      if (wrapE) tx += 4u * 128u;
+      mbar_arrive_expect_tx(br, tx);
+      tma_load_3d(st, mp, 0, y0, 0, br);
+      double* fix = st + H::FIXO;
+      for (int c = 0; c < 4; ++c) {
+        if (wrapW) tma_load_1d(fix + (0 * 4 + c) * 16, rb + c * cs + (long long)iw * NP, NP * 8, br);
+        if (wrapE) tma_load_1d(fix + (1 * 4 + c) * 16, rb + c * cs + (long long)ie * NP, NP * 8, br);
+      }
+    } else {
+      uint32_t tx = 0;
+      for (int c = 0; c < 4; ++c) {
+        const double* comp = rb + c * cs;
+        tx += piece_bytes(comp + (long long)i0 * NP, TXv * NP);
+        if (!mirW) tx += piece_bytes(comp + (long long)iw * NP, NP);
+        if (!mirE) tx += piece_bytes(comp + (long long)ie * NP, NP);
+      }
+      mbar_arrive_expect_tx(br, tx);
+      for (int c = 0; c < 4; ++c) {
+        const double* comp = rb + c * cs;
+        double* dst = st + c * CREG;
+        const double* s1 = comp + (long long)i0 * NP;
+        tma_load_1d(dst + CW, piece_src(s1), piece_bytes(s1, TXv * NP), br);
+        if (!mirW) {
+          const double* s0 = comp + (long long)iw * NP;
+          tma_load_1d(dst, piece_src(s0), piece_bytes(s0, NP), br);
+        }
+        if (!mirE) {
+          const double* s2 = comp + (long long)ie * NP;
+          tma_load_1d(dst + CW + CM, piece_src(s2), piece_bytes(s2, NP), br);
+        }
       }
     }
-    tx = __reduce_add_sync(0xffffffffu, tx);
-    if (tid == 0) mbar_arrive_expect_tx(br, tx);
-    __syncwarp();
-    if (!rb) return;
-    double* st = ring + (L % NSTG) * 4 * NSL * NPS;
-    for (int t = tid; t < 4 * nsl; t += 32) {
-      const int c = t / nsl, e = t - c * nsl;
-      const int ge = slot_elem(e);
-      if (ge < 0) continue;
-      const double* src = rb + c * cs + (long long)ge * NP;
-      const uintptr_t s0 = reinterpret_cast<uintptr_t>(src);
-      const uintptr_t a0 = s0 & ~uintptr_t(15), a1 = (s0 + NP * 8 + 15) & ~uintptr_t(15);
-      tma_load_1d(st + (c * NSL + e) * NPS, reinterpret_cast<const void*>(a0), (uint32_t)(a1 - a0), br);
+  };
+
+  // ---- addressing of stage data: element slot e (0 W halo, 1..TXv own, TXv+1 E halo) ----
+  struct RowView {
+    const double* st;
+    int dW, dM, dE;  // 1-D path offsets
+    bool have;
+  };
+  auto view = [&](int L) {
+    RowView v;
+    long long cs;
+    const double* rb = row_src(a, jb - 1 + L, NP, cs);
+    v.st = ring + (L % NSTG) * STGA;
+    v.have = rb != nullptr;
+    v.dW = v.dM = v.dE = 0;
+    if (!H::SWZ && rb) {  // cs is a multiple of 2 doubles only for even NP; take each piece's own offset
+      v.dM = piece_off(rb + (long long)i0 * NP);
+      v.dW = piece_off(rb + (long long)iw * NP);
+      v.dE = piece_off(rb + (long long)ie * NP);
+    }
+    return v;
+  };
+  // value (c, p) of own element slot e = lx + 1 (hot path: no branches)
+  auto own_at = [&](const RowView& v, int c, int e, int p) -> double {
+    if constexpr (H::SWZ) {
+      const int r = c * NSL + e;
+      return v.st[r * 16 + ((((p >> 1) ^ (r & 7)) << 1) | (p & 1))];
+    } else {
+      return v.st[c * CREG + CW + v.dM + (e - 1) * NP + p];
     }
   };
-  // element data in a stage: slot e, component c -> pointer to point 0
-  auto elem = [&](int L, int c, int e, long long cs, const double* rb) -> const double* {
-    const double* st = ring + (L % NSTG) * 4 * NSL * NPS + (c * NSL + e) * NPS;
-    if (NP & 1) {  // odd element size: the copy started at the 16-byte boundary below
-      const uintptr_t s0 = reinterpret_cast<uintptr_t>(rb + c * cs + (long long)slot_elem(e) * NP);
-      return st + ((s0 >> 3) & 1);
+  auto any_at = [&](const RowView& v, int c, int e, int p) -> double {
+    if constexpr (H::SWZ) {
+      const double* fix = v.st + H::FIXO;
+      if (e == 0 && wrapW) return fix[(0 * 4 + c) * 16 + p];
+      if (e == TXv + 1 && wrapE) return fix[(1 * 4 + c) * 16 + p];
+      return own_at(v, c, e, p);
+    } else {
+      if (e == 0) return v.st[c * CREG + v.dW + p];
+      if (e == TXv + 1) return v.st[c * CREG + CW + CM + v.dE + p];
+      return own_at(v, c, e, p);
     }
-    return st;
   };
 
   for (int L = 0; L < NSTG && L < nload; ++L) issue_row(L);
@@ -201,28 +279,17 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB) gll_stage_kernel(
   for (int L = 0; L <= RBv; ++L) {
     mbar_wait(&bar[L % NSTG], (L / NSTG) & 1);
     mbar_wait(&bar[(L + 1) % NSTG], ((L + 1) / NSTG) & 1);
-    long long csc, csn;
-    const double* rbc = row_src(a, jb - 1 + L, NP, csc);
-    const double* rbn = row_src(a, jb + L, NP, csn);
+    const RowView vc = view(L), vn = view(L + 1);
     double* jSc = sJS + (L & 1) * TX * N * 4;        // S jumps of row L (written in step L-1)
     double* jSn = sJS + ((L + 1) & 1) * TX * N * 4;  // S jumps of row L+1 (written now)
     const long long jr = jb - 1 + L;                 // local strip row of this step
 
-    double q[4][N], fW[4], fE[4], jW[4], q0v[4][N];
+    double q[4][N], fW[4], fE[4], jW[4];
     if (L > 0 && own) {
-      const long long base = (jr * a.nx + i0 + lx) * NP + b * N;
-      if (a.q0) {  // q^n of the line, issued early (pointwise, HBM)
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
+      for (int c = 0; c < 4; ++c)
 #pragma unroll
-          for (int x = 0; x < N; ++x) q0v[c][x] = a.q0[c * a.cs + base + x];
-      }
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const double* e0 = elem(L, c, lx + 1, csc, rbc) + b * N;
-#pragma unroll
-        for (int x = 0; x < N; ++x) q[c][x] = e0[x];
-      }
+        for (int x = 0; x < N; ++x) q[c][x] = own_at(vc, c, lx + 1, b * N + x);
       // W face (computed by the element on its right) and the strip's last E face
       double qw[4] = {q[0][0], q[1][0], q[2][0], q[3][0]}, sw;
       double qe[4] = {q[0][N - 1], q[1][N - 1], q[2][N - 1], q[3][N - 1]}, se;
@@ -234,7 +301,7 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB) gll_stage_kernel(
       } else {
         double ql[4], fl[4], sl;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) ql[c] = elem(L, c, lx, csc, rbc)[b * N + N - 1];
+        for (int c = 0; c < 4; ++c) ql[c] = any_at(vc, c, lx, b * N + N - 1);
         node_eval<0>(ql, gm1, gam, fl, sl);
         rus(ql, fl, sl, qw, fW, sw, F);
       }
@@ -247,7 +314,7 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB) gll_stage_kernel(
         } else {
           double qr[4], fr[4], sr;
 #pragma unroll
-          for (int c = 0; c < 4; ++c) qr[c] = elem(L, c, TXv + 1, csc, rbc)[b * N];
+          for (int c = 0; c < 4; ++c) qr[c] = any_at(vc, c, TXv + 1, b * N);
           node_eval<0>(qr, gm1, gam, fr, sr);
           rus(qe, fE, se, qr, fr, sr, F);
         }
@@ -264,29 +331,21 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB) gll_stage_kernel(
     }
     // N faces of row L (line n-1): jumps for row L (jN) and for row L+1 (jS)
     if (own && b == N - 1) {
-      const bool hc = rbc != nullptr, hn = rbn != nullptr;
-      const double* ec[4];
-      const double* en[4];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        ec[c] = hc ? elem(L, c, lx + 1, csc, rbc) : nullptr;
-        en[c] = hn ? elem(L + 1, c, lx + 1, csn, rbn) : nullptr;
-      }
 #pragma unroll
       for (int x = 0; x < N; ++x) {
         double qd[4], gd[4], sd, qu[4], gu[4], su, Gf[4], j[4];
-        if (hc) {
+        if (vc.have) {
 #pragma unroll
-          for (int c = 0; c < 4; ++c) qd[c] = ec[c][(N - 1) * N + x];
+          for (int c = 0; c < 4; ++c) qd[c] = own_at(vc, c, lx + 1, (N - 1) * N + x);
           node_eval<1>(qd, gm1, gam, gd, sd);
         }
-        if (hn) {
+        if (vn.have) {
 #pragma unroll
-          for (int c = 0; c < 4; ++c) qu[c] = en[c][x];
+          for (int c = 0; c < 4; ++c) qu[c] = own_at(vn, c, lx + 1, x);
           node_eval<1>(qu, gm1, gam, gu, su);
         }
-        if (!hc) { for (int c = 0; c < 4; ++c) { qd[c] = qu[c]; gd[c] = gu[c]; } sd = su; }
-        if (!hn) { for (int c = 0; c < 4; ++c) { qu[c] = qd[c]; gu[c] = gd[c]; } su = sd; }
+        if (!vc.have) { for (int c = 0; c < 4; ++c) { qd[c] = qu[c]; gd[c] = gu[c]; } sd = su; }
+        if (!vn.have) { for (int c = 0; c < 4; ++c) { qu[c] = qd[c]; gu[c] = gd[c]; } su = sd; }
         rus(qd, gd, sd, qu, gu, su, Gf);
         if (L > 0) {
 #pragma unroll
@@ -301,6 +360,14 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB) gll_stage_kernel(
     __syncthreads();
 
     if (L > 0 && own) {
+      const long long base = (jr * a.nx + i0 + lx) * NP + b * N;
+      double q0v[4][N];
+      if (a.q0) {  // q^n of the line (pointwise, HBM)
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int x = 0; x < N; ++x) q0v[c][x] = a.q0[c * a.cs + base + x];
+      }
       double F[4], jE[4];
       ld4(sFW + ((lx + 1) * N + b) * 4, F);
 #pragma unroll
@@ -315,10 +382,6 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB) gll_stage_kernel(
           for (int c = 0; c < 4; ++c) fxl[c][x] = f[c];
         }
       }
-      const double* col[4];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) col[c] = elem(L, c, lx + 1, csc, rbc);
-      const long long base = (jr * a.nx + i0 + lx) * NP + b * N;
 #pragma unroll
       for (int x = 0; x < N; ++x) {
         double v[4] = {q[0][x], q[1][x], q[2][x], q[3][x]};
@@ -328,7 +391,7 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB) gll_stage_kernel(
           const double db = D[b * N + l];
           if (M == GM_CPR) {
 #pragma unroll
-            for (int c = 0; c < 4; ++c) dy[c] += db * col[c][l * N + x];
+            for (int c = 0; c < 4; ++c) dy[c] += db * own_at(vc, c, lx + 1, l * N + x);
           } else {
             double u[4];
             ld4(sG + ((lx * NP) + l * N + x) * 4, u);
@@ -378,12 +441,42 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB) gll_stage_kernel(
     }
     __syncthreads();  // stage L % NSTG and the face buffers are free again
     if (L + NSTG < nload) {
-      if (tid < 32) fence_proxy_async_smem();
+      if (tid == 0) fence_proxy_async_smem();
       issue_row(L + NSTG);
     }
   }
   if (a.lam) block_max_to(lam, a.lam, sm + H::ORD);
 }
+
+// ---- host: tensor maps (P3 path) ------------------------------------------------------
+namespace {
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// {16 points, nelem elements, 4 components} fp64, box {16, box_e, 4}, 128-byte swizzle
+bool make_map(CUtensorMap* m, const double* base, long long nelem, long long cs, int box_e) {
+  memset(m, 0, sizeof(*m));
+  if (!base) return true;  // transmissive boundary: never used
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {16, (cuuint64_t)nelem, 4};
+  cuuint64_t strides[2] = {16 * sizeof(double), (cuuint64_t)cs * sizeof(double)};
+  cuuint32_t box[3] = {16, (cuuint32_t)box_e, 4};
+  cuuint32_t es[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+}  // namespace
 
 template <int M, int K>
 static int launch_g(const StageArgs& a, cudaStream_t s) {
@@ -394,8 +487,16 @@ static int launch_g(const StageArgs& a, cudaStream_t s) {
     attr = true;
   }
   static const GTab tab = make_gtab<K>();
+  GMaps maps;
+  memset(&maps, 0, sizeof(maps));
+  if (H::SWZ) {
+    const long long nel = (long long)a.nx * a.nrows;
+    if (!make_map(&maps.q, a.q, nel, a.cs, H::NSL) || !make_map(&maps.lo, a.ghost_lo, a.nx, a.gcs, H::NSL) ||
+        !make_map(&maps.hi, a.ghost_hi, a.nx, a.gcs, H::NSL))
+      return (int)cudaErrorInvalidValue;
+  }
   dim3 grid((a.nx + H::TX - 1) / H::TX, (a.nrows + H::RB - 1) / H::RB);
-  gll_stage_kernel<M, K><<<grid, H::NT, H::SMEM, s>>>(a, tab);
+  gll_stage_kernel<M, K><<<grid, H::NT, H::SMEM, s>>>(a, tab, maps);
   return (int)cudaPeekAtLastError();
 }
 

@@ -1,8 +1,11 @@
-// tma.cuh -- minimal sm_90+/sm_100a bulk-copy (TMA, cp.async.bulk) and mbarrier
-// helpers: one elected thread streams contiguous global segments into shared
-// memory; consumers wait on the mbarrier's phase parity.
+// tma.cuh -- minimal sm_90+/sm_100a TMA helpers: bulk copies (cp.async.bulk),
+// tensor-map tile copies (cp.async.bulk.tensor) and mbarrier waits.  One
+// elected thread streams global tiles into shared memory; consumers wait on the
+// mbarrier's phase parity.
 #pragma once
 #include <cstdint>
+
+#include <cuda.h>
 
 namespace h2d {
 
@@ -46,7 +49,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
-// bytes: multiple of 16; dst, src 16-byte aligned
+// 1-D bulk copy; bytes multiple of 16; dst, src 16-byte aligned
 __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   uint64_t g;
   asm volatile("cvta.to.global.u64 %0, %1;" : "=l"(g) : "l"(src));
@@ -54,6 +57,15 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
                    smem_u32(dst)),
                "l"(g), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
+}
+
+// 3-D tensor-map tile copy (box and swizzle fixed by the map)
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
 }
 
 }  // namespace h2d
