@@ -71,7 +71,7 @@ struct G {
   static constexpr int ORD = OT + ((N * N + 2 * N + 1) & ~1);
   static constexpr int OB = ORD + 32;                 // mbarriers (as doubles)
   static constexpr int TOTAL = OB + NSTG;
-  static constexpr size_t SMEM = TOTAL * sizeof(double) + 1024;  // + alignment slack
+  static constexpr size_t SMEM = TOTAL * sizeof(double);
 };
 
 struct GTab {
@@ -145,8 +145,8 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
   using H = G<M, K>;
   constexpr int N = H::N, NP = H::NP, TX = H::TX, RB = H::RB, NT = H::NT, NSL = H::NSL;
   constexpr int CW = H::CW, CM = H::CM, CREG = H::CREG, STGA = H::STGA;
-  extern __shared__ double4 smem4[];
-  double* sm = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(smem4) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) double4 smem4[];  // no static smem: the window base is 1024-B aligned
+  double* sm = reinterpret_cast<double*>(smem4);
   double* ring = sm + H::OR_;
   double* sFW = sm + H::OFW;
   double* sJN = sm + H::OJN;
@@ -230,7 +230,8 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
   // ---- addressing of stage data: element slot e (0 W halo, 1..TXv own, TXv+1 E halo) ----
   struct RowView {
     const double* st;
-    int dW, dM, dE;  // 1-D path offsets
+    int dW, dM, dE;  // 1-D path offsets of component 0 (odd component strides flip them)
+    int csodd;
     bool have;
   };
   auto view = [&](int L) {
@@ -240,7 +241,8 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
     v.st = ring + (L % NSTG) * STGA;
     v.have = rb != nullptr;
     v.dW = v.dM = v.dE = 0;
-    if (!H::SWZ && rb) {  // cs is a multiple of 2 doubles only for even NP; take each piece's own offset
+    v.csodd = (int)(cs & 1);
+    if (!H::SWZ && rb) {
       v.dM = piece_off(rb + (long long)i0 * NP);
       v.dW = piece_off(rb + (long long)iw * NP);
       v.dE = piece_off(rb + (long long)ie * NP);
@@ -253,7 +255,7 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
       const int r = c * NSL + e;
       return v.st[r * 16 + ((((p >> 1) ^ (r & 7)) << 1) | (p & 1))];
     } else {
-      return v.st[c * CREG + CW + v.dM + (e - 1) * NP + p];
+      return v.st[c * CREG + CW + (v.dM ^ (c & v.csodd)) + (e - 1) * NP + p];
     }
   };
   auto any_at = [&](const RowView& v, int c, int e, int p) -> double {
@@ -263,8 +265,8 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
       if (e == TXv + 1 && wrapE) return fix[(1 * 4 + c) * 16 + p];
       return own_at(v, c, e, p);
     } else {
-      if (e == 0) return v.st[c * CREG + v.dW + p];
-      if (e == TXv + 1) return v.st[c * CREG + CW + CM + v.dE + p];
+      if (e == 0) return v.st[c * CREG + (v.dW ^ (c & v.csodd)) + p];
+      if (e == TXv + 1) return v.st[c * CREG + CW + CM + (v.dE ^ (c & v.csodd)) + p];
       return own_at(v, c, e, p);
     }
   };
@@ -329,10 +331,11 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
         }
       }
     }
-    // N faces of row L (line n-1): jumps for row L (jN) and for row L+1 (jS)
-    if (own && b == N - 1) {
-#pragma unroll
-      for (int x = 0; x < N; ++x) {
+    // N faces of row L, column x = b of each element (spread over the lines, no
+    // divergence): jumps for row L (jN) and for row L+1 (jS)
+    if (own) {
+      {
+        const int x = b;
         double qd[4], gd[4], sd, qu[4], gu[4], su, Gf[4], j[4];
         if (vc.have) {
 #pragma unroll
