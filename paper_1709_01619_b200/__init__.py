@@ -15,7 +15,8 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libhom2d.so")
+# HOM2D_LIB selects an alternative in-tree build (A/B timing of kernel variants)
+LIB_PATH = os.environ.get("HOM2D_LIB") or os.path.join(HERE, "libhom2d.so")
 
 FV, CPR, DG, NDG, SD = 0, 1, 2, 3, 4
 PERIODIC, TRANSMISSIVE = 0, 1

@@ -49,20 +49,27 @@ def stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not stale():
+def build(force: bool = False, verbose: bool = False, out: str = LIB, extra=()) -> str:
+    """Compile all csrc/*.cu into `out` (variants for A/B timing: out + extra -D flags)."""
+    if out == LIB and not force and not stale():
         return LIB
     nd = nccl_dir()
-    cmd = [NVCC, *ARCH, *FLAGS, "-I", os.path.join(ROOT, "include"), "-I", os.path.join(nd, "include"), "-o", LIB,
+    cmd = [NVCC, *ARCH, *FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-I", os.path.join(nd, "include"),
+           "-o", out,
            *sources(), "-L", os.path.join(nd, "lib"), "-l:libnccl.so.2", "-Xlinker",
            "-rpath=" + os.path.join(nd, "lib")]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), flush=True)
     subprocess.check_call(cmd)
-    return LIB
+    return out
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(LIB)
+    # python -m paper_1709_01619_b200.build [--force] [-v] [--out PATH -DNAME=VAL ...]
+    args = sys.argv[1:]
+    out = LIB
+    if "--out" in args:
+        out = os.path.abspath(args[args.index("--out") + 1])
+    extra = [a for a in args if a.startswith("-D")]
+    print(build(force="--force" in args, verbose="-v" in args, out=out, extra=extra))

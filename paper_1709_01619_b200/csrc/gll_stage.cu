@@ -38,7 +38,10 @@ namespace {
 template <int K> struct GTile;
 template <> struct GTile<1> { static constexpr int TX = 64, RB = 64, MINB = 2; };  // 128 threads
 template <> struct GTile<2> { static constexpr int TX = 32, RB = 64, MINB = 2; };  //  96 threads
-template <> struct GTile<3> { static constexpr int TX = 32, RB = 64, MINB = 2; };  // 128 threads
+#ifndef H2D_MINB3
+#define H2D_MINB3 2
+#endif
+template <> struct GTile<3> { static constexpr int TX = 32, RB = 64, MINB = H2D_MINB3; };  // 128 threads
 template <> struct GTile<4> { static constexpr int TX = 32, RB = 64, MINB = 1; };  // 160 threads
 
 enum { GM_CPR = 1, GM_NDG = 3 };
@@ -58,8 +61,11 @@ struct G {
   static constexpr int CW = (NP + 1 + 1) & ~1;
   static constexpr int CM = ((TX * NP + 1) + 1) & ~1;
   static constexpr int CREG = CW + CM + CW;
-  // per stage (doubles): SWZ: 4 * NSL rows of 16 (+ 8 unswizzled fix-up rows); else 4 * CREG
-  static constexpr int FIXO = (4 * NSL * 16 + 127) & ~127;
+  // per stage (doubles): SWZ: 4 components x RSW rows of 16, each component at a
+  // 1024-B boundary so the swizzle phase of a slot is (slot & 7) for every
+  // component (+ 8 unswizzled fix-up rows); else 4 * CREG
+  static constexpr int RSW = (NSL + 7) & ~7;
+  static constexpr int FIXO = 4 * RSW * 16;
   static constexpr int STG = SWZ ? FIXO + 8 * 16 : 4 * CREG;
   static constexpr int STGA = (STG + 127) & ~127;    // 1024-byte aligned stages
   static constexpr int OR_ = 0;
@@ -195,7 +201,7 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
       if (wrapW) tx += 4u * 128u;
       if (wrapE) tx += 4u * 128u;
       mbar_arrive_expect_tx(br, tx);
-      tma_load_3d(st, mp, 0, y0, 0, br);
+      for (int c = 0; c < 4; ++c) tma_load_3d(st + c * H::RSW * 16, mp, 0, y0, c, br);
       double* fix = st + H::FIXO;
       for (int c = 0; c < 4; ++c) {
         if (wrapW) tma_load_1d(fix + (0 * 4 + c) * 16, rb + c * cs + (long long)iw * NP, NP * 8, br);
@@ -251,9 +257,8 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
   };
   // value (c, p) of own element slot e = lx + 1 (hot path: no branches)
   auto own_at = [&](const RowView& v, int c, int e, int p) -> double {
-    if constexpr (H::SWZ) {
-      const int r = c * NSL + e;
-      return v.st[r * 16 + ((((p >> 1) ^ (r & 7)) << 1) | (p & 1))];
+    if constexpr (H::SWZ) {  // 128-B swizzle: 16-B chunk (p >> 1) of row e sits at chunk (p >> 1) ^ (e & 7)
+      return v.st[(c * H::RSW + e) * 16 + ((((p >> 1) ^ (e & 7)) << 1) | (p & 1))];
     } else {
       return v.st[c * CREG + CW + (v.dM ^ (c & v.csodd)) + (e - 1) * NP + p];
     }
@@ -465,7 +470,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// {16 points, nelem elements, 4 components} fp64, box {16, box_e, 4}, 128-byte swizzle
+// {16 points, nelem elements, 4 components} fp64, box {16, box_e, 1}, 128-byte swizzle
 bool make_map(CUtensorMap* m, const double* base, long long nelem, long long cs, int box_e) {
   memset(m, 0, sizeof(*m));
   if (!base) return true;  // transmissive boundary: never used
@@ -473,7 +478,7 @@ bool make_map(CUtensorMap* m, const double* base, long long nelem, long long cs,
   if (!fn) return false;
   cuuint64_t dims[3] = {16, (cuuint64_t)nelem, 4};
   cuuint64_t strides[2] = {16 * sizeof(double), (cuuint64_t)cs * sizeof(double)};
-  cuuint32_t box[3] = {16, (cuuint32_t)box_e, 4};
+  cuuint32_t box[3] = {16, (cuuint32_t)box_e, 1};  // one component per copy
   cuuint32_t es[3] = {1, 1, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
