@@ -260,7 +260,8 @@ def main():
     achieved = ndof_local * (BYTES_PER_DOF_STEP / 3.0) / (stage_avg_ms * 1e-3) / 1e9
     tr = traffic_from_profiles(wl)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": tr, "peak_source": peak_src, "kernel": f"ho_stage_kernel<{method},{k}>",
+                "traffic": tr, "peak_source": peak_src, "kernel": (f"gll_stage_kernel<{method},{k}>" if method in ("cpr", "ndg") else
+                           f"fv_stage_kernel<{k}>" if method == "fv" else f"ho_stage_kernel<{method},{k}>"),
                 "stage_avg_ms": stage_avg_ms, "bytes_per_launch": ndof_local * BYTES_PER_DOF_STEP / 3.0,
                 "stage_share_of_step": 3 * stage_avg_ms / (ms / args.steps)}
 

@@ -83,6 +83,19 @@ typedef struct {
   void* cuda_stream;          /* cudaStream_t, borrowed; NULL = default stream */
 } hom2d_dist;
 
+/* Host-only (no CUDA): the y-strip partition of rank `rank` of `nranks` and its
+ * per-stage halo exchange plan.  Rows are element (FV: cell) rows.  The ghost
+ * rows below the strip come from `peer_lo` (its last `ghost_rows` rows), the
+ * ghost rows above from `peer_hi` (its first `ghost_rows` rows); has_lo/has_hi
+ * = 0 at a physical transmissive boundary (no exchange).  row_values = values
+ * of one row of one component (nx * points per element). */
+typedef struct {
+  int32_t row0, nrows, ghost_rows;
+  int32_t peer_lo, peer_hi, has_lo, has_hi;
+  int64_t row_values;
+} hom2d_strip_plan_t;
+hom2d_status hom2d_strip_plan(const hom2d_config* cfg, int32_t rank, int32_t nranks, hom2d_strip_plan_t* out);
+
 /* Bytes of device workspace hom2d_create needs for this config/partition. */
 hom2d_status hom2d_workspace_bytes(const hom2d_config* cfg, const hom2d_dist* dist, size_t* bytes);
 

@@ -26,7 +26,7 @@ STATUS = {0: "OK", 1: "ERR_ARG", 2: "ERR_MESH", 3: "ERR_ORDER", 4: "ERR_NONPHYSI
           6: "ERR_NCCL", 7: "ERR_NOMEM", 8: "ERR_STATE"}
 
 # every symbol include/hom2d.h declares
-EXPORTS = ["hom2d_workspace_bytes", "hom2d_nccl_unique_id", "hom2d_create", "hom2d_local_extent",
+EXPORTS = ["hom2d_strip_plan", "hom2d_workspace_bytes", "hom2d_nccl_unique_id", "hom2d_create", "hom2d_local_extent",
            "hom2d_set_state", "hom2d_get_state", "hom2d_init_case", "hom2d_residual", "hom2d_limit",
            "hom2d_compute_dt", "hom2d_step", "hom2d_error", "hom2d_time", "hom2d_decisions",
            "hom2d_launch_count", "hom2d_stage_timing", "hom2d_stage_time", "hom2d_last_error", "hom2d_destroy"]
@@ -53,6 +53,12 @@ class Config(C.Structure):
     ]
 
 
+class StripPlan(C.Structure):
+    _fields_ = [("row0", C.c_int32), ("nrows", C.c_int32), ("ghost_rows", C.c_int32),
+                ("peer_lo", C.c_int32), ("peer_hi", C.c_int32), ("has_lo", C.c_int32), ("has_hi", C.c_int32),
+                ("row_values", C.c_int64)]
+
+
 class Dist(C.Structure):
     _fields_ = [("rank", C.c_int32), ("nranks", C.c_int32), ("device", C.c_int32),
                 ("nccl_id", C.c_void_p), ("cuda_stream", C.c_void_p)]
@@ -71,6 +77,7 @@ def load(path: str = LIB_PATH):
         raise RuntimeError(f"libhom2d.so not built ({path}); run `python -m paper_1709_01619_b200.build`")
     L = C.CDLL(path)
     i32, i64, d, vp, P = C.c_int32, C.c_int64, C.c_double, C.c_void_p, C.POINTER
+    L.hom2d_strip_plan.argtypes = [P(Config), i32, i32, P(StripPlan)]
     L.hom2d_workspace_bytes.argtypes = [P(Config), P(Dist), P(C.c_size_t)]
     L.hom2d_nccl_unique_id.argtypes = [vp]
     L.hom2d_create.argtypes = [P(Config), P(Dist), vp, C.c_size_t, P(vp)]
@@ -105,6 +112,15 @@ def make_config(nx, ny, method="cpr", k=1, bc=PERIODIC, box=(-5.0, 5.0, -5.0, 5.
     m = METHODS[method] if isinstance(method, str) else int(method)
     return Config(nx, ny, box[0], box[1], box[2], box[3], bc, m, k, gamma, cfl, limiter, limiter_eps,
                   cpr_chain_rule, record_decisions)
+
+
+def strip_plan(cfg: Config, rank: int, nranks: int) -> StripPlan:
+    """Host-only y-strip partition and halo plan of one rank (no CUDA)."""
+    out = StripPlan()
+    st = load().hom2d_strip_plan(C.byref(cfg), int(rank), int(nranks), C.byref(out))
+    if st:
+        raise Hom2dError(st, "strip_plan")
+    return out
 
 
 def nccl_unique_id() -> bytes:

@@ -139,11 +139,24 @@ AuxArgs aux(const hom2d* h) {
   return a;
 }
 
-bool has_lo(const hom2d* h) { return h->cfg.bc == HOM2D_PERIODIC || h->rank > 0; }
-bool has_hi(const hom2d* h) { return h->cfg.bc == HOM2D_PERIODIC || h->rank < h->nranks - 1; }
+hom2d_strip_plan_t plan_of(const hom2d_config& c, int rank, int R) {
+  hom2d_strip_plan_t p;
+  p.nrows = c.ny / R;
+  p.row0 = rank * p.nrows;
+  p.ghost_rows = c.method == HOM2D_FV ? 2 : 1;
+  p.peer_lo = (rank + R - 1) % R;
+  p.peer_hi = (rank + 1) % R;
+  p.has_lo = (c.bc == HOM2D_PERIODIC || rank > 0) ? 1 : 0;
+  p.has_hi = (c.bc == HOM2D_PERIODIC || rank < R - 1) ? 1 : 0;
+  p.row_values = (int64_t)c.nx * points_per_elem(c);
+  return p;
+}
 
 // Exchange G boundary rows of the stage input X with the strip neighbours and
-// return the ghost pointers the stage kernel reads (y-strip partition, P:L6).
+// return the ghost pointers the stage kernel reads (y-strip partition).
+// Message order per peer: "last rows -> peer_hi" before "first rows -> peer_lo"
+// and "recv lo" before "recv hi", so that with 2 periodic ranks (peer_lo ==
+// peer_hi) NCCL's in-order matching pairs last->lo and first->hi.
 hom2d_status exchange(hom2d* h, const double* X, long long comp_stride, long long row_vals, const double** lo,
                       const double** hi, long long* gcs, double* rlo, double* rhi, int G) {
   const int R = h->nranks;
@@ -153,23 +166,19 @@ hom2d_status exchange(hom2d* h, const double* X, long long comp_stride, long lon
     *hi = (h->cfg.bc == HOM2D_PERIODIC) ? X : nullptr;
     return HOM2D_OK;
   }
+  const hom2d_strip_plan_t P = plan_of(h->cfg, h->rank, R);
   const long long cnt = (long long)G * row_vals;
-  const int prev = (h->rank + R - 1) % R, next = (h->rank + 1) % R;
-  const bool lo_ok = has_lo(h), hi_ok = has_hi(h);
   NC(h, ncclGroupStart());
   for (int c = 0; c < 4; ++c) {
     const double* first = X + c * comp_stride;
     const double* last = X + c * comp_stride + (long long)(h->nrows - G) * row_vals;
-    if (lo_ok) {
-      NC(h, ncclSend(first, cnt, ncclDouble, prev, h->comm, h->stream));
-      NC(h, ncclRecv(rlo + c * cnt, cnt, ncclDouble, prev, h->comm, h->stream));
-    }
-    if (hi_ok) {
-      NC(h, ncclSend(last, cnt, ncclDouble, next, h->comm, h->stream));
-      NC(h, ncclRecv(rhi + c * cnt, cnt, ncclDouble, next, h->comm, h->stream));
-    }
+    if (P.has_hi) NC(h, ncclSend(last, cnt, ncclDouble, P.peer_hi, h->comm, h->stream));
+    if (P.has_lo) NC(h, ncclSend(first, cnt, ncclDouble, P.peer_lo, h->comm, h->stream));
+    if (P.has_lo) NC(h, ncclRecv(rlo + c * cnt, cnt, ncclDouble, P.peer_lo, h->comm, h->stream));
+    if (P.has_hi) NC(h, ncclRecv(rhi + c * cnt, cnt, ncclDouble, P.peer_hi, h->comm, h->stream));
   }
   NC(h, ncclGroupEnd());
+  const bool lo_ok = P.has_lo, hi_ok = P.has_hi;
   *gcs = cnt;
   *lo = lo_ok ? rlo : nullptr;
   *hi = hi_ok ? rhi : nullptr;
@@ -256,6 +265,14 @@ hom2d_status reset_clock(hom2d* h, double t0) {
 }  // namespace
 
 extern "C" {
+
+hom2d_status hom2d_strip_plan(const hom2d_config* cfg, int32_t rank, int32_t nranks, hom2d_strip_plan_t* out) {
+  hom2d_status st = check_cfg(cfg, nranks);
+  if (st) return st;
+  if (!out || rank < 0 || rank >= nranks) return HOM2D_ERR_ARG;
+  *out = plan_of(*cfg, rank, nranks);
+  return HOM2D_OK;
+}
 
 hom2d_status hom2d_workspace_bytes(const hom2d_config* cfg, const hom2d_dist* dist, size_t* bytes) {
   const int R = dist ? dist->nranks : 1;
