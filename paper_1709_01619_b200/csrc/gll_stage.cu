@@ -76,9 +76,27 @@ struct G {
   static constexpr int OT = OG + (M == GM_NDG ? TX * NP * 4 : 0);
   static constexpr int ORD = OT + ((N * N + 2 * N + 1) & ~1);
   static constexpr int OB = ORD + 32;                 // mbarriers (as doubles)
-  static constexpr int TOTAL = OB + NSTG;
+  static constexpr int LP = (N + 1) & ~1;             // q^n line slot (16-B multiple)
+  static constexpr int OQ0 = OB + ((NSTG + 1) & ~1);  // q^n prefetch [4][NT][LP], thread-private
+  static constexpr int TOTAL = OQ0 + 4 * NT * LP;
   static constexpr size_t SMEM = TOTAL * sizeof(double);
 };
+
+// cp.async (LDGSTS) of this thread's q^n line (4 components x N doubles) into its
+// private smem slots, one row ahead of its use
+template <int N, int NT, int LP>
+__device__ __forceinline__ void q0_prefetch(double* sq0, const double* q0, long long cs, long long base, int tid) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const double* s = q0 + c * cs + base;
+#pragma unroll
+    for (int x = 0; x < N; ++x)  // layout [c][x][thread]: conflict-free read-back
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(sq0 + (c * N + x) * NT + tid)),
+                   "l"(s + x)
+                   : "memory");
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
 
 struct GTab {
   double v[25 + 10];
@@ -160,6 +178,7 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
   double* sG = sm + H::OG;
   double* sT = sm + H::OT;
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + H::OB);
+  double* sQ0 = sm + H::OQ0;
 
   double dtv = 1.0;
   if (a.dt) {
@@ -277,6 +296,8 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
   };
 
   for (int L = 0; L < NSTG && L < nload; ++L) issue_row(L);
+  if (a.q0 && own)  // q^n of the first own row (step L = 1)
+    q0_prefetch<N, NT, H::LP>(sQ0, a.q0, a.cs, ((long long)jb * a.nx + i0 + lx) * NP + b * N, tid);
 
   const double* D = sT;
   const double gLb = sT[N * N + b], gRb = sT[N * N + N + b];
@@ -369,13 +390,9 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
 
     if (L > 0 && own) {
       const long long base = (jr * a.nx + i0 + lx) * NP + b * N;
-      double q0v[4][N];
-      if (a.q0) {  // q^n of the line (pointwise, HBM)
-#pragma unroll
-        for (int c = 0; c < 4; ++c)
-#pragma unroll
-          for (int x = 0; x < N; ++x) q0v[c][x] = a.q0[c * a.cs + base + x];
-      }
+      // q^n of the line: prefetched by cp.async one row ahead into thread-private smem
+      if (a.q0) asm volatile("cp.async.wait_group 0;" ::: "memory");
+#define Q0V(c, x) sQ0[((c) * N + (x)) * NT + tid]
       double F[4], jE[4];
       ld4(sFW + ((lx + 1) * N + b) * 4, F);
 #pragma unroll
@@ -439,13 +456,15 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
           const double gy = Gy[c] + gLb * jS[c] + gRb * jN[c];
           const double R = -a.rdx2 * fx - a.rdy2 * gy;
           double val = a.a1 * v[c] + bdt * R;
-          if (a.q0) val += a.a0 * q0v[c][x];
+          if (a.q0) val += a.a0 * Q0V(c, x);
           o[c] = val;
           a.out[c * a.cs + base + x] = val;
         }
         if (a.lam) lam = fmax(lam, wave_speed(o, gm1, gam));
         if (a.bad && nonphysical(o, gm1)) atomicMin(a.bad, (unsigned long long)(base + x));
       }
+      if (a.q0 && L < RBv)  // q^n of the next row into the (now consumed) private slots
+        q0_prefetch<N, NT, H::LP>(sQ0, a.q0, a.cs, base + (long long)a.nx * NP, tid);
     }
     __syncthreads();  // stage L % NSTG and the face buffers are free again
     if (L + NSTG < nload) {
