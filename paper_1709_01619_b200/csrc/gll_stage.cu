@@ -317,7 +317,18 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
 #pragma unroll
       for (int c = 0; c < 4; ++c)
 #pragma unroll
-        for (int x = 0; x < N; ++x) q[c][x] = own_at(vc, c, lx + 1, b * N + x);
+        for (int x = 0; x < N; ++x) {
+          if constexpr (H::SWZ) {  // 16-B chunks: points (4b + 2h, 4b + 2h + 1)
+            if ((x & 1) == 0) {
+              const double2 u = *reinterpret_cast<const double2*>(
+                  vc.st + (c * H::RSW + lx + 1) * 16 + (((2 * b + (x >> 1)) ^ ((lx + 1) & 7)) << 1));
+              q[c][x] = u.x;
+              q[c][x + 1] = u.y;
+            }
+          } else {
+            q[c][x] = own_at(vc, c, lx + 1, b * N + x);
+          }
+        }
       // W face (computed by the element on its right) and the strip's last E face
       double qw[4] = {q[0][0], q[1][0], q[2][0], q[3][0]}, sw;
       double qe[4] = {q[0][N - 1], q[1][N - 1], q[2][N - 1], q[3][N - 1]}, se;
@@ -397,6 +408,28 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
       ld4(sFW + ((lx + 1) * N + b) * 4, F);
 #pragma unroll
       for (int c = 0; c < 4; ++c) jE[c] = F[c] - fE[c];
+      // CPR P3: eta-derivatives of all points of the line at once, two points per
+      // 16-B swizzled chunk (half the shared-memory loads of a per-point loop)
+      double dyall[N][4];
+      if constexpr (M == GM_CPR && H::SWZ) {
+#pragma unroll
+        for (int x = 0; x < N; ++x)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) dyall[x][c] = 0.0;
+#pragma unroll
+        for (int l = 0; l < N; ++l) {
+          const double db = D[b * N + l];
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+#pragma unroll
+            for (int h = 0; h < N / 2; ++h) {
+              const double2 u = *reinterpret_cast<const double2*>(
+                  vc.st + (c * H::RSW + lx + 1) * 16 + (((2 * l + h) ^ ((lx + 1) & 7)) << 1));
+              dyall[2 * h][c] += db * u.x;
+              dyall[2 * h + 1][c] += db * u.y;
+            }
+        }
+      }
       double fxl[4][N];
       if (M == GM_NDG) {
 #pragma unroll
@@ -414,7 +447,12 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
 #pragma unroll
         for (int l = 0; l < N; ++l) {  // column x of the element (broadcast over its lines)
           const double db = D[b * N + l];
-          if (M == GM_CPR) {
+          if (M == GM_CPR && H::SWZ) {
+            if (l == 0) {
+#pragma unroll
+              for (int c = 0; c < 4; ++c) dy[c] = dyall[x][c];
+            }
+          } else if (M == GM_CPR) {
 #pragma unroll
             for (int c = 0; c < 4; ++c) dy[c] += db * own_at(vc, c, lx + 1, l * N + x);
           } else {
