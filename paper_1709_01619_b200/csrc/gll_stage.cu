@@ -466,7 +466,7 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
           double dx[4] = {0, 0, 0, 0};
 #pragma unroll
           for (int l = 0; l < N; ++l) {
-            const double da = D[x * N + l];
+            const double da = tab.v[x * N + l];  // compile-time index: constant-bank operand
 #pragma unroll
             for (int c = 0; c < 4; ++c) dx[c] += da * q[c][l];
           }
@@ -478,7 +478,7 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
           for (int c = 0; c < 4; ++c) {
             double s = 0.0;
 #pragma unroll
-            for (int l = 0; l < N; ++l) s += D[x * N + l] * fxl[c][l];
+            for (int l = 0; l < N; ++l) s += tab.v[x * N + l] * fxl[c][l];
             Fx[c] = s;
             Gy[c] = dy[c];
           }
@@ -486,7 +486,7 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
         double jS[4], jN[4];
         ld4(jSc + (lx * N + x) * 4, jS);
         ld4(sJN + (lx * N + x) * 4, jN);
-        const double gLa = sT[N * N + x], gRa = sT[N * N + N + x];
+        const double gLa = tab.v[N * N + x], gRa = tab.v[N * N + N + x];
         double o[4];
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
@@ -498,8 +498,12 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
           o[c] = val;
           a.out[c * a.cs + base + x] = val;
         }
-        if (a.lam) lam = fmax(lam, wave_speed(o, gm1, gam));
-        if (a.bad && nonphysical(o, gm1)) atomicMin(a.bad, (unsigned long long)(base + x));
+        if (a.lam || a.bad) {  // dt wave speed and non-physical check share one reciprocal
+          const Prim w = prims(o, gm1);
+          if (a.lam) lam = fmax(lam, fmax(fabs(w.u), fabs(w.v)) + fsqrt(gam * w.p * w.ri));
+          const bool fin = isfinite(o[0]) && isfinite(o[1]) && isfinite(o[2]) && isfinite(o[3]);
+          if (a.bad && (!fin || !(o[0] > 0.0) || !(w.p > 0.0))) atomicMin(a.bad, (unsigned long long)(base + x));
+        }
       }
       if (a.q0 && L < RBv)  // q^n of the next row into the (now consumed) private slots
         q0_prefetch<N, NT, H::LP>(sQ0, a.q0, a.cs, base + (long long)a.nx * NP, tid);
