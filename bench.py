@@ -37,6 +37,15 @@ WORKLOADS = {
     "cpr_p3_2048": ("cpr", 3, 2048, 2048, 0.08, False),   # BASELINE configs[2] (d3)
     "cpr_p2_8192w": ("cpr", 2, 8192, 1024, 0.13, True),   # configs[4], per-GPU strip (d5)
     "fv2_8192w": ("fv", 1, 8192, 1024, 0.37, True),       # configs[4], per-GPU strip (d5)
+    # per-method throughput at matched DOF (268M points; FV 16384^2 cells)
+    "ndg_p3_4096": ("ndg", 3, 4096, 4096, 0.08, False),
+    "dg_p3_4096": ("dg", 3, 4096, 4096, 0.08, False),
+    "sd_p3_4096": ("sd", 3, 4096, 4096, 0.10, False),
+    "cpr_p2_4096": ("cpr", 2, 4096, 4096, 0.13, False),
+    "cpr_p1_8192": ("cpr", 1, 8192, 8192, 0.24, False),
+    "cpr_p4_4096": ("cpr", 4, 4096, 4096, 0.05, False),
+    "fv2_16384": ("fv", 1, 16384, 16384, 0.37, False),
+    "fv3_16384": ("fv", 2, 16384, 16384, 0.37, False),
 }
 BYTES_PER_DOF_STEP = 256.0   # algorithmic HBM bytes: stage 1 64 B, stages 2/3 96 B
 

@@ -124,6 +124,15 @@ hom2d_status hom2d_init_case(hom2d* h, int32_t case_id);
 /* r = R(q), the spatial residual dq/dt of one RK stage (tests; device pointers). */
 hom2d_status hom2d_residual(hom2d* h, const double* q_dev, double* r_dev);
 
+/* Residual of the local strip with caller-supplied neighbour rows (device
+ * pointers, layout [4][ghost_rows][nx * np], NULL = physical transmissive
+ * boundary): exactly the kernel path a multi-GPU stage takes after its halo
+ * exchange.  Needs nranks > 1; such a handle may be created WITHOUT an NCCL id
+ * ("strip-only": collectives are then skipped), which lets one GPU check the
+ * strip decomposition against the whole-grid residual. */
+hom2d_status hom2d_residual_strip(hom2d* h, const double* q_dev, const double* ghost_lo_dev,
+                                  const double* ghost_hi_dev, double* r_dev);
+
 /* Apply the HO limiter (Eq. (35), Algs. 9-11) in place to the current state. */
 hom2d_status hom2d_limit(hom2d* h);
 

@@ -27,7 +27,7 @@ STATUS = {0: "OK", 1: "ERR_ARG", 2: "ERR_MESH", 3: "ERR_ORDER", 4: "ERR_NONPHYSI
 
 # every symbol include/hom2d.h declares
 EXPORTS = ["hom2d_strip_plan", "hom2d_workspace_bytes", "hom2d_nccl_unique_id", "hom2d_create", "hom2d_local_extent",
-           "hom2d_set_state", "hom2d_get_state", "hom2d_init_case", "hom2d_residual", "hom2d_limit",
+           "hom2d_set_state", "hom2d_get_state", "hom2d_init_case", "hom2d_residual", "hom2d_residual_strip", "hom2d_limit",
            "hom2d_compute_dt", "hom2d_step", "hom2d_error", "hom2d_time", "hom2d_decisions",
            "hom2d_launch_count", "hom2d_stage_timing", "hom2d_stage_time", "hom2d_last_error", "hom2d_destroy"]
 
@@ -86,6 +86,7 @@ def load(path: str = LIB_PATH):
     L.hom2d_get_state.argtypes = [vp, vp, i64, i32]
     L.hom2d_init_case.argtypes = [vp, i32]
     L.hom2d_residual.argtypes = [vp, vp, vp]
+    L.hom2d_residual_strip.argtypes = [vp, vp, vp, vp, vp]
     L.hom2d_limit.argtypes = [vp]
     L.hom2d_compute_dt.argtypes = [vp, P(d)]
     L.hom2d_step.argtypes = [vp, i32, d, P(d), P(i64)]
@@ -202,6 +203,15 @@ class Solver:
         assert q.is_cuda and q.dtype == torch.float64 and q.is_contiguous() and q.numel() == self.n_values
         r = torch.empty_like(q)
         self._check(self._L.hom2d_residual(self.h, C.c_void_p(q.data_ptr()), C.c_void_p(r.data_ptr())))
+        return r
+
+    def residual_strip(self, q, ghost_lo=None, ghost_hi=None):
+        """R(q) of the local strip with explicit neighbour rows (device tensors)."""
+        import torch
+        assert q.is_cuda and q.dtype == torch.float64 and q.is_contiguous() and q.numel() == self.n_values
+        r = torch.empty_like(q)
+        ptr = lambda t: C.c_void_p(t.data_ptr()) if t is not None else None  # noqa: E731
+        self._check(self._L.hom2d_residual_strip(self.h, ptr(q), ptr(ghost_lo), ptr(ghost_hi), ptr(r)))
         return r
 
     def limit(self):

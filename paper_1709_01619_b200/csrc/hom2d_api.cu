@@ -34,6 +34,8 @@ struct hom2d {
   double *glo = nullptr, *ghi = nullptr;   // received ghost rows [4][G*nx*np]
   double *qblo = nullptr, *qbhi = nullptr; // received ghost average rows [4][nx]
   double* t_host = nullptr;
+  bool ovr_active = false;                 // hom2d_residual_strip ghost override
+  const double *ovr_lo = nullptr, *ovr_hi = nullptr;
   bool poisoned = false;
   long long launches = 0;
   std::vector<cudaEvent_t> ev;             // stage-kernel timing: pairs (start, stop)
@@ -160,12 +162,19 @@ hom2d_strip_plan_t plan_of(const hom2d_config& c, int rank, int R) {
 hom2d_status exchange(hom2d* h, const double* X, long long comp_stride, long long row_vals, const double** lo,
                       const double** hi, long long* gcs, double* rlo, double* rhi, int G) {
   const int R = h->nranks;
+  if (h->ovr_active) {  // hom2d_residual_strip: caller-supplied ghost rows
+    *gcs = (long long)G * row_vals;
+    *lo = h->ovr_lo;
+    *hi = h->ovr_hi;
+    return HOM2D_OK;
+  }
   if (R == 1) {
     *gcs = comp_stride;
     *lo = (h->cfg.bc == HOM2D_PERIODIC) ? X + (long long)(h->nrows - G) * row_vals : nullptr;
     *hi = (h->cfg.bc == HOM2D_PERIODIC) ? X : nullptr;
     return HOM2D_OK;
   }
+  if (!h->comm) return fail(h, HOM2D_ERR_STATE, "strip-only handle (created without an NCCL id)");
   const hom2d_strip_plan_t P = plan_of(h->cfg, h->rank, R);
   const long long cnt = (long long)G * row_vals;
   NC(h, ncclGroupStart());
@@ -236,7 +245,7 @@ hom2d_status run_limiter(hom2d* h, double* X, const double* dt = nullptr) {
 }
 
 hom2d_status allreduce_max_lam(hom2d* h) {
-  if (h->nranks > 1) NC(h, ncclAllReduce(h->lam, h->lam, 1, ncclUint64, ncclMax, h->comm, h->stream));
+  if (h->nranks > 1 && h->comm) NC(h, ncclAllReduce(h->lam, h->lam, 1, ncclUint64, ncclMax, h->comm, h->stream));
   return HOM2D_OK;
 }
 
@@ -318,8 +327,7 @@ hom2d_status hom2d_create(const hom2d_config* cfg, const hom2d_dist* dist, void*
   if (ce != cudaSuccess) { delete h; return HOM2D_ERR_CUDA; }
   carve(h, *cfg, R, (char*)workspace);
   if (cudaMallocHost(&h->t_host, 8 * sizeof(double)) != cudaSuccess) { delete h; return HOM2D_ERR_CUDA; }
-  if (R > 1) {
-    if (!dist->nccl_id) { cudaFreeHost(h->t_host); delete h; return HOM2D_ERR_ARG; }
+  if (R > 1 && dist->nccl_id) {  // (no id: strip-only handle, see hom2d_residual_strip)
     ncclUniqueId id;
     memcpy(&id, dist->nccl_id, sizeof(id));
     if (ncclCommInitRank(&h->comm, R, id, h->rank) != ncclSuccess) { cudaFreeHost(h->t_host); delete h; return HOM2D_ERR_NCCL; }
@@ -387,6 +395,28 @@ hom2d_status hom2d_residual(hom2d* h, const double* q_dev, double* r_dev) {
   if (st) return st;
   CU(h, cudaMemcpyAsync(r_dev, h->Q2, 4 * h->nloc * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
   if (st) return st;
+  CU(h, cudaStreamSynchronize(h->stream));
+  return HOM2D_OK;
+}
+
+hom2d_status hom2d_residual_strip(hom2d* h, const double* q_dev, const double* ghost_lo_dev,
+                                  const double* ghost_hi_dev, double* r_dev) {
+  GUARD(h);
+  if (!q_dev || !r_dev) return fail(h, HOM2D_ERR_ARG, "residual_strip: null pointer");
+  const long long gvals = 4LL * h->G * h->cfg.nx * h->np;
+  if (!h->glo || !h->ghi) return fail(h, HOM2D_ERR_STATE, "residual_strip needs a handle with nranks > 1");
+  CU(h, cudaMemcpyAsync(h->Q1, q_dev, 4 * h->nloc * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+  if (ghost_lo_dev)
+    CU(h, cudaMemcpyAsync(h->glo, ghost_lo_dev, gvals * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+  if (ghost_hi_dev)
+    CU(h, cudaMemcpyAsync(h->ghi, ghost_hi_dev, gvals * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+  h->ovr_active = true;
+  h->ovr_lo = ghost_lo_dev ? h->glo : nullptr;
+  h->ovr_hi = ghost_hi_dev ? h->ghi : nullptr;
+  hom2d_status st = run_stage(h, h->Q1, nullptr, h->Q2, 0.0, 0.0, 1.0, nullptr, nullptr, nullptr);
+  h->ovr_active = false;
+  if (st) return st;
+  CU(h, cudaMemcpyAsync(r_dev, h->Q2, 4 * h->nloc * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
   CU(h, cudaStreamSynchronize(h->stream));
   return HOM2D_OK;
 }
@@ -478,7 +508,7 @@ hom2d_status hom2d_error(hom2d* h, int32_t case_id, int32_t var, double* l1, dou
   launch_error_final(h->part, nb, h->err3, h->stream);
   h->launches += 2;
   CU(h, cudaPeekAtLastError());
-  if (h->nranks > 1) {
+  if (h->nranks > 1 && h->comm) {
     NC(h, ncclAllReduce(h->err3, h->err3, 2, ncclDouble, ncclSum, h->comm, h->stream));
     NC(h, ncclAllReduce(h->err3 + 2, h->err3 + 2, 1, ncclDouble, ncclMax, h->comm, h->stream));
   }
@@ -507,7 +537,7 @@ hom2d_status hom2d_decisions(hom2d* h, int64_t* counts8) {
   if (!counts8) return HOM2D_ERR_ARG;
   CU(h, cudaMemcpyAsync(counts8, h->dec, 8 * sizeof(long long), cudaMemcpyDeviceToHost, h->stream));
   CU(h, cudaStreamSynchronize(h->stream));
-  if (h->nranks > 1) {  // sum over ranks through the device scratch
+  if (h->nranks > 1 && h->comm) {  // sum over ranks through the device scratch
     NC(h, ncclAllReduce(h->dec, h->part, 8, ncclInt64, ncclSum, h->comm, h->stream));
     CU(h, cudaMemcpyAsync(counts8, h->part, 8 * sizeof(long long), cudaMemcpyDeviceToHost, h->stream));
     CU(h, cudaStreamSynchronize(h->stream));

@@ -45,8 +45,11 @@ def pair(orc, P, nx, ny, method, k, bc=0, box=(-5.0, 5.0, -5.0, 5.0), cfl=None, 
 
 
 def rel_linf(a, b):
+    """max over components of L-inf(a - b) / L-inf(b); an identically zero
+    component of b (e.g. momenta of the quiescent shock-tube start) must match
+    to 1e-300, i.e. exactly up to denormals."""
     a, b = a.reshape(4, -1), b.reshape(4, -1)
-    return max(np.abs(a[c] - b[c]).max() / np.abs(b[c]).max() for c in range(4))
+    return max(np.abs(a[c] - b[c]).max() / max(np.abs(b[c]).max(), 1e-300) for c in range(4))
 
 
 def rel_linf_res(a, b):

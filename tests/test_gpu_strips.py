@@ -1,0 +1,59 @@
+"""Multi-GPU strip decomposition on ONE GPU: G strip-only handles (rank r of G,
+created without an NCCL id) each compute the residual of their y-strip from
+caller-supplied neighbour rows -- the exact kernel path a multi-GPU stage takes
+after its NCCL halo exchange.  The concatenated strip residuals must equal the
+whole-grid residual BITWISE (per-element arithmetic is partition-independent,
+SURVEY 8(e)); the gloo test (test_dist_host.py) covers the exchange plan."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+CASES = [(m, k) for m in ("cpr", "ndg", "dg", "sd") for k in (1, 2, 3, 4)] + [("fv", 1), ("fv", 2)]
+
+
+@pytest.fixture(scope="module")
+def P():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1709_01619_b200 as P
+    from paper_1709_01619_b200 import build
+    build.build()
+    P.load()
+    return P
+
+
+@pytest.mark.parametrize("method,k", CASES)
+@pytest.mark.parametrize("G", [2, 4])
+@pytest.mark.parametrize("bc", [0, 1])
+def test_strips_bitwise(orc, P, method, k, G, bc):
+    import torch
+    from paper_1709_01619_b200.inputs import perturb
+    rows = 8 if method == "fv" else 5
+    nx, ny = 19, rows * G
+    npe = 1 if method == "fv" else (k + 1) ** 2
+    box = (-5.0, 5.0, -5.0, 5.0)
+    oc = orc.config(nx=nx, ny=ny, method=method, k=k, bc=bc, box=box)
+    q = perturb(orc.init_case(oc), seed=31 + k, amp=1e-2)
+    cfg = P.make_config(nx, ny, method=method, k=k, bc=bc, box=box)
+    whole = P.Solver(cfg)
+    r_glob = whole.residual(torch.from_numpy(q).cuda()).cpu().numpy().reshape(4, ny, nx, npe)
+    Q = q.reshape(4, ny, nx, npe)
+    gr = 2 if method == "fv" else 1
+    parts = []
+    for r in range(G):
+        s = P.Solver(cfg, rank=r, nranks=G)
+        assert (s.row0, s.nrows) == (r * rows, rows)
+        loc = torch.from_numpy(np.ascontiguousarray(Q[:, s.row0:s.row0 + rows]).reshape(-1)).cuda()
+        lo_rows = [s.row0 - gr + g for g in range(gr)]
+        hi_rows = [s.row0 + rows + g for g in range(gr)]
+        lo = hi = None
+        if bc == 0 or r > 0:
+            lo = torch.from_numpy(np.ascontiguousarray(Q[:, [x % ny for x in lo_rows]]).reshape(-1)).cuda()
+        if bc == 0 or r < G - 1:
+            hi = torch.from_numpy(np.ascontiguousarray(Q[:, [x % ny for x in hi_rows]]).reshape(-1)).cuda()
+        parts.append(s.residual_strip(loc, lo, hi).cpu().numpy().reshape(4, rows, nx, npe))
+        s.close()
+    np.testing.assert_array_equal(np.concatenate(parts, axis=1), r_glob)
+    whole.close()
