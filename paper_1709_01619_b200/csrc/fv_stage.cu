@@ -1,17 +1,27 @@
 // fv_stage.cu -- fused RK-stage kernel of the MUSCL finite-volume method
 // (Eqs. (6)-(8); MUSCL + minmod; Alg. 1).
+//
 // The paper's two kernels (FV_Reconstruct writing face fluxes to global memory,
-// then the flux-derivative kernel) become one: a TX x TY cell tile
-// plus a 2-cell halo is staged in shared memory, every tile face is
-// reconstructed and Rusanov-coupled once, the flux differences and the SSP-RK3
-// combination are applied in registers, and only the new state is written.
+// then the flux-derivative kernel) become one marching kernel:
+//  * a CTA owns a strip of TX cells (one thread per cell column) and marches up
+//    RB cell rows;
+//  * a 5-row ring in shared memory holds rows j-1..j+2 (the MUSCL stencil of
+//    the x faces of row j and of its N face); row j+3 is prefetched into
+//    registers one step ahead (coalesced loads), so HBM latency hides behind a
+//    step's arithmetic and each value is read from HBM once;
+//  * x faces: one reconstruction + Rusanov per face (each thread its W face, the
+//    strip's last thread also the E face), exchanged through shared memory;
+//    y faces: each thread computes the N face of its column and carries it in
+//    registers as the S face of the next row -- no face array ever reaches HBM;
+//  * flux differences, the SSP-RK combination, the dt wave speed and the
+//    non-physical check are fused; one coalesced store per component.
 #include "common.cuh"
 
 namespace h2d {
 
 namespace {
-constexpr int FTX = 32, FTY = 8, FNT = FTX * FTY;
-constexpr int FSX = FTX + 4, FSY = FTY + 4;
+constexpr int FTX = 128, FRB = 64, FNS = 5;   // cells per strip, rows per march, ring rows
+constexpr int FW = FTX + 4;                    // ring row width: 2 halo cells each side
 
 // face states from the stencil (i-1, i, i+1, i+2) for the face i+1/2
 template <int ORDER>
@@ -29,13 +39,24 @@ __device__ __forceinline__ void muscl(double qm1, double q0, double q1, double q
     qE = q1 - 0.25 * ((1.0 - kap) * minmod2(dp1, beta * dm1, dec) + (1.0 + kap) * minmod2(dm1, beta * dp1, dec));
   }
 }
+
+// reconstruct both face states from a 4-cell stencil s[t][c] and take Rusanov
+template <int ORDER, int DIR>
+__device__ __forceinline__ void face_flux(const double s[4][4], double gm1, double gam, double F[4], long long* dec) {
+  double qW[4], qE[4], fL[4], fR[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) muscl<ORDER>(s[0][c], s[1][c], s[2][c], s[3][c], qW[c], qE[c], dec);
+  rusanov<DIR>(qW, qE, gm1, gam, F, fL, fR);
+}
 }  // namespace
 
+#ifndef H2D_FV_MINB
+#define H2D_FV_MINB 4
+#endif
 template <int ORDER>
-__global__ void __launch_bounds__(FNT) fv_stage_kernel(const StageArgs a) {
-  __shared__ double sq[4][FSY][FSX];
-  __shared__ double sF[FTY][FTX + 1][4];
-  __shared__ double sG[FTY + 1][FTX][4];
+__global__ void __launch_bounds__(FTX, H2D_FV_MINB) fv_stage_kernel(const StageArgs a) {
+  __shared__ double ring[FNS][4][FW];
+  __shared__ double sF[FTX + 1][4];   // W-face fluxes of the row (+ the strip's last E face)
   __shared__ double sred[32];
   double dtv = 1.0;
   if (a.dt) {
@@ -43,83 +64,142 @@ __global__ void __launch_bounds__(FNT) fv_stage_kernel(const StageArgs a) {
     if (dtv == 0.0) return;
   }
   const int tid = threadIdx.x;
-  const int i0 = blockIdx.x * FTX, j0 = blockIdx.y * FTY;
-  const int TXv = min(FTX, a.nx - i0), TYv = min(FTY, a.nrows - j0);
+  const int i0 = blockIdx.x * FTX, jb = blockIdx.y * FRB;
+  const int TXv = min(FTX, a.nx - i0), RBv = min(FRB, a.nrows - jb);
   const double gam = a.gamma, gm1 = a.gamma - 1.0;
+  const bool own = tid < TXv;
 
-  // cells (j0-2 .. j0+TYv+1) x (i0-2 .. i0+TXv+1), corners excluded
-  for (int t = tid; t < 4 * FSY * FSX; t += FNT) {
-    const int sx = t % FSX, sy = (t / FSX) % FSY, c = t / (FSX * FSY);
-    if (sx >= TXv + 4 || sy >= TYv + 4) continue;
-    const bool hx = (sx < 2 || sx >= TXv + 2), hy = (sy < 2 || sy >= TYv + 2);
-    if (hx && hy) continue;
-    int i = i0 - 2 + sx, j = j0 - 2 + sy;
-    if (a.bcx == 0) i = (i % a.nx + a.nx) % a.nx;
-    else i = i < 0 ? 0 : (i >= a.nx ? a.nx - 1 : i);  // ghost cells copy the boundary cell
+  // global cell (row jr, column gi) -> value of component c (x: periodic wrap or
+  // clamp; y: ghost rows, or clamp at a transmissive boundary)
+  auto cell = [&](int jr, int gi, int c) -> double {
+    if (a.bcx == 0) gi = (gi % a.nx + a.nx) % a.nx;
+    else gi = gi < 0 ? 0 : (gi >= a.nx ? a.nx - 1 : gi);
     const double* base = a.q;
     long long cs = a.cs;
-    if (j < 0) {
-      if (a.ghost_lo) { base = a.ghost_lo; cs = a.gcs; j += 2; } else j = 0;
-    } else if (j >= a.nrows) {
-      if (a.ghost_hi) { base = a.ghost_hi; cs = a.gcs; j -= a.nrows; } else j = a.nrows - 1;
+    if (jr < 0) {
+      if (a.ghost_lo) { base = a.ghost_lo; cs = a.gcs; jr += 2; } else jr = 0;
+    } else if (jr >= a.nrows) {
+      if (a.ghost_hi) { base = a.ghost_hi; cs = a.gcs; jr -= a.nrows; } else jr = a.nrows - 1;
     }
-    sq[c][sy][sx] = __ldg(base + c * cs + (long long)j * a.nx + i);
-  }
-  __syncthreads();
-
-  for (int t = tid; t < FTY * (FTX + 1); t += FNT) {  // x-faces: between cells fx-1 and fx
-    const int fx = t % (FTX + 1), ly = t / (FTX + 1);
-    if (ly >= TYv || fx > TXv) continue;
-    double qW[4], qE[4], F[4], fL[4], fR[4];
-    // tile-edge faces are computed by both neighbouring tiles; count each face once
-    long long* dec = (fx < TXv || i0 + TXv == a.nx) ? a.dec : nullptr;
-#pragma unroll
-    for (int c = 0; c < 4; ++c)
-      muscl<ORDER>(sq[c][ly + 2][fx], sq[c][ly + 2][fx + 1], sq[c][ly + 2][fx + 2], sq[c][ly + 2][fx + 3], qW[c],
-                   qE[c], dec);
-    rusanov<0>(qW, qE, gm1, gam, F, fL, fR);
-#pragma unroll
-    for (int c = 0; c < 4; ++c) sF[ly][fx][c] = F[c];
-  }
-  for (int t = tid; t < (FTY + 1) * FTX; t += FNT) {  // y-faces
-    const int lx = t % FTX, fy = t / FTX;
-    if (lx >= TXv || fy > TYv) continue;
-    double qW[4], qE[4], F[4], fL[4], fR[4];
-    long long* dec = (fy < TYv || (j0 + TYv == a.nrows && a.count_top)) ? a.dec : nullptr;
-#pragma unroll
-    for (int c = 0; c < 4; ++c)
-      muscl<ORDER>(sq[c][fy][lx + 2], sq[c][fy + 1][lx + 2], sq[c][fy + 2][lx + 2], sq[c][fy + 3][lx + 2], qW[c],
-                   qE[c], dec);
-    rusanov<1>(qW, qE, gm1, gam, F, fL, fR);
-#pragma unroll
-    for (int c = 0; c < 4; ++c) sG[fy][lx][c] = F[c];
-  }
-  __syncthreads();
-
-  double lam = 0.0;
-  const int lx = tid % FTX, ly = tid / FTX;
-  if (lx < TXv && ly < TYv) {
-    const long long gidx = (long long)(j0 + ly) * a.nx + (i0 + lx);
-    const double bdt = a.bcoef * dtv;
-    double o[4];
+    return __ldg(base + c * cs + (long long)jr * a.nx + gi);
+  };
+  // this thread's ring column(s): own cell (slot tid + 2); threads 0..3 also the halo slots
+  auto load_row = [&](int jr, double v[4], double h[4]) {
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-      const double R = -(sF[ly][lx + 1][c] - sF[ly][lx][c]) * a.rdx2 - (sG[ly + 1][lx][c] - sG[ly][lx][c]) * a.rdy2;
-      double v = a.a1 * sq[c][ly + 2][lx + 2] + bdt * R;
-      if (a.q0) v += a.a0 * a.q0[c * a.cs + gidx];
-      o[c] = v;
-      a.out[c * a.cs + gidx] = v;
+      v[c] = own ? cell(jr, i0 + tid, c) : 0.0;
+      h[c] = 0.0;
     }
-    if (a.lam) lam = wave_speed(o, gm1, gam);
-    if (a.bad && nonphysical(o, gm1)) atomicMin(a.bad, (unsigned long long)gidx);
+    if (tid < 4) {  // halo slots 0, 1 (cells i0-2, i0-1) and TXv+2, TXv+3 (cells i0+TXv, +1)
+      const int gi = tid < 2 ? i0 - 2 + tid : i0 + TXv + (tid - 2);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) h[c] = cell(jr, gi, c);
+    }
+  };
+  auto store_row = [&](int slot, const double v[4], const double h[4]) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      if (own) ring[slot][c][tid + 2] = v[c];
+      if (tid < 4) ring[slot][c][tid < 2 ? tid : TXv + tid] = h[c];
+    }
+  };
+
+  // prologue: rows jb-2 .. jb+1 into the ring, jb+2 into registers
+  double pv[4], ph[4];
+  for (int r = -2; r <= 1; ++r) {
+    load_row(jb + r, pv, ph);
+    store_row((r + FNS) % FNS, pv, ph);
+  }
+  load_row(jb + 2, pv, ph);
+  __syncthreads();
+  auto slot_of = [&](int r) { return ((r % FNS) + FNS) % FNS; };  // r = row - jb
+
+  // S face of the first row (between rows jb-1 and jb)
+  double GS[4];
+  {
+    // counted only for the domain's bottom face (every other S face is the N face of a row below)
+    long long* dec = (a.dec && own && jb == 0 && a.count_bot) ? a.dec : nullptr;
+    double s[4][4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) s[t][c] = own ? ring[slot_of(-2 + t)][c][tid + 2] : 1.0;
+    if (own) face_flux<ORDER, 1>(s, gm1, gam, GS, dec);
+  }
+
+  double lam = 0.0;
+  const double bdt = a.bcoef * dtv;
+  for (int r = 0; r < RBv; ++r) {
+    // the prefetched row r+2 enters the ring; prefetch row r+3
+    store_row(slot_of(r + 2), pv, ph);
+    if (r + 3 <= RBv + 1) load_row(jb + r + 3, pv, ph);
+    __syncthreads();
+    const int sc = slot_of(r);
+    const long long gidx = (long long)(jb + r) * a.nx + (i0 + tid);
+    double q0v[4] = {0, 0, 0, 0};
+    if (own && a.q0) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) q0v[c] = a.q0[c * a.cs + gidx];
+    }
+    // x faces: the W face of each own cell, plus the strip's last E face
+    if (own) {
+      double s[4][4], F[4];
+      long long* dec = a.dec;
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) s[t][c] = ring[sc][c][tid + t];   // cells tid-2 .. tid+1
+      face_flux<ORDER, 0>(s, gm1, gam, F, dec);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) sF[tid][c] = F[c];
+      if (tid == TXv - 1) {
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) s[t][c] = ring[sc][c][tid + 1 + t];
+        face_flux<ORDER, 0>(s, gm1, gam, F, (i0 + TXv == a.nx) ? dec : nullptr);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) sF[tid + 1][c] = F[c];
+      }
+    }
+    // N face of the column (rows r-1 .. r+2), carried as the next row's S face
+    double GN[4];
+    if (own) {
+      double s[4][4];
+      long long* dec = a.dec;
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) s[t][c] = ring[slot_of(r - 1 + t)][c][tid + 2];
+      face_flux<ORDER, 1>(s, gm1, gam, GN, dec);
+    }
+    __syncthreads();
+    if (own) {
+      double o[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const double R = -(sF[tid + 1][c] - sF[tid][c]) * a.rdx2 - (GN[c] - GS[c]) * a.rdy2;
+        double v = a.a1 * ring[sc][c][tid + 2] + bdt * R;
+        if (a.q0) v += a.a0 * q0v[c];
+        o[c] = v;
+        a.out[c * a.cs + gidx] = v;
+        GS[c] = GN[c];
+      }
+      if (a.lam || a.bad) {
+        const Prim w = prims(o, gm1);
+        if (a.lam) lam = fmax(lam, fmax(fabs(w.u), fabs(w.v)) + fsqrt(gam * w.p * w.ri));
+        const bool fin = isfinite(o[0]) && isfinite(o[1]) && isfinite(o[2]) && isfinite(o[3]);
+        if (a.bad && (!fin || !(o[0] > 0.0) || !(w.p > 0.0))) atomicMin(a.bad, (unsigned long long)gidx);
+      }
+    }
   }
   if (a.lam) block_max_to(lam, a.lam, sred);
 }
 
 int launch_fv_stage(int k, const StageArgs& a, cudaStream_t s) {
-  dim3 grid((a.nx + FTX - 1) / FTX, (a.nrows + FTY - 1) / FTY);
-  if (k == 1) fv_stage_kernel<1><<<grid, FNT, 0, s>>>(a);
-  else fv_stage_kernel<2><<<grid, FNT, 0, s>>>(a);
+  dim3 grid((a.nx + FTX - 1) / FTX, (a.nrows + FRB - 1) / FRB);
+  if (k == 1) fv_stage_kernel<1><<<grid, FTX, 0, s>>>(a);
+  else fv_stage_kernel<2><<<grid, FTX, 0, s>>>(a);
   return (int)cudaPeekAtLastError();
 }
 

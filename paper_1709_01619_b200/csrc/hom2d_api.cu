@@ -208,7 +208,7 @@ hom2d_status run_stage(hom2d* h, const double* q, const double* q0, double* out,
   s.a0 = a0; s.a1 = a1; s.bcoef = b; s.dt = dt; s.gamma = h->cfg.gamma;
   s.lam = lam; s.bad = bad;
   s.dec = h->cfg.record_decisions ? h->dec : nullptr;
-  s.count_top = (h->rank == h->nranks - 1);
+  s.count_bot = (h->rank == 0);
   int e;
   const bool timed = 2 * (h->ev_used + 1) <= (int)h->ev.size();
   if (timed) cudaEventRecord(h->ev[2 * h->ev_used], h->stream);

@@ -26,8 +26,8 @@ struct StageArgs {
   double gamma;
   unsigned long long* lam; // optional: atomicMax of max(|u|,|v|)+c of `out` (bits of a double >= 0)
   unsigned long long* bad; // optional: atomicMin of the first non-physical point index
-  long long* dec;          // optional: decision counters [4]
-  int count_top;           // this strip owns the top boundary face row (decision counting)
+  long long* dec;          // optional: decision counters [8]
+  int count_bot;           // this strip owns the domain's bottom face row (decision counting)
 };
 
 int launch_ho_stage(int method, int k, const StageArgs& a, cudaStream_t s);   // DG, SD
