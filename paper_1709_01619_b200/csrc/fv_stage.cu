@@ -64,8 +64,8 @@ __global__ void __launch_bounds__(FTX, H2D_FV_MINB) fv_stage_kernel(const StageA
     if (dtv == 0.0) return;
   }
   const int tid = threadIdx.x;
-  const int i0 = blockIdx.x * FTX, jb = blockIdx.y * FRB;
-  const int TXv = min(FTX, a.nx - i0), RBv = min(FRB, a.nrows - jb);
+  const int i0 = blockIdx.x * FTX, jb = blockIdx.y * a.rows;
+  const int TXv = min(FTX, a.nx - i0), RBv = min(a.rows, a.nrows - jb);
   const double gam = a.gamma, gm1 = a.gamma - 1.0;
   const bool own = tid < TXv;
 
@@ -196,8 +196,25 @@ __global__ void __launch_bounds__(FTX, H2D_FV_MINB) fv_stage_kernel(const StageA
   if (a.lam) block_max_to(lam, a.lam, sred);
 }
 
-int launch_fv_stage(int k, const StageArgs& a, cudaStream_t s) {
-  dim3 grid((a.nx + FTX - 1) / FTX, (a.nrows + FRB - 1) / FRB);
+int march_rows(int nrows, int strips, int rb_max) {
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || nsm <= 0) nsm = 148;
+  }
+  const long long target = 4LL * nsm;
+  long long rows = ((long long)nrows * strips + target - 1) / target;
+  if (rows > rb_max) rows = rb_max;
+  if (rows < 4) rows = 4;
+  return (int)rows;
+}
+
+int launch_fv_stage(int k, const StageArgs& a0, cudaStream_t s) {
+  StageArgs a = a0;
+  const int strips = (a.nx + FTX - 1) / FTX;
+  a.rows = march_rows(a.nrows, strips, FRB);
+  dim3 grid(strips, (a.nrows + a.rows - 1) / a.rows);
   if (k == 1) fv_stage_kernel<1><<<grid, FTX, 0, s>>>(a);
   else fv_stage_kernel<2><<<grid, FTX, 0, s>>>(a);
   return (int)cudaPeekAtLastError();

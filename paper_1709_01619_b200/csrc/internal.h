@@ -28,7 +28,12 @@ struct StageArgs {
   unsigned long long* bad; // optional: atomicMin of the first non-physical point index
   long long* dec;          // optional: decision counters [8]
   int count_bot;           // this strip owns the domain's bottom face row (decision counting)
+  int rows;                // marching kernels: element rows per CTA (set by the launcher)
 };
+
+// rows per CTA for a marching kernel: enough CTAs to fill the GPU (>= 4 per SM),
+// at most rb_max, at least 4 (the march costs 1-2 prologue rows)
+int march_rows(int nrows, int strips, int rb_max);
 
 int launch_ho_stage(int method, int k, const StageArgs& a, cudaStream_t s);   // DG, SD
 int launch_gll_stage(int method, int k, const StageArgs& a, cudaStream_t s);  // CPR, NDG
