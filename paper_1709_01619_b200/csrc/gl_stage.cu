@@ -1,0 +1,558 @@
+// gl_stage.cu -- fused RK-stage kernels of the methods with Gauss-Legendre
+// solution points: DG (weak form on GL points, Eqs. (18)-(21), Algs. 2-4,
+// P:240-267) and SD (GL solution points, Chebyshev-Gauss-Lobatto flux
+// points, Eqs. (30)-(34), Algs. 5-6).
+//
+// Same B200 design as gll_stage.cu (marching strips, TMA row ring, one thread
+// per element line); what the GL point sets add:
+//  * traces are interpolated (DG: Alg. 2; SD: flux points 0 and n of a line),
+//    the W neighbour's E trace is interpolated by the thread on its right from
+//    the ring, the N/S traces from the element's columns;
+//  * DG is evaluated in its equivalent strong form with the Radau (g_DG)
+//    correction on GL points (the weak form's surface terms l_a(+-1)/w_a equal
+//    g'_R/L(xi_a), SBP identity -- pinned in tests/test_oracle_pins.py P7):
+//    R = -(2/dx)[D f + g'_L (F^W - f_W) + g'_R (F^E - f_E)] - (2/dy)[...] with
+//    f_W, f_E the INTERPOLATED flux at the edges (sum-factorised, no dense M^-1);
+//  * SD interpolates each line and each column to its n+1 flux points, evaluates
+//    the interior flux points and differentiates the flux polynomial at the
+//    solution points; the end flux points carry the Rusanov fluxes;
+//  * the N face flux of row j is carried to row j+1 as its S face flux.
+#include <cstring>
+
+#include "common.cuh"
+#include "ops_tables.h"
+#include "tma.cuh"
+
+namespace h2d {
+
+namespace {
+
+template <int K> struct LTile;
+template <> struct LTile<1> { static constexpr int TX = 64, RB = 64; };
+template <> struct LTile<2> { static constexpr int TX = 32, RB = 64; };
+template <> struct LTile<3> { static constexpr int TX = 32, RB = 64; };
+template <> struct LTile<4> { static constexpr int TX = 32, RB = 64; };
+
+enum { LM_DG = 2, LM_SD = 4 };
+constexpr int NSTG = 3;
+
+struct LMaps {
+  CUtensorMap q, lo, hi;
+};
+
+// operator table (kernel parameter: compile-time indices become constant-bank operands)
+template <int K>
+struct LOps {
+  static constexpr int N = K + 1;
+  static constexpr int D = 0;                  // D_gl[N][N]
+  static constexpr int GL = D + N * N;         // g'_L at GL points
+  static constexpr int GR = GL + N;            // g'_R at GL points
+  static constexpr int EL = GR + N;            // l_l(-1)
+  static constexpr int ER = EL + N;            // l_l(+1)
+  static constexpr int SI = ER + N;            // sd_I[N+1][N]
+  static constexpr int SD = SI + (N + 1) * N;  // sd_D[N][N+1]
+  static constexpr int TOT = SD + N * (N + 1);
+};
+struct LTab {
+  double v[25 + 20 + 30 + 30];
+};
+template <int K>
+LTab make_ltab() {
+  using O = Ops<K>;
+  using T = LOps<K>;
+  constexpr int N = K + 1;
+  LTab t{};
+  for (int a = 0; a < N; ++a) {
+    for (int l = 0; l < N; ++l) t.v[T::D + a * N + l] = O::D_gl[a][l];
+    t.v[T::GL + a] = O::gLp_gl[a];
+    t.v[T::GR + a] = O::gRp_gl[a];
+    t.v[T::EL + a] = O::eL_gl[a];
+    t.v[T::ER + a] = O::eR_gl[a];
+    for (int r = 0; r <= N; ++r) {
+      t.v[T::SI + r * N + a] = O::sd_I[r][a];
+      t.v[T::SD + a * (N + 1) + r] = O::sd_D[a][r];
+    }
+  }
+  return t;
+}
+
+template <int M, int K>
+struct L {
+  static constexpr int N = K + 1, NP = N * N;
+  static constexpr int TX = LTile<K>::TX, RB = LTile<K>::RB, NT = TX * N;
+  static constexpr bool SWZ = (NP == 16);
+  static constexpr int NSL = TX + 2;
+  static constexpr int CW = (NP + 1 + 1) & ~1;
+  static constexpr int CM = ((TX * NP + 1) + 1) & ~1;
+  static constexpr int CREG = CW + CM + CW;
+  static constexpr int RSW = (NSL + 7) & ~7;
+  static constexpr int FIXO = 4 * RSW * 16;
+  static constexpr int STG = SWZ ? FIXO + 8 * 16 : 4 * CREG;
+  static constexpr int STGA = (STG + 127) & ~127;
+  static constexpr int OR_ = 0;
+  static constexpr int OFW = OR_ + NSTG * STGA;            // W-face fluxes [TX+1][N][4]
+  static constexpr int OFN = OFW + (TX + 1) * N * 4;       // N-face fluxes, double-buffered [2][TX][N][4]
+  static constexpr int OJ = OFN + 2 * TX * N * 4;          // DG: y jumps [TX][2][N][4]
+  static constexpr int OG = OJ + (M == LM_DG ? TX * 2 * N * 4 : 0);  // DG: g at points [TX][NP][4]
+  static constexpr int OPY = OG + (M == LM_DG ? TX * NP * 4 : 0);    // SD: column interior fluxes [TX][N][N-1][4]
+  static constexpr int OT = OPY + (M == LM_SD ? TX * N * (N - 1) * 4 : 0);
+  static constexpr int ORD = OT + ((LOps<K>::TOT + 1) & ~1);
+  static constexpr int OB = ORD + 32;
+  static constexpr int TOTAL = OB + ((NSTG + 1) & ~1);
+  static constexpr size_t SMEM = TOTAL * sizeof(double);
+};
+
+__device__ __forceinline__ void st4(double* p, const double v[4]) {
+  reinterpret_cast<double2*>(p)[0] = make_double2(v[0], v[1]);
+  reinterpret_cast<double2*>(p)[1] = make_double2(v[2], v[3]);
+}
+__device__ __forceinline__ void ld4(const double* p, double v[4]) {
+  const double2 a = reinterpret_cast<const double2*>(p)[0], b = reinterpret_cast<const double2*>(p)[1];
+  v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+}
+template <int DIR>
+__device__ __forceinline__ void node_eval(const double q[4], double gm1, double gam, double f[4], double& s) {
+  const Prim w = prims(q, gm1);
+  flux<DIR>(q, w, f);
+  s = fabs(DIR == 0 ? w.u : w.v) + fsqrt(gam * w.p * w.ri);
+}
+__device__ __forceinline__ void rus(const double qL[4], const double fL[4], double sL, const double qR[4],
+                                    const double fR[4], double sR, double F[4]) {
+  const double lam = fmax(sL, sR);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) F[c] = 0.5 * (fL[c] + fR[c]) - 0.5 * lam * (qR[c] - qL[c]);
+}
+__device__ __forceinline__ const double* row_src(const StageArgs& a, int jr, int np, long long& cs) {
+  if (jr < 0) { cs = a.gcs; return a.ghost_lo; }
+  if (jr >= a.nrows) { cs = a.gcs; return a.ghost_hi; }
+  cs = a.cs;
+  return a.q + (long long)jr * a.nx * np;
+}
+__device__ __forceinline__ int piece_off(const double* src) {
+  return (int)((reinterpret_cast<uintptr_t>(src) >> 3) & 1);
+}
+__device__ __forceinline__ uint32_t piece_bytes(const double* src, int n) {
+  const uintptr_t s0 = reinterpret_cast<uintptr_t>(src);
+  return (uint32_t)(((s0 + (uintptr_t)n * 8 + 15) & ~uintptr_t(15)) - (s0 & ~uintptr_t(15)));
+}
+__device__ __forceinline__ const void* piece_src(const double* src) {
+  return reinterpret_cast<const void*>(reinterpret_cast<uintptr_t>(src) & ~uintptr_t(15));
+}
+
+}  // namespace
+
+template <int M, int K>
+__global__ void __launch_bounds__(L<M, K>::NT) gl_stage_kernel(const StageArgs a, const LTab tab,
+                                                               const __grid_constant__ LMaps maps) {
+  using H = L<M, K>;
+  using T = LOps<K>;
+  constexpr int N = H::N, NP = H::NP, TX = H::TX, NT = H::NT, NSL = H::NSL;
+  constexpr int CW = H::CW, CM = H::CM, CREG = H::CREG, STGA = H::STGA;
+  extern __shared__ __align__(1024) double4 smem4[];
+  double* sm = reinterpret_cast<double*>(smem4);
+  double* ring = sm + H::OR_;
+  double* sFW = sm + H::OFW;
+  double* sFN = sm + H::OFN;
+  double* sJ = sm + H::OJ;
+  double* sG = sm + H::OG;
+  double* sPY = sm + H::OPY;
+  double* sT = sm + H::OT;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + H::OB);
+
+  double dtv = 1.0;
+  if (a.dt) {
+    dtv = *a.dt;
+    if (dtv == 0.0) return;
+  }
+  const int tid = threadIdx.x;
+  const int i0 = blockIdx.x * TX, jb = blockIdx.y * a.rows;
+  const int TXv = min(TX, a.nx - i0), RBv = min(a.rows, a.nrows - jb);
+  const double gam = a.gamma, gm1 = a.gamma - 1.0;
+  const int lx = tid / N, b = tid - lx * N;
+  const bool own = lx < TXv;
+  const bool mirW = (i0 == 0 && a.bcx), mirE = (i0 + TXv == a.nx && a.bcx);
+  const bool wrapW = (i0 == 0 && !a.bcx), wrapE = (i0 + TXv == a.nx && !a.bcx);
+  const int iw = i0 > 0 ? i0 - 1 : a.nx - 1;
+  const int ie = i0 + TXv < a.nx ? i0 + TXv : 0;
+  const int nload = RBv + 2;
+
+  for (int i = tid; i < T::TOT; i += NT) sT[i] = tab.v[i];
+  if (tid == 0) {
+    for (int s = 0; s < NSTG; ++s) mbar_init(&bar[s], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  auto issue_row = [&](int Lr) {
+    if (tid != 0) return;
+    const int jr = jb - 1 + Lr;
+    long long cs;
+    const double* rb = row_src(a, jr, NP, cs);
+    uint64_t* br = &bar[Lr % NSTG];
+    double* st = ring + (Lr % NSTG) * STGA;
+    if (!rb) { mbar_arrive_expect_tx(br, 0); return; }
+    if constexpr (H::SWZ) {
+      const CUtensorMap* mp = jr < 0 ? &maps.lo : (jr >= a.nrows ? &maps.hi : &maps.q);
+      const int y0 = (jr < 0 || jr >= a.nrows ? 0 : jr * a.nx) + i0 - 1;
+      uint32_t tx = 4u * NSL * 128u;
+      if (wrapW) tx += 4u * 128u;
+      if (wrapE) tx += 4u * 128u;
+      mbar_arrive_expect_tx(br, tx);
+      for (int c = 0; c < 4; ++c) tma_load_3d(st + c * H::RSW * 16, mp, 0, y0, c, br);
+      double* fix = st + H::FIXO;
+      for (int c = 0; c < 4; ++c) {
+        if (wrapW) tma_load_1d(fix + (0 * 4 + c) * 16, rb + c * cs + (long long)iw * NP, NP * 8, br);
+        if (wrapE) tma_load_1d(fix + (1 * 4 + c) * 16, rb + c * cs + (long long)ie * NP, NP * 8, br);
+      }
+    } else {
+      uint32_t tx = 0;
+      for (int c = 0; c < 4; ++c) {
+        const double* comp = rb + c * cs;
+        tx += piece_bytes(comp + (long long)i0 * NP, TXv * NP);
+        if (!mirW) tx += piece_bytes(comp + (long long)iw * NP, NP);
+        if (!mirE) tx += piece_bytes(comp + (long long)ie * NP, NP);
+      }
+      mbar_arrive_expect_tx(br, tx);
+      for (int c = 0; c < 4; ++c) {
+        const double* comp = rb + c * cs;
+        double* dst = st + c * CREG;
+        const double* s1 = comp + (long long)i0 * NP;
+        tma_load_1d(dst + CW, piece_src(s1), piece_bytes(s1, TXv * NP), br);
+        if (!mirW) {
+          const double* s0 = comp + (long long)iw * NP;
+          tma_load_1d(dst, piece_src(s0), piece_bytes(s0, NP), br);
+        }
+        if (!mirE) {
+          const double* s2 = comp + (long long)ie * NP;
+          tma_load_1d(dst + CW + CM, piece_src(s2), piece_bytes(s2, NP), br);
+        }
+      }
+    }
+  };
+  struct RowView {
+    const double* st;
+    int dW, dM, dE, csodd;
+    bool have;
+  };
+  auto view = [&](int Lr) {
+    RowView v;
+    long long cs;
+    const double* rb = row_src(a, jb - 1 + Lr, NP, cs);
+    v.st = ring + (Lr % NSTG) * STGA;
+    v.have = rb != nullptr;
+    v.dW = v.dM = v.dE = 0;
+    v.csodd = (int)(cs & 1);
+    if (!H::SWZ && rb) {
+      v.dM = piece_off(rb + (long long)i0 * NP);
+      v.dW = piece_off(rb + (long long)iw * NP);
+      v.dE = piece_off(rb + (long long)ie * NP);
+    }
+    return v;
+  };
+  auto own_at = [&](const RowView& v, int c, int e, int p) -> double {
+    if constexpr (H::SWZ) {
+      return v.st[(c * H::RSW + e) * 16 + ((((p >> 1) ^ (e & 7)) << 1) | (p & 1))];
+    } else {
+      return v.st[c * CREG + CW + (v.dM ^ (c & v.csodd)) + (e - 1) * NP + p];
+    }
+  };
+  auto any_at = [&](const RowView& v, int c, int e, int p) -> double {
+    if constexpr (H::SWZ) {
+      const double* fix = v.st + H::FIXO;
+      if (e == 0 && wrapW) return fix[(0 * 4 + c) * 16 + p];
+      if (e == TXv + 1 && wrapE) return fix[(1 * 4 + c) * 16 + p];
+      return own_at(v, c, e, p);
+    } else {
+      if (e == 0) return v.st[c * CREG + (v.dW ^ (c & v.csodd)) + p];
+      if (e == TXv + 1) return v.st[c * CREG + CW + CM + (v.dE ^ (c & v.csodd)) + p];
+      return own_at(v, c, e, p);
+    }
+  };
+  // interpolation of a line (dir 0: row bb of slot e) or column (dir 1: column bb)
+  // of the element in slot e with the weights w[l]
+  auto interp = [&](const RowView& v, int e, int dir, int bb, const double* w, double out[4], bool anyslot) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      double s = 0.0;
+#pragma unroll
+      for (int l = 0; l < N; ++l) {
+        const int p = dir == 0 ? bb * N + l : l * N + bb;
+        s += w[l] * (anyslot ? any_at(v, c, e, p) : own_at(v, c, e, p));
+      }
+      out[c] = s;
+    }
+  };
+
+  for (int Lr = 0; Lr < NSTG && Lr < nload; ++Lr) issue_row(Lr);
+
+  double lam = 0.0;
+  const double bdt = a.bcoef * dtv;
+  const double* EL = tab.v + T::EL;
+  const double* ER = tab.v + T::ER;
+  const double* SI0 = tab.v + T::SI;               // flux point 0 row of sd_I (== eL)
+  const double* SIN = tab.v + T::SI + N * N;       // flux point n row (== eR)
+
+  for (int Lr = 0; Lr <= RBv; ++Lr) {
+    mbar_wait(&bar[Lr % NSTG], (Lr / NSTG) & 1);
+    mbar_wait(&bar[(Lr + 1) % NSTG], ((Lr + 1) / NSTG) & 1);
+    const RowView vc = view(Lr), vn = view(Lr + 1);
+    double* FNc = sFN + (Lr & 1) * TX * N * 4;        // N-face fluxes of this row (written now)
+    double* FSc = sFN + ((Lr + 1) & 1) * TX * N * 4;  // S-face fluxes of this row (written in step Lr-1)
+    const long long jr = jb - 1 + Lr;
+
+    double q[4][N];
+    double fW[4], fWi[4], fEi[4], jW[4];  // DG: trace flux / interpolated edge fluxes / W jump
+    double phi[N + 1][4];           // SD: x flux-point fluxes (interior; [0] = F^W)
+    double fl[4][N];                // DG: x fluxes of the line
+    if (Lr > 0 && own) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int x = 0; x < N; ++x) q[c][x] = own_at(vc, c, lx + 1, b * N + x);
+      const double* wl = (M == LM_DG) ? EL : SI0;
+      const double* wr = (M == LM_DG) ? ER : SIN;
+      double qw[4], qe[4], sw, se, fE[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+        for (int l = 0; l < N; ++l) { s0 += wl[l] * q[c][l]; s1 += wr[l] * q[c][l]; }
+        qw[c] = s0;
+        qe[c] = s1;
+      }
+      node_eval<0>(qw, gm1, gam, fW, sw);
+      node_eval<0>(qe, gm1, gam, fE, se);
+      if (M == LM_DG) {
+#pragma unroll
+        for (int x = 0; x < N; ++x) {
+          double v[4] = {q[0][x], q[1][x], q[2][x], q[3][x]}, f[4], g[4];
+          const Prim w = prims(v, gm1);
+          flux<0>(v, w, f);
+          flux<1>(v, w, g);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) fl[c][x] = f[c];
+          st4(sG + (lx * NP + b * N + x) * 4, g);
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+          for (int l = 0; l < N; ++l) { s0 += EL[l] * fl[c][l]; s1 += ER[l] * fl[c][l]; }
+          fWi[c] = s0;
+          fEi[c] = s1;
+        }
+      } else {  // SD: interior x flux points
+#pragma unroll
+        for (int r = 1; r < N; ++r) {
+          double v[4];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            double s = 0.0;
+#pragma unroll
+            for (int l = 0; l < N; ++l) s += tab.v[T::SI + r * N + l] * q[c][l];
+            v[c] = s;
+          }
+          flux<0>(v, prims(v, gm1), phi[r]);
+        }
+      }
+      // W face (left neighbour's E trace interpolated here), strip's last E face
+      double F[4];
+      if (lx == 0 && mirW) {
+        rus(qw, fW, sw, qw, fW, sw, F);
+      } else {
+        double ql[4], flf[4], sl;
+        interp(vc, lx, 0, b, wr, ql, true);
+        node_eval<0>(ql, gm1, gam, flf, sl);
+        rus(ql, flf, sl, qw, fW, sw, F);
+      }
+      st4(sFW + (lx * N + b) * 4, F);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        phi[0][c] = F[c];
+        jW[c] = F[c] - fWi[c];
+      }
+      if (lx == TXv - 1) {
+        double G[4];
+        if (mirE) {
+          rus(qe, fE, se, qe, fE, se, G);
+        } else {
+          double qr[4], fr[4], sr;
+          interp(vc, TXv + 1, 0, b, wl, qr, true);
+          node_eval<0>(qr, gm1, gam, fr, sr);
+          rus(qe, fE, se, qr, fr, sr, G);
+        }
+        st4(sFW + (TXv * N + b) * 4, G);
+      }
+    }
+    // column b: SD interior y flux points; N face (own N trace vs next row's S trace)
+    if (own) {
+      const double* wl = (M == LM_DG) ? EL : SI0;
+      const double* wr = (M == LM_DG) ? ER : SIN;
+      if (M == LM_SD && Lr > 0) {
+#pragma unroll
+        for (int r = 1; r < N; ++r) {
+          double v[4], g[4];
+          interp(vc, lx + 1, 1, b, tab.v + T::SI + r * N, v, false);
+          flux<1>(v, prims(v, gm1), g);
+          st4(sPY + ((lx * N + b) * (N - 1) + (r - 1)) * 4, g);
+        }
+      }
+      double qd[4], gd[4], sd, qu[4], gu[4], su, G[4];
+      if (vc.have) {
+        interp(vc, lx + 1, 1, b, wr, qd, false);
+        node_eval<1>(qd, gm1, gam, gd, sd);
+      }
+      if (vn.have) {
+        interp(vn, lx + 1, 1, b, wl, qu, false);
+        node_eval<1>(qu, gm1, gam, gu, su);
+      }
+      if (!vc.have) { for (int c = 0; c < 4; ++c) { qd[c] = qu[c]; gd[c] = gu[c]; } sd = su; }
+      if (!vn.have) { for (int c = 0; c < 4; ++c) { qu[c] = qd[c]; gu[c] = gd[c]; } su = sd; }
+      rus(qd, gd, sd, qu, gu, su, G);
+      st4(FNc + (lx * N + b) * 4, G);
+    }
+    __syncthreads();
+
+    double jE[4];
+    if (M == LM_DG) {  // jumps against the interpolated edge fluxes
+      if (Lr > 0 && own) {
+        double F[4];
+        ld4(sFW + ((lx + 1) * N + b) * 4, F);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) jE[c] = F[c] - fEi[c];
+        double gS[4] = {0, 0, 0, 0}, gN[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int l = 0; l < N; ++l) {
+          double g[4];
+          ld4(sG + (lx * NP + l * N + b) * 4, g);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) { gS[c] += EL[l] * g[c]; gN[c] += ER[l] * g[c]; }
+        }
+        double FS[4], FN[4], j[4];
+        ld4(FSc + (lx * N + b) * 4, FS);
+        ld4(FNc + (lx * N + b) * 4, FN);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) j[c] = FS[c] - gS[c];
+        st4(sJ + ((lx * 2 + 0) * N + b) * 4, j);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) j[c] = FN[c] - gN[c];
+        st4(sJ + ((lx * 2 + 1) * N + b) * 4, j);
+      }
+      __syncthreads();
+    }
+
+    if (Lr > 0 && own) {
+      const long long base = (jr * a.nx + i0 + lx) * NP + b * N;
+      if (M == LM_SD) {
+        double F[4];
+        ld4(sFW + ((lx + 1) * N + b) * 4, F);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) phi[N][c] = F[c];
+      }
+#pragma unroll
+      for (int x = 0; x < N; ++x) {
+        double v[4] = {q[0][x], q[1][x], q[2][x], q[3][x]};
+        double R[4];
+        if (M == LM_DG) {
+          double jS[4], jN[4];
+          ld4(sJ + ((lx * 2 + 0) * N + x) * 4, jS);
+          ld4(sJ + ((lx * 2 + 1) * N + x) * 4, jN);
+          const double gLa = tab.v[T::GL + x], gRa = tab.v[T::GR + x];
+          const double gLb = sT[T::GL + b], gRb = sT[T::GR + b];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            double fx = 0.0, gy = 0.0;
+#pragma unroll
+            for (int l = 0; l < N; ++l) {
+              fx += tab.v[T::D + x * N + l] * fl[c][l];
+              gy += sT[T::D + b * N + l] * sG[(lx * NP + l * N + x) * 4 + c];
+            }
+            fx += gLa * jW[c] + gRa * jE[c];
+            gy += gLb * jS[c] + gRb * jN[c];
+            R[c] = -a.rdx2 * fx - a.rdy2 * gy;
+          }
+        } else {  // SD
+          double FS[4], FN[4];
+          ld4(FSc + (lx * N + x) * 4, FS);
+          ld4(FNc + (lx * N + x) * 4, FN);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            double fx = 0.0, gy = 0.0;
+#pragma unroll
+            for (int r = 0; r <= N; ++r) fx += tab.v[T::SD + x * (N + 1) + r] * phi[r][c];
+            gy = sT[T::SD + b * (N + 1) + 0] * FS[c] + sT[T::SD + b * (N + 1) + N] * FN[c];
+#pragma unroll
+            for (int r = 1; r < N; ++r) gy += sT[T::SD + b * (N + 1) + r] * sPY[((lx * N + x) * (N - 1) + (r - 1)) * 4 + c];
+            R[c] = -a.rdx2 * fx - a.rdy2 * gy;
+          }
+        }
+        double o[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          double val = a.a1 * v[c] + bdt * R[c];
+          if (a.q0) val += a.a0 * a.q0[c * a.cs + base + x];
+          o[c] = val;
+          a.out[c * a.cs + base + x] = val;
+        }
+        if (a.lam || a.bad) {
+          const Prim w = prims(o, gm1);
+          if (a.lam) lam = fmax(lam, fmax(fabs(w.u), fabs(w.v)) + fsqrt(gam * w.p * w.ri));
+          const bool fin = isfinite(o[0]) && isfinite(o[1]) && isfinite(o[2]) && isfinite(o[3]);
+          if (a.bad && (!fin || !(o[0] > 0.0) || !(w.p > 0.0))) atomicMin(a.bad, (unsigned long long)(base + x));
+        }
+      }
+    }
+    __syncthreads();
+    if (Lr + NSTG < nload) {
+      if (tid == 0) fence_proxy_async_smem();
+      issue_row(Lr + NSTG);
+    }
+  }
+  if (a.lam) block_max_to(lam, a.lam, sm + H::ORD);
+}
+
+template <int M, int K>
+static int launch_l(const StageArgs& a, cudaStream_t s) {
+  using H = L<M, K>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(gl_stage_kernel<M, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)H::SMEM);
+    attr = true;
+  }
+  static const LTab tab = make_ltab<K>();
+  LMaps maps;
+  memset(&maps, 0, sizeof(maps));
+  if (H::SWZ) {
+    const long long nel = (long long)a.nx * a.nrows;
+    if (!make_map(&maps.q, a.q, nel, a.cs, H::NSL) || !make_map(&maps.lo, a.ghost_lo, a.nx, a.gcs, H::NSL) ||
+        !make_map(&maps.hi, a.ghost_hi, a.nx, a.gcs, H::NSL))
+      return (int)cudaErrorInvalidValue;
+  }
+  StageArgs b = a;
+  const int strips = (a.nx + H::TX - 1) / H::TX;
+  b.rows = march_rows(a.nrows, strips, H::RB);
+  dim3 grid(strips, (a.nrows + b.rows - 1) / b.rows);
+  gl_stage_kernel<M, K><<<grid, H::NT, H::SMEM, s>>>(b, tab, maps);
+  return (int)cudaPeekAtLastError();
+}
+
+int launch_gl_stage(int method, int k, const StageArgs& a, cudaStream_t s) {
+  if (method == LM_DG) {
+    switch (k) {
+      case 1: return launch_l<LM_DG, 1>(a, s);
+      case 2: return launch_l<LM_DG, 2>(a, s);
+      case 3: return launch_l<LM_DG, 3>(a, s);
+      case 4: return launch_l<LM_DG, 4>(a, s);
+    }
+  } else if (method == LM_SD) {
+    switch (k) {
+      case 1: return launch_l<LM_SD, 1>(a, s);
+      case 2: return launch_l<LM_SD, 2>(a, s);
+      case 3: return launch_l<LM_SD, 3>(a, s);
+      case 4: return launch_l<LM_SD, 4>(a, s);
+    }
+  }
+  return (int)cudaErrorInvalidValue;
+}
+
+}  // namespace h2d

@@ -530,6 +530,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   }
   return fn;
 }
+}  // namespace
 
 // {16 points, nelem elements, 4 components} fp64, box {16, box_e, 1}, 128-byte swizzle
 bool make_map(CUtensorMap* m, const double* base, long long nelem, long long cs, int box_e) {
@@ -545,7 +546,6 @@ bool make_map(CUtensorMap* m, const double* base, long long nelem, long long cs,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
-}  // namespace
 
 template <int M, int K>
 static int launch_g(const StageArgs& a, cudaStream_t s) {

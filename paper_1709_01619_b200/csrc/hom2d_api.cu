@@ -218,7 +218,7 @@ hom2d_status run_stage(hom2d* h, const double* q, const double* q0, double* out,
     int method = h->cfg.method;
     if (method == HOM2D_CPR && !h->cfg.cpr_chain_rule) method = HOM2D_NDG;  // flux-differentiation CPR == NDG
     e = (method == HOM2D_CPR || method == HOM2D_NDG) ? launch_gll_stage(method, h->cfg.k, s, h->stream)
-                                                      : launch_ho_stage(method, h->cfg.k, s, h->stream);
+                                                      : launch_gl_stage(method, h->cfg.k, s, h->stream);
   }
   if (timed) cudaEventRecord(h->ev[2 * h->ev_used++ + 1], h->stream);
   h->launches++;

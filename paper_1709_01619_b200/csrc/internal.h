@@ -1,6 +1,7 @@
 // internal.h -- host-side declarations shared by the API and the kernel files.
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace h2d {
@@ -35,7 +36,13 @@ struct StageArgs {
 // at most rb_max, at least 4 (the march costs 1-2 prologue rows)
 int march_rows(int nrows, int strips, int rb_max);
 
-int launch_ho_stage(int method, int k, const StageArgs& a, cudaStream_t s);   // DG, SD
+// host: 3-D TMA tensor map {16 points, nelem elements, 4 components} (fp64,
+// box {16, box_e, 1}, 128-B swizzle) over an element-row array; base == nullptr
+// gives an unused zero map (transmissive boundary)
+bool make_map(CUtensorMap* m, const double* base, long long nelem, long long cs, int box_e);
+
+int launch_ho_stage(int method, int k, const StageArgs& a, cudaStream_t s);   // DG, SD (tile kernel)
+int launch_gl_stage(int method, int k, const StageArgs& a, cudaStream_t s);   // DG, SD (marching)
 int launch_gll_stage(int method, int k, const StageArgs& a, cudaStream_t s);  // CPR, NDG
 int launch_fv_stage(int k, const StageArgs& a, cudaStream_t s);
 
