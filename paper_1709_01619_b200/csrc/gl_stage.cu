@@ -94,8 +94,11 @@ struct L {
   static constexpr int OFN = OFW + (TX + 1) * N * 4;       // N-face fluxes, double-buffered [2][TX][N][4]
   static constexpr int OJ = OFN + 2 * TX * N * 4;          // DG: y jumps [TX][2][N][4]
   static constexpr int OG = OJ + (M == LM_DG ? TX * 2 * N * 4 : 0);  // DG: g at points [TX][NP][4]
-  static constexpr int OPY = OG + (M == LM_DG ? TX * NP * 4 : 0);    // SD: column interior fluxes [TX][N][N-1][4]
-  static constexpr int OT = OPY + (M == LM_SD ? TX * N * (N - 1) * 4 : 0);
+  // per-element strides padded to 2 mod 4 doubles: the column reads of 8
+  // elements of a warp then fall into 8 different 16-B bank groups
+  static constexpr int GS = NP * 4 + 2, PYS = N * (N - 1) * 4 + 2;
+  static constexpr int OPY = OG + (M == LM_DG ? TX * GS : 0);        // SD: column interior fluxes [TX][N][N-1][4]
+  static constexpr int OT = OPY + (M == LM_SD ? TX * PYS : 0);
   static constexpr int ORD = OT + ((LOps<K>::TOT + 1) & ~1);
   static constexpr int OB = ORD + 32;
   static constexpr int TOTAL = OB + ((NSTG + 1) & ~1);
@@ -331,7 +334,7 @@ __global__ void __launch_bounds__(L<M, K>::NT) gl_stage_kernel(const StageArgs a
           flux<1>(v, w, g);
 #pragma unroll
           for (int c = 0; c < 4; ++c) fl[c][x] = f[c];
-          st4(sG + (lx * NP + b * N + x) * 4, g);
+          st4(sG + lx * H::GS + (b * N + x) * 4, g);
         }
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
@@ -394,7 +397,7 @@ __global__ void __launch_bounds__(L<M, K>::NT) gl_stage_kernel(const StageArgs a
           double v[4], g[4];
           interp(vc, lx + 1, 1, b, tab.v + T::SI + r * N, v, false);
           flux<1>(v, prims(v, gm1), g);
-          st4(sPY + ((lx * N + b) * (N - 1) + (r - 1)) * 4, g);
+          st4(sPY + lx * H::PYS + (b * (N - 1) + (r - 1)) * 4, g);
         }
       }
       double qd[4], gd[4], sd, qu[4], gu[4], su, G[4];
@@ -424,7 +427,7 @@ __global__ void __launch_bounds__(L<M, K>::NT) gl_stage_kernel(const StageArgs a
 #pragma unroll
         for (int l = 0; l < N; ++l) {
           double g[4];
-          ld4(sG + (lx * NP + l * N + b) * 4, g);
+          ld4(sG + lx * H::GS + (l * N + b) * 4, g);
 #pragma unroll
           for (int c = 0; c < 4; ++c) { gS[c] += EL[l] * g[c]; gN[c] += ER[l] * g[c]; }
         }
@@ -465,7 +468,7 @@ __global__ void __launch_bounds__(L<M, K>::NT) gl_stage_kernel(const StageArgs a
 #pragma unroll
             for (int l = 0; l < N; ++l) {
               fx += tab.v[T::D + x * N + l] * fl[c][l];
-              gy += sT[T::D + b * N + l] * sG[(lx * NP + l * N + x) * 4 + c];
+              gy += sT[T::D + b * N + l] * sG[lx * H::GS + (l * N + x) * 4 + c];
             }
             fx += gLa * jW[c] + gRa * jE[c];
             gy += gLb * jS[c] + gRb * jN[c];
@@ -482,7 +485,8 @@ __global__ void __launch_bounds__(L<M, K>::NT) gl_stage_kernel(const StageArgs a
             for (int r = 0; r <= N; ++r) fx += tab.v[T::SD + x * (N + 1) + r] * phi[r][c];
             gy = sT[T::SD + b * (N + 1) + 0] * FS[c] + sT[T::SD + b * (N + 1) + N] * FN[c];
 #pragma unroll
-            for (int r = 1; r < N; ++r) gy += sT[T::SD + b * (N + 1) + r] * sPY[((lx * N + x) * (N - 1) + (r - 1)) * 4 + c];
+            for (int r = 1; r < N; ++r)
+              gy += sT[T::SD + b * (N + 1) + r] * sPY[lx * H::PYS + (x * (N - 1) + (r - 1)) * 4 + c];
             R[c] = -a.rdx2 * fx - a.rdy2 * gy;
           }
         }

@@ -73,7 +73,8 @@ struct G {
   static constexpr int OJN = OFW + (TX + 1) * N * 4;  // N jumps of the current row [TX][N][4]
   static constexpr int OJS = OJN + TX * N * 4;        // S jumps, double-buffered [2][TX][N][4]
   static constexpr int OG = OJS + 2 * TX * N * 4;     // NDG: g at every point [TX][NP][4]
-  static constexpr int OT = OG + (M == GM_NDG ? TX * NP * 4 : 0);
+  static constexpr int GS = NP * 4 + 2;  // padded element stride (conflict-free column reads)
+  static constexpr int OT = OG + (M == GM_NDG ? TX * GS : 0);
   static constexpr int ORD = OT + ((N * N + 2 * N + 1) & ~1);
   static constexpr int OB = ORD + 32;                 // mbarriers (as doubles)
   static constexpr int LP = (N + 1) & ~1;             // q^n line slot (16-B multiple)
@@ -364,7 +365,7 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
         for (int x = 0; x < N; ++x) {
           double v[4] = {q[0][x], q[1][x], q[2][x], q[3][x]}, g[4];
           flux<1>(v, prims(v, gm1), g);
-          st4(sG + ((lx * NP) + b * N + x) * 4, g);
+          st4(sG + lx * H::GS + (b * N + x) * 4, g);
         }
       }
     }
@@ -457,7 +458,7 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
             for (int c = 0; c < 4; ++c) dy[c] += db * own_at(vc, c, lx + 1, l * N + x);
           } else {
             double u[4];
-            ld4(sG + ((lx * NP) + l * N + x) * 4, u);
+            ld4(sG + lx * H::GS + (l * N + x) * 4, u);
 #pragma unroll
             for (int c = 0; c < 4; ++c) dy[c] += db * u[c];
           }
