@@ -101,9 +101,23 @@ struct L {
   static constexpr int OT = OPY + (M == LM_SD ? TX * PYS : 0);
   static constexpr int ORD = OT + ((LOps<K>::TOT + 1) & ~1);
   static constexpr int OB = ORD + 32;
-  static constexpr int TOTAL = OB + ((NSTG + 1) & ~1);
+  static constexpr int OQ0 = OB + ((NSTG + 1) & ~1);  // q^n prefetch [4][N][NT], thread-private
+  static constexpr int TOTAL = OQ0 + 4 * N * NT;
   static constexpr size_t SMEM = TOTAL * sizeof(double);
 };
+
+// cp.async of this thread's q^n line into its private smem slots, one row ahead
+template <int N, int NT>
+__device__ __forceinline__ void q0_prefetch(double* sq0, const double* q0, long long cs, long long base, int tid) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+#pragma unroll
+    for (int x = 0; x < N; ++x)
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(sq0 + (c * N + x) * NT + tid)),
+                   "l"(q0 + c * cs + base + x)
+                   : "memory");
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
 
 __device__ __forceinline__ void st4(double* p, const double v[4]) {
   reinterpret_cast<double2*>(p)[0] = make_double2(v[0], v[1]);
@@ -161,6 +175,7 @@ __global__ void __launch_bounds__(L<M, K>::NT) gl_stage_kernel(const StageArgs a
   double* sPY = sm + H::OPY;
   double* sT = sm + H::OT;
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + H::OB);
+  double* sQ0 = sm + H::OQ0;
 
   double dtv = 1.0;
   if (a.dt) {
@@ -287,6 +302,8 @@ __global__ void __launch_bounds__(L<M, K>::NT) gl_stage_kernel(const StageArgs a
   };
 
   for (int Lr = 0; Lr < NSTG && Lr < nload; ++Lr) issue_row(Lr);
+  if (a.q0 && own)  // q^n of the first own row
+    q0_prefetch<N, NT>(sQ0, a.q0, a.cs, ((long long)jb * a.nx + i0 + lx) * NP + b * N, tid);
 
   double lam = 0.0;
   const double bdt = a.bcoef * dtv;
@@ -446,6 +463,7 @@ __global__ void __launch_bounds__(L<M, K>::NT) gl_stage_kernel(const StageArgs a
 
     if (Lr > 0 && own) {
       const long long base = (jr * a.nx + i0 + lx) * NP + b * N;
+      if (a.q0) asm volatile("cp.async.wait_group 0;" ::: "memory");
       if (M == LM_SD) {
         double F[4];
         ld4(sFW + ((lx + 1) * N + b) * 4, F);
@@ -494,7 +512,7 @@ __global__ void __launch_bounds__(L<M, K>::NT) gl_stage_kernel(const StageArgs a
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           double val = a.a1 * v[c] + bdt * R[c];
-          if (a.q0) val += a.a0 * a.q0[c * a.cs + base + x];
+          if (a.q0) val += a.a0 * sQ0[(c * N + x) * NT + tid];
           o[c] = val;
           a.out[c * a.cs + base + x] = val;
         }
@@ -505,6 +523,8 @@ __global__ void __launch_bounds__(L<M, K>::NT) gl_stage_kernel(const StageArgs a
           if (a.bad && (!fin || !(o[0] > 0.0) || !(w.p > 0.0))) atomicMin(a.bad, (unsigned long long)(base + x));
         }
       }
+      if (a.q0 && Lr < RBv)  // q^n of the next row into the consumed private slots
+        q0_prefetch<N, NT>(sQ0, a.q0, a.cs, base + (long long)a.nx * NP, tid);
     }
     __syncthreads();
     if (Lr + NSTG < nload) {
