@@ -41,7 +41,6 @@ int march_rows(int nrows, int strips, int rb_max);
 // gives an unused zero map (transmissive boundary)
 bool make_map(CUtensorMap* m, const double* base, long long nelem, long long cs, int box_e);
 
-int launch_ho_stage(int method, int k, const StageArgs& a, cudaStream_t s);   // DG, SD (tile kernel)
 int launch_gl_stage(int method, int k, const StageArgs& a, cudaStream_t s);   // DG, SD (marching)
 int launch_gll_stage(int method, int k, const StageArgs& a, cudaStream_t s);  // CPR, NDG
 int launch_fv_stage(int k, const StageArgs& a, cudaStream_t s);
