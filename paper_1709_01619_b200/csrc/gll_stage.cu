@@ -39,9 +39,12 @@ template <int K> struct GTile;
 template <> struct GTile<1> { static constexpr int TX = 64, RB = 64, MINB = 2; };  // 128 threads
 template <> struct GTile<2> { static constexpr int TX = 32, RB = 64, MINB = 2; };  //  96 threads
 #ifndef H2D_MINB3
-#define H2D_MINB3 2
+#define H2D_MINB3 4
 #endif
-template <> struct GTile<3> { static constexpr int TX = 32, RB = 64, MINB = H2D_MINB3; };  // 128 threads
+#ifndef H2D_TX3
+#define H2D_TX3 16  // 64 threads: 4 CTAs/SM interleave their barrier phases (A/B: +2.5 % over 32)
+#endif
+template <> struct GTile<3> { static constexpr int TX = H2D_TX3, RB = 64, MINB = H2D_MINB3; };  // 128 threads
 template <> struct GTile<4> { static constexpr int TX = 32, RB = 64, MINB = 1; };  // 160 threads
 
 enum { GM_CPR = 1, GM_NDG = 3 };
