@@ -98,6 +98,34 @@ __device__ __forceinline__ void jac(const double q[4], const Prim& w, double gm1
   }
 }
 
+// The same Jacobian actions through the primitive-variable differentials
+// (A(q).d = d f along d): du = (d1 - u d0)/rho, dv = (d2 - v d0)/rho,
+// dp = (gamma-1)(d3 - u d1 - v d2 + (u^2+v^2)/2 d0), then
+// d f = (d1, d1 u + rho u du + dp, d1 v + rho u dv, du (e+p) + u (d3 + dp)) and
+// d g = (d2, d2 u + rho v du, d2 v + rho v dv + dp, dv (e+p) + v (d3 + dp)).
+// Algebraically identical to jac<0> + jac<1> (tests compare them to the
+// oracle's matrix form); ~30 % fewer fp64 operations for the pair.
+__device__ __forceinline__ void jac_pair(const double q[4], const Prim& w, double gm1, const double dx[4],
+                                         const double dy[4], double fx[4], double gy[4]) {
+  const double u = w.u, v = w.v, k = 0.5 * (u * u + v * v), ep = q[3] + w.p;
+  {
+    const double du = w.ri * fma(-u, dx[0], dx[1]), dv = w.ri * fma(-v, dx[0], dx[2]);
+    const double dp = gm1 * fma(k, dx[0], fma(-v, dx[2], fma(-u, dx[1], dx[3])));
+    fx[0] = dx[1];
+    fx[1] = fma(dx[1], u, fma(q[1], du, dp));
+    fx[2] = fma(dx[1], v, q[1] * dv);
+    fx[3] = fma(du, ep, u * (dx[3] + dp));
+  }
+  {
+    const double du = w.ri * fma(-u, dy[0], dy[1]), dv = w.ri * fma(-v, dy[0], dy[2]);
+    const double dp = gm1 * fma(k, dy[0], fma(-v, dy[2], fma(-u, dy[1], dy[3])));
+    gy[0] = dy[2];
+    gy[1] = fma(dy[2], u, q[2] * du);
+    gy[2] = fma(dy[2], v, fma(q[2], dv, dp));
+    gy[3] = fma(dv, ep, v * (dy[3] + dp));
+  }
+}
+
 // max(|u|,|v|) + c  (2-D reading of Eq. (36))
 __device__ __forceinline__ double wave_speed(const double q[4], double gm1, double gam) {
   Prim w = prims(q, gm1);

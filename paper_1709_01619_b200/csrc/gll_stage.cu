@@ -475,8 +475,7 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
             for (int c = 0; c < 4; ++c) dx[c] += da * q[c][l];
           }
           const Prim w = prims(v, gm1);
-          jac<0>(v, w, gm1, gam, dx, Fx);
-          jac<1>(v, w, gm1, gam, dy, Gy);
+          jac_pair(v, w, gm1, dx, dy, Fx, Gy);
         } else {            // NDG: D[F]
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
