@@ -276,10 +276,10 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        sn = 512 if method != "fv" else 2048
-        v, el = oracle_rate(method, k, sn, sn, cfl, 3)
+        sn = 768 if method != "fv" else 3072   # ~15 s of single-core oracle work
+        v, el = oracle_rate(method, k, sn, sn, cfl, 6)
         cpu = {"value": v, "unit": "DOF-stage/s", "cores": 1, "kind": "oracle",
-               "sample": f"{method.upper()} P{k} vortex {sn}x{sn} elements, 3 SSP-RK3 steps ({el:.1f} s)",
+               "sample": f"{method.upper()} P{k} vortex {sn}x{sn} elements, 6 SSP-RK3 steps ({el:.1f} s)",
                "cpu": cpu_info()}
 
     if rank == 0:
