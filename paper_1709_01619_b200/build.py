@@ -42,11 +42,23 @@ def deps():
         os.path.join(ROOT, "include", "hom2d.h")]
 
 
+def src_hash() -> str:
+    import hashlib
+    h = hashlib.sha256()
+    for p in sorted(deps()):
+        h.update(os.path.basename(p).encode())
+        with open(p, "rb") as f:
+            h.update(f.read())
+    return h.hexdigest()
+
+
 def stale() -> bool:
-    if not os.path.exists(LIB):
+    """Content-based: the library is stale when the sources hash differs from the
+    one recorded at build time (robust to snapshot copies that reset mtimes)."""
+    if not os.path.exists(LIB) or not os.path.exists(LIB + ".srchash"):
         return True
-    t = os.path.getmtime(LIB)
-    return any(os.path.getmtime(p) > t for p in deps())
+    with open(LIB + ".srchash") as f:
+        return f.read().strip() != src_hash()
 
 
 def build(force: bool = False, verbose: bool = False, out: str = LIB, extra=()) -> str:
@@ -62,6 +74,9 @@ def build(force: bool = False, verbose: bool = False, out: str = LIB, extra=()) 
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), flush=True)
     subprocess.check_call(cmd)
+    if out == LIB:
+        with open(LIB + ".srchash", "w") as f:
+            f.write(src_hash())
     return out
 
 
