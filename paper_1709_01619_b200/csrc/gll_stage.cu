@@ -317,6 +317,7 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
     const long long jr = jb - 1 + L;                 // local strip row of this step
 
     double q[4][N], fW[4], fE[4], jW[4];
+    Prim pW, pE;
     if (L > 0 && own) {
 #pragma unroll
       for (int c = 0; c < 4; ++c)
@@ -336,8 +337,12 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
       // W face (computed by the element on its right) and the strip's last E face
       double qw[4] = {q[0][0], q[1][0], q[2][0], q[3][0]}, sw;
       double qe[4] = {q[0][N - 1], q[1][N - 1], q[2][N - 1], q[3][N - 1]}, se;
-      node_eval<0>(qw, gm1, gam, fW, sw);
-      node_eval<0>(qe, gm1, gam, fE, se);
+      pW = prims(qw, gm1);  // kept for the chain rule at points 0 and n-1
+      pE = prims(qe, gm1);
+      flux<0>(qw, pW, fW);
+      flux<0>(qe, pE, fE);
+      sw = fabs(pW.u) + fsqrt(gam * pW.p * pW.ri);
+      se = fabs(pE.u) + fsqrt(gam * pE.p * pE.ri);
       double F[4];
       if (lx == 0 && mirW) {
         rus(qw, fW, sw, qw, fW, sw, F);
@@ -474,7 +479,7 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
 #pragma unroll
             for (int c = 0; c < 4; ++c) dx[c] += da * q[c][l];
           }
-          const Prim w = prims(v, gm1);
+          const Prim w = (x == 0) ? pW : (x == N - 1) ? pE : prims(v, gm1);
           jac_pair(v, w, gm1, dx, dy, Fx, Gy);
         } else {            // NDG: D[F]
 #pragma unroll
