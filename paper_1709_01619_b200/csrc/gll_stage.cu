@@ -83,21 +83,31 @@ struct G {
   static constexpr int LP = (N + 1) & ~1;             // q^n line slot (16-B multiple)
   static constexpr int OQ0 = OB + ((NSTG + 1) & ~1);  // q^n prefetch [4][NT][LP], thread-private
   static constexpr int TOTAL = OQ0 + 4 * NT * LP;
+  static_assert(OQ0 % 2 == 0, "16-B cp.async slots");
   static constexpr size_t SMEM = TOTAL * sizeof(double);
 };
 
 // cp.async (LDGSTS) of this thread's q^n line (4 components x N doubles) into its
 // private smem slots, one row ahead of its use
 template <int N, int NT, int LP>
-__device__ __forceinline__ void q0_prefetch(double* sq0, const double* q0, long long cs, long long base, int tid) {
+__device__ __forceinline__ void q0_prefetch(double* sq0, const double* q0, long long cs, long long base, int tid,
+                                            bool vec) {
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
     const double* s = q0 + c * cs + base;
+    if (N % 2 == 0 && vec) {  // 16-B pieces, layout [c][x/2][thread] of double2
 #pragma unroll
-    for (int x = 0; x < N; ++x)  // layout [c][x][thread]: conflict-free read-back
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(sq0 + (c * N + x) * NT + tid)),
-                   "l"(s + x)
-                   : "memory");
+      for (int x = 0; x < N; x += 2)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sq0 + (c * N + x) * NT + 2 * tid)),
+                     "l"(s + x)
+                     : "memory");
+    } else {
+#pragma unroll
+      for (int x = 0; x < N; ++x)  // layout [c][x][thread]: conflict-free read-back
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(sq0 + (c * N + x) * NT + tid)),
+                     "l"(s + x)
+                     : "memory");
+    }
   }
   asm volatile("cp.async.commit_group;" ::: "memory");
 }
@@ -195,6 +205,10 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
   const double gam = a.gamma, gm1 = a.gamma - 1.0;
   const int lx = tid / N, b = tid - lx * N;
   const bool own = lx < TXv;
+  // vector global access: every line start 32-B (P3) / 16-B aligned in out and q^n
+  const unsigned long long amask = N == 4 ? 31ull : 15ull;
+  const bool vec = ((((unsigned long long)a.out | (unsigned long long)a.q0 |
+                      (unsigned long long)(a.cs * 8)) & amask) == 0);
   const bool mirW = (i0 == 0 && a.bcx), mirE = (i0 + TXv == a.nx && a.bcx);
   const bool wrapW = (i0 == 0 && !a.bcx), wrapE = (i0 + TXv == a.nx && !a.bcx);
   const int iw = i0 > 0 ? i0 - 1 : a.nx - 1;      // W halo element (periodic wrap)
@@ -301,7 +315,7 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
 
   for (int L = 0; L < NSTG && L < nload; ++L) issue_row(L);
   if (a.q0 && own)  // q^n of the first own row (step L = 1)
-    q0_prefetch<N, NT, H::LP>(sQ0, a.q0, a.cs, ((long long)jb * a.nx + i0 + lx) * NP + b * N, tid);
+    q0_prefetch<N, NT, H::LP>(sQ0, a.q0, a.cs, ((long long)jb * a.nx + i0 + lx) * NP + b * N, tid, vec);
 
   const double* D = sT;
   const double gLb = sT[N * N + b], gRb = sT[N * N + N + b];
@@ -412,7 +426,8 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
       const long long base = (jr * a.nx + i0 + lx) * NP + b * N;
       // q^n of the line: prefetched by cp.async one row ahead into thread-private smem
       if (a.q0) asm volatile("cp.async.wait_group 0;" ::: "memory");
-#define Q0V(c, x) sQ0[((c) * N + (x)) * NT + tid]
+#define Q0V(c, x) (N % 2 == 0 && vec ? sQ0[((c) * N + ((x) & ~1)) * NT + 2 * tid + ((x) & 1)] \
+                                     : sQ0[((c) * N + (x)) * NT + tid])
       double F[4], jE[4];
       ld4(sFW + ((lx + 1) * N + b) * 4, F);
 #pragma unroll
@@ -439,7 +454,7 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
             }
         }
       }
-      double fxl[4][N];
+      double fxl[4][N], ov[4][N];
       if (M == GM_NDG) {
 #pragma unroll
         for (int x = 0; x < N; ++x) {
@@ -504,7 +519,7 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
           double val = a.a1 * v[c] + bdt * R;
           if (a.q0) val += a.a0 * Q0V(c, x);
           o[c] = val;
-          a.out[c * a.cs + base + x] = val;
+          ov[c][x] = val;
         }
         if (a.lam || a.bad) {  // dt wave speed and non-physical check share one reciprocal
           const Prim w = prims(o, gm1);
@@ -513,8 +528,24 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
           if (a.bad && (!fin || !(o[0] > 0.0) || !(w.p > 0.0))) atomicMin(a.bad, (unsigned long long)(base + x));
         }
       }
+      // a thread's line of one component is N contiguous doubles: one 32-B (P3) or
+      // 16-B (P1) store per component when aligned
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        double* o = a.out + c * a.cs + base;
+        if (N == 4 && vec) {
+          asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(o), "d"(ov[c][0]), "d"(ov[c][1 % N]),
+                       "d"(ov[c][2 % N]), "d"(ov[c][3 % N])
+                       : "memory");
+        } else if (N == 2 && vec) {
+          asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(o), "d"(ov[c][0]), "d"(ov[c][1 % N]) : "memory");
+        } else {
+#pragma unroll
+          for (int x = 0; x < N; ++x) o[x] = ov[c][x];
+        }
+      }
       if (a.q0 && L < RBv)  // q^n of the next row into the (now consumed) private slots
-        q0_prefetch<N, NT, H::LP>(sQ0, a.q0, a.cs, base + (long long)a.nx * NP, tid);
+        q0_prefetch<N, NT, H::LP>(sQ0, a.q0, a.cs, base + (long long)a.nx * NP, tid, vec);
     }
     __syncthreads();  // stage L % NSTG and the face buffers are free again
     if (L + NSTG < nload) {
