@@ -132,10 +132,19 @@ __device__ __forceinline__ double wave_speed(const double q[4], double gm1, doub
   return fmax(fabs(w.u), fabs(w.v)) + fsqrt(gam * w.p * w.ri);
 }
 
+// Non-physical state (rho <= 0, p <= 0 or any component non-finite),
+// decided from rho and p = (gamma-1)(e - (rho u u + rho v v)/2) alone: given
+// 0 < rho < inf, a non-finite rho u or rho v makes the kinetic term +inf or NaN
+// (p = -inf or NaN), a non-finite e makes p = +-inf or NaN, and finite inputs
+// give p <= (gamma-1) e < inf (the kinetic term is >= 0). So
+// "0 < rho < inf and 0 < p < inf" is exactly "all finite, rho > 0, p > 0".
+__device__ __forceinline__ bool admissible(double rho, double p) {
+  return rho > 0.0 && rho < HUGE_VAL && p > 0.0 && p < HUGE_VAL;
+}
+
 __device__ __forceinline__ bool nonphysical(const double q[4], double gm1) {
   Prim w = prims(q, gm1);
-  bool fin = isfinite(q[0]) && isfinite(q[1]) && isfinite(q[2]) && isfinite(q[3]);
-  return !fin || !(q[0] > 0.0) || !(w.p > 0.0);
+  return !admissible(q[0], w.p);
 }
 
 __device__ __forceinline__ double warp_max(double v) {
@@ -170,14 +179,12 @@ __device__ __forceinline__ void count_dec(long long* dec, int which) {
 // two fp64 evaluation orders.
 #define DEC_TIE 1e-12
 __device__ __forceinline__ double minmod2(double a, double b, long long* dec) {
-  double r = 0.0;
-  int which = 1;
-  if (a > 0.0 && b > 0.0) {
-    if (a <= b) { r = a; which = 2; } else { r = b; which = 3; }
-  } else if (a < 0.0 && b < 0.0) {
-    if (a >= b) { r = a; which = 2; } else { r = b; which = 3; }
-  }
+  // value without branches: both positive -> the smaller, both negative -> the
+  // larger (equal arguments give the same value either way), else 0
+  const double r = (a > 0.0 && b > 0.0) ? fmin(a, b) : ((a < 0.0 && b < 0.0) ? fmax(a, b) : 0.0);
   if (dec) {
+    int which = 1;
+    if ((a > 0.0 && b > 0.0) || (a < 0.0 && b < 0.0)) which = (fabs(a) <= fabs(b)) ? 2 : 3;
     if (fabs(a) <= DEC_TIE || fabs(b) <= DEC_TIE || fabs(a - b) <= DEC_TIE) which = 4;
     count_dec(dec, which);
   }

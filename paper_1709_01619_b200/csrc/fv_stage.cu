@@ -53,7 +53,7 @@ __device__ __forceinline__ void face_flux(const double s[4][4], double gm1, doub
 #ifndef H2D_FV_MINB
 #define H2D_FV_MINB 4
 #endif
-template <int ORDER>
+template <int ORDER, bool REC>
 __global__ void __launch_bounds__(FTX, H2D_FV_MINB) fv_stage_kernel(const StageArgs a) {
   __shared__ double ring[FNS][4][FW];
   __shared__ double sF[FTX + 1][4];   // W-face fluxes of the row (+ the strip's last E face)
@@ -69,31 +69,32 @@ __global__ void __launch_bounds__(FTX, H2D_FV_MINB) fv_stage_kernel(const StageA
   const double gam = a.gamma, gm1 = a.gamma - 1.0;
   const bool own = tid < TXv;
 
-  // global cell (row jr, column gi) -> value of component c (x: periodic wrap or
-  // clamp; y: ghost rows, or clamp at a transmissive boundary)
-  auto cell = [&](int jr, int gi, int c) -> double {
-    if (a.bcx == 0) gi = (gi % a.nx + a.nx) % a.nx;
-    else gi = gi < 0 ? 0 : (gi >= a.nx ? a.nx - 1 : gi);
-    const double* base = a.q;
-    long long cs = a.cs;
+  long long* const dec = REC ? a.dec : nullptr;  // decision counters (parity runs only)
+  // this thread's halo column (threads 0..3: slots 0, 1 = cells i0-2, i0-1 and
+  // TXv+2, TXv+3 = cells i0+TXv, +1): x periodic wrap or transmissive clamp, once
+  int hx = tid < 2 ? i0 - 2 + tid : i0 + TXv + (tid - 2);
+  if (a.bcx == 0) hx = hx < 0 ? hx + a.nx : (hx >= a.nx ? hx - a.nx : hx);
+  else hx = hx < 0 ? 0 : (hx >= a.nx ? a.nx - 1 : hx);
+  // start of cell row jr (y: ghost rows, or clamp at a transmissive boundary)
+  auto row_ptr = [&](int jr, long long& cs) -> const double* {
+    cs = a.cs;
     if (jr < 0) {
-      if (a.ghost_lo) { base = a.ghost_lo; cs = a.gcs; jr += 2; } else jr = 0;
+      if (a.ghost_lo) { cs = a.gcs; return a.ghost_lo + (long long)(jr + 2) * a.nx; }
+      jr = 0;
     } else if (jr >= a.nrows) {
-      if (a.ghost_hi) { base = a.ghost_hi; cs = a.gcs; jr -= a.nrows; } else jr = a.nrows - 1;
+      if (a.ghost_hi) { cs = a.gcs; return a.ghost_hi + (long long)(jr - a.nrows) * a.nx; }
+      jr = a.nrows - 1;
     }
-    return __ldg(base + c * cs + (long long)jr * a.nx + gi);
+    return a.q + (long long)jr * a.nx;
   };
-  // this thread's ring column(s): own cell (slot tid + 2); threads 0..3 also the halo slots
+  // this thread's ring column(s): own cell (slot tid + 2), threads 0..3 also a halo slot
   auto load_row = [&](int jr, double v[4], double h[4]) {
+    long long cs;
+    const double* rb = row_ptr(jr, cs);
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-      v[c] = own ? cell(jr, i0 + tid, c) : 0.0;
-      h[c] = 0.0;
-    }
-    if (tid < 4) {  // halo slots 0, 1 (cells i0-2, i0-1) and TXv+2, TXv+3 (cells i0+TXv, +1)
-      const int gi = tid < 2 ? i0 - 2 + tid : i0 + TXv + (tid - 2);
-#pragma unroll
-      for (int c = 0; c < 4; ++c) h[c] = cell(jr, gi, c);
+      v[c] = own ? __ldg(rb + c * cs + i0 + tid) : 0.0;
+      h[c] = tid < 4 ? __ldg(rb + c * cs + hx) : 0.0;
     }
   };
   auto store_row = [&](int slot, const double v[4], const double h[4]) {
@@ -118,13 +119,13 @@ __global__ void __launch_bounds__(FTX, H2D_FV_MINB) fv_stage_kernel(const StageA
   double GS[4];
   {
     // counted only for the domain's bottom face (every other S face is the N face of a row below)
-    long long* dec = (a.dec && own && jb == 0 && a.count_bot) ? a.dec : nullptr;
+    long long* dec0 = (own && jb == 0 && a.count_bot) ? dec : nullptr;
     double s[4][4];
 #pragma unroll
     for (int t = 0; t < 4; ++t)
 #pragma unroll
       for (int c = 0; c < 4; ++c) s[t][c] = own ? ring[slot_of(-2 + t)][c][tid + 2] : 1.0;
-    if (own) face_flux<ORDER, 1>(s, gm1, gam, GS, dec);
+    if (own) face_flux<ORDER, 1>(s, gm1, gam, GS, dec0);
   }
 
   double lam = 0.0;
@@ -144,7 +145,6 @@ __global__ void __launch_bounds__(FTX, H2D_FV_MINB) fv_stage_kernel(const StageA
     // x faces: the W face of each own cell, plus the strip's last E face
     if (own) {
       double s[4][4], F[4];
-      long long* dec = a.dec;
 #pragma unroll
       for (int t = 0; t < 4; ++t)
 #pragma unroll
@@ -166,7 +166,6 @@ __global__ void __launch_bounds__(FTX, H2D_FV_MINB) fv_stage_kernel(const StageA
     double GN[4];
     if (own) {
       double s[4][4];
-      long long* dec = a.dec;
 #pragma unroll
       for (int t = 0; t < 4; ++t)
 #pragma unroll
@@ -188,8 +187,7 @@ __global__ void __launch_bounds__(FTX, H2D_FV_MINB) fv_stage_kernel(const StageA
       if (a.lam || a.bad) {
         const Prim w = prims(o, gm1);
         if (a.lam) lam = fmax(lam, fmax(fabs(w.u), fabs(w.v)) + fsqrt(gam * w.p * w.ri));
-        const bool fin = isfinite(o[0]) && isfinite(o[1]) && isfinite(o[2]) && isfinite(o[3]);
-        if (a.bad && (!fin || !(o[0] > 0.0) || !(w.p > 0.0))) atomicMin(a.bad, (unsigned long long)gidx);
+        if (a.bad && !admissible(o[0], w.p)) atomicMin(a.bad, (unsigned long long)gidx);
       }
     }
   }
@@ -215,8 +213,13 @@ int launch_fv_stage(int k, const StageArgs& a0, cudaStream_t s) {
   const int strips = (a.nx + FTX - 1) / FTX;
   a.rows = march_rows(a.nrows, strips, FRB);
   dim3 grid(strips, (a.nrows + a.rows - 1) / a.rows);
-  if (k == 1) fv_stage_kernel<1><<<grid, FTX, 0, s>>>(a);
-  else fv_stage_kernel<2><<<grid, FTX, 0, s>>>(a);
+  if (a.dec) {
+    if (k == 1) fv_stage_kernel<1, true><<<grid, FTX, 0, s>>>(a);
+    else fv_stage_kernel<2, true><<<grid, FTX, 0, s>>>(a);
+  } else {
+    if (k == 1) fv_stage_kernel<1, false><<<grid, FTX, 0, s>>>(a);
+    else fv_stage_kernel<2, false><<<grid, FTX, 0, s>>>(a);
+  }
   return (int)cudaPeekAtLastError();
 }
 

@@ -524,8 +524,7 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
         if (a.lam || a.bad) {  // dt wave speed and non-physical check share one reciprocal
           const Prim w = prims(o, gm1);
           if (a.lam) lam = fmax(lam, fmax(fabs(w.u), fabs(w.v)) + fsqrt(gam * w.p * w.ri));
-          const bool fin = isfinite(o[0]) && isfinite(o[1]) && isfinite(o[2]) && isfinite(o[3]);
-          if (a.bad && (!fin || !(o[0] > 0.0) || !(w.p > 0.0))) atomicMin(a.bad, (unsigned long long)(base + x));
+          if (a.bad && !admissible(o[0], w.p)) atomicMin(a.bad, (unsigned long long)(base + x));
         }
       }
       // a thread's line of one component is N contiguous doubles: one 32-B (P3) or
