@@ -168,8 +168,8 @@ __device__ __forceinline__ void block_max_to(double v, unsigned long long* dst, 
   }
 }
 
-__device__ __forceinline__ void count_dec(long long* dec, int which) {
-  if (dec) atomicAdd((unsigned long long*)&dec[which], 1ull);
+__device__ __forceinline__ void count_dec(long long* dec, int which, int w = 1) {
+  if (dec && w) atomicAdd((unsigned long long*)&dec[which], (unsigned long long)w);
 }
 
 // minmod of two arguments (ties return the first argument, zero if the
@@ -178,15 +178,18 @@ __device__ __forceinline__ void count_dec(long long* dec, int which) {
 // as a tie (slot 4), not by outcome: its branch may legitimately differ between
 // two fp64 evaluation orders.
 #define DEC_TIE 1e-12
-__device__ __forceinline__ double minmod2(double a, double b, long long* dec) {
-  // value without branches: both positive -> the smaller, both negative -> the
-  // larger (equal arguments give the same value either way), else 0
-  const double r = (a > 0.0 && b > 0.0) ? fmin(a, b) : ((a < 0.0 && b < 0.0) ? fmax(a, b) : 0.0);
+// (w: how many of the paper's face evaluations this one call stands for)
+__device__ __forceinline__ double minmod2(double a, double b, long long* dec, int w = 1) {
+  // value without branches: the argument of smaller magnitude when both have the
+  // same strict sign (equal magnitudes: equal values), else 0
+  const bool same = (a > 0.0 && b > 0.0) || (a < 0.0 && b < 0.0);
+  const double m = fabs(a) <= fabs(b) ? a : b;
+  const double r = __longlong_as_double(same ? __double_as_longlong(m) : 0ll);  // 9 SASS ops
   if (dec) {
     int which = 1;
     if ((a > 0.0 && b > 0.0) || (a < 0.0 && b < 0.0)) which = (fabs(a) <= fabs(b)) ? 2 : 3;
     if (fabs(a) <= DEC_TIE || fabs(b) <= DEC_TIE || fabs(a - b) <= DEC_TIE) which = 4;
-    count_dec(dec, which);
+    count_dec(dec, which, w);
   }
   return r;
 }

@@ -23,35 +23,42 @@ namespace {
 constexpr int FTX = 128, FRB = 64, FNS = 5;   // cells per strip, rows per march, ring rows
 constexpr int FW = FTX + 4;                    // ring row width: 2 halo cells each side
 
-// face states from the stencil (i-1, i, i+1, i+2) for the face i+1/2
+// the two reconstructed face values of cell i (stencil i-1, i, i+1): lo at its
+// i-1/2 face, hi at its i+1/2 face (the face states of P:346-351; SURVEY C8 with
+// the same arithmetic as the per-face form, so values are bitwise those of
+// reconstructing at each face).  w = how many face evaluations of the paper's
+// form this one reconstruction stands for (decision counting only).
 template <int ORDER>
-__device__ __forceinline__ void muscl(double qm1, double q0, double q1, double q2, double& qW, double& qE,
-                                      long long* dec) {
+__device__ __forceinline__ void cell_faces(double qm, double q0, double qp, double& lo, double& hi, long long* dec,
+                                           int w) {
   if (ORDER == 1) {
-    const double s0 = minmod2(q0 - qm1, q1 - q0, dec);
-    const double s1 = minmod2(q1 - q0, q2 - q1, dec);
-    qW = q0 + 0.5 * s0;
-    qE = q1 - 0.5 * s1;
+    const double s = minmod2(q0 - qm, qp - q0, dec, w);
+    hi = q0 + 0.5 * s;
+    lo = q0 - 0.5 * s;
   } else {  // kappa = 1/3, beta = (3 - kappa)/(1 - kappa) = 4
     constexpr double kap = 1.0 / 3.0, beta = (3.0 - kap) / (1.0 - kap);
-    const double dm0 = q0 - qm1, dp0 = q1 - q0, dm1 = q1 - q0, dp1 = q2 - q1;
-    qW = q0 + 0.25 * ((1.0 - kap) * minmod2(dm0, beta * dp0, dec) + (1.0 + kap) * minmod2(dp0, beta * dm0, dec));
-    qE = q1 - 0.25 * ((1.0 - kap) * minmod2(dp1, beta * dm1, dec) + (1.0 + kap) * minmod2(dm1, beta * dp1, dec));
+    const double dm = q0 - qm, dp = qp - q0;
+    const double A = minmod2(dm, beta * dp, dec, w), B = minmod2(dp, beta * dm, dec, w);
+    hi = q0 + 0.25 * ((1.0 - kap) * A + (1.0 + kap) * B);
+    lo = q0 - 0.25 * ((1.0 - kap) * B + (1.0 + kap) * A);
   }
 }
 
 // reconstruct both face states from a 4-cell stencil s[t][c] and take Rusanov
 template <int ORDER, int DIR>
 __device__ __forceinline__ void face_flux(const double s[4][4], double gm1, double gam, double F[4], long long* dec) {
-  double qW[4], qE[4], fL[4], fR[4];
+  double qW[4], qE[4], fL[4], fR[4], dummy;
 #pragma unroll
-  for (int c = 0; c < 4; ++c) muscl<ORDER>(s[0][c], s[1][c], s[2][c], s[3][c], qW[c], qE[c], dec);
+  for (int c = 0; c < 4; ++c) {
+    cell_faces<ORDER>(s[0][c], s[1][c], s[2][c], dummy, qW[c], dec, 1);
+    cell_faces<ORDER>(s[1][c], s[2][c], s[3][c], qE[c], dummy, dec, 1);
+  }
   rusanov<DIR>(qW, qE, gm1, gam, F, fL, fR);
 }
 }  // namespace
 
 #ifndef H2D_FV_MINB
-#define H2D_FV_MINB 4
+#define H2D_FV_MINB 3  // 168 registers, no spills (A/B: +12 % over 4 at 128 registers)
 #endif
 template <int ORDER, bool REC>
 __global__ void __launch_bounds__(FTX, H2D_FV_MINB) fv_stage_kernel(const StageArgs a) {
@@ -115,17 +122,25 @@ __global__ void __launch_bounds__(FTX, H2D_FV_MINB) fv_stage_kernel(const StageA
   __syncthreads();
   auto slot_of = [&](int r) { return ((r % FNS) + FNS) % FNS; };  // r = row - jb
 
-  // S face of the first row (between rows jb-1 and jb)
-  double GS[4];
+  // y reconstruction once per cell: the hi (N-side) state of the row below the
+  // current one is carried in registers.  Decision weights: an own row stands
+  // for its S and N face evaluations (2); the ghost row below the domain's first
+  // row (bottom face, counted once: count_bot) and the one above the strip's
+  // last row when that is the domain's top (1); rows of a neighbouring CTA are
+  // counted by their owner (0).
+  double GS[4], yHi[4];
   {
-    // counted only for the domain's bottom face (every other S face is the N face of a row below)
-    long long* dec0 = (own && jb == 0 && a.count_bot) ? dec : nullptr;
-    double s[4][4];
+    double lo[4], hi[4], dm;
+    const int wb = (jb == 0 && a.count_bot) ? 1 : 0;
 #pragma unroll
-    for (int t = 0; t < 4; ++t)
-#pragma unroll
-      for (int c = 0; c < 4; ++c) s[t][c] = own ? ring[slot_of(-2 + t)][c][tid + 2] : 1.0;
-    if (own) face_flux<ORDER, 1>(s, gm1, gam, GS, dec0);
+    for (int c = 0; c < 4; ++c) {
+      const double r0 = own ? ring[slot_of(-2)][c][tid + 2] : 1.0, r1 = own ? ring[slot_of(-1)][c][tid + 2] : 1.0;
+      const double r2 = own ? ring[slot_of(0)][c][tid + 2] : 1.0, r3 = own ? ring[slot_of(1)][c][tid + 2] : 1.0;
+      cell_faces<ORDER>(r0, r1, r2, dm, hi[c], own ? dec : nullptr, wb);
+      cell_faces<ORDER>(r1, r2, r3, lo[c], yHi[c], own ? dec : nullptr, 2);
+    }
+    double fL[4], fR[4];
+    if (own) rusanov<1>(hi, lo, gm1, gam, GS, fL, fR);
   }
 
   double lam = 0.0;
@@ -162,15 +177,19 @@ __global__ void __launch_bounds__(FTX, H2D_FV_MINB) fv_stage_kernel(const StageA
         for (int c = 0; c < 4; ++c) sF[tid + 1][c] = F[c];
       }
     }
-    // N face of the column (rows r-1 .. r+2), carried as the next row's S face
+    // N face of the column: carried hi state of row r, lo state of row r+1
+    // (reconstructed now from rows r..r+2; its hi state is carried on)
     double GN[4];
     if (own) {
-      double s[4][4];
+      const int wn = (r + 1 < RBv) ? 2 : ((jb + RBv == a.nrows) ? 1 : 0);
+      double lo[4], hi[4], fL[4], fR[4];
 #pragma unroll
-      for (int t = 0; t < 4; ++t)
+      for (int c = 0; c < 4; ++c)
+        cell_faces<ORDER>(ring[sc][c][tid + 2], ring[slot_of(r + 1)][c][tid + 2], ring[slot_of(r + 2)][c][tid + 2],
+                          lo[c], hi[c], dec, wn);
+      rusanov<1>(yHi, lo, gm1, gam, GN, fL, fR);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) s[t][c] = ring[slot_of(r - 1 + t)][c][tid + 2];
-      face_flux<ORDER, 1>(s, gm1, gam, GN, dec);
+      for (int c = 0; c < 4; ++c) yHi[c] = hi[c];
     }
     __syncthreads();
     if (own) {
