@@ -58,12 +58,13 @@ __device__ __forceinline__ void face_flux(const double s[4][4], double gm1, doub
 }  // namespace
 
 #ifndef H2D_FV_MINB
-#define H2D_FV_MINB 3  // 168 registers, no spills (A/B: +12 % over 4 at 128 registers)
+#define H2D_FV_MINB 4  // 124 registers, no spills (A/B: +12 % over 3)
 #endif
 template <int ORDER, bool REC>
 __global__ void __launch_bounds__(FTX, H2D_FV_MINB) fv_stage_kernel(const StageArgs a) {
   __shared__ double ring[FNS][4][FW];
   __shared__ double sF[FTX + 1][4];   // W-face fluxes of the row (+ the strip's last E face)
+  __shared__ double sXL[2][4][FTX + 2], sXH[2][4][FTX + 2];  // x face states lo/hi per cell, 2 rows
   __shared__ double sred[32];
   double dtv = 1.0;
   if (a.dt) {
@@ -143,6 +144,32 @@ __global__ void __launch_bounds__(FTX, H2D_FV_MINB) fv_stage_kernel(const StageA
     if (own) rusanov<1>(hi, lo, gm1, gam, GS, fL, fR);
   }
 
+  // x reconstruction once per cell, one row ahead, into buffer buf: slot s holds
+  // cell i0-1+s (own cells 1..TXv; slot 0 / TXv+1 the strip's halo cells, whose
+  // hi / lo state the strip's end faces need).  Decision weights as for y: own
+  // cells 2, the domain's end cells' ghosts 1, a neighbouring strip's cells 0.
+  auto recon_x = [&](int rs, int buf) {
+    double dm;
+    if (own) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        cell_faces<ORDER>(ring[rs][c][tid + 1], ring[rs][c][tid + 2], ring[rs][c][tid + 3], sXL[buf][c][tid + 1],
+                          sXH[buf][c][tid + 1], dec, 2);
+    }
+    if (tid == 0) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        cell_faces<ORDER>(ring[rs][c][0], ring[rs][c][1], ring[rs][c][2], dm, sXH[buf][c][0], dec, i0 == 0 ? 1 : 0);
+    }
+    if (tid == TXv - 1) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        cell_faces<ORDER>(ring[rs][c][TXv + 1], ring[rs][c][TXv + 2], ring[rs][c][TXv + 3], sXL[buf][c][TXv + 1], dm,
+                          dec, (i0 + TXv == a.nx) ? 1 : 0);
+    }
+  };
+  recon_x(slot_of(0), 0);  // read after the first loop barrier
+
   double lam = 0.0;
   const double bdt = a.bcoef * dtv;
   for (int r = 0; r < RBv; ++r) {
@@ -157,26 +184,31 @@ __global__ void __launch_bounds__(FTX, H2D_FV_MINB) fv_stage_kernel(const StageA
 #pragma unroll
       for (int c = 0; c < 4; ++c) q0v[c] = a.q0[c * a.cs + gidx];
     }
-    // x faces: the W face of each own cell, plus the strip's last E face
+    // x faces: the W face of each own cell, plus the strip's last E face, from
+    // the face states reconstructed one row earlier
     if (own) {
-      double s[4][4], F[4];
+      const int b = r & 1;
+      double qL[4], qR[4], F[4], fL[4], fR[4];
 #pragma unroll
-      for (int t = 0; t < 4; ++t)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) s[t][c] = ring[sc][c][tid + t];   // cells tid-2 .. tid+1
-      face_flux<ORDER, 0>(s, gm1, gam, F, dec);
+      for (int c = 0; c < 4; ++c) {
+        qL[c] = sXH[b][c][tid];
+        qR[c] = sXL[b][c][tid + 1];
+      }
+      rusanov<0>(qL, qR, gm1, gam, F, fL, fR);
 #pragma unroll
       for (int c = 0; c < 4; ++c) sF[tid][c] = F[c];
       if (tid == TXv - 1) {
 #pragma unroll
-        for (int t = 0; t < 4; ++t)
-#pragma unroll
-          for (int c = 0; c < 4; ++c) s[t][c] = ring[sc][c][tid + 1 + t];
-        face_flux<ORDER, 0>(s, gm1, gam, F, (i0 + TXv == a.nx) ? dec : nullptr);
+        for (int c = 0; c < 4; ++c) {
+          qL[c] = sXH[b][c][tid + 1];
+          qR[c] = sXL[b][c][tid + 2];
+        }
+        rusanov<0>(qL, qR, gm1, gam, F, fL, fR);
 #pragma unroll
         for (int c = 0; c < 4; ++c) sF[tid + 1][c] = F[c];
       }
     }
+    if (r + 1 < RBv) recon_x(slot_of(r + 1), (r + 1) & 1);
     // N face of the column: carried hi state of row r, lo state of row r+1
     // (reconstructed now from rows r..r+2; its hi state is carried on)
     double GN[4];
