@@ -44,6 +44,15 @@ WORKLOADS = {
     "cpr_p2_4096": ("cpr", 2, 4096, 4096, 0.13, False),
     "cpr_p1_8192": ("cpr", 1, 8192, 8192, 0.24, False),
     "cpr_p4_4096": ("cpr", 4, 4096, 4096, 0.05, False),
+    "ndg_p1_8192": ("ndg", 1, 8192, 8192, 0.24, False),
+    "ndg_p2_4096": ("ndg", 2, 4096, 4096, 0.13, False),
+    "ndg_p4_4096": ("ndg", 4, 4096, 4096, 0.05, False),
+    "dg_p1_8192": ("dg", 1, 8192, 8192, 0.24, False),
+    "dg_p2_4096": ("dg", 2, 4096, 4096, 0.13, False),
+    "dg_p4_4096": ("dg", 4, 4096, 4096, 0.05, False),
+    "sd_p1_8192": ("sd", 1, 8192, 8192, 0.3, False),
+    "sd_p2_4096": ("sd", 2, 4096, 4096, 0.2, False),
+    "sd_p4_4096": ("sd", 4, 4096, 4096, 0.08, False),
     "fv2_16384": ("fv", 1, 16384, 16384, 0.37, False),
     "fv3_16384": ("fv", 2, 16384, 16384, 0.37, False),
 }

@@ -27,13 +27,23 @@ namespace h2d {
 
 namespace {
 
-template <int K> struct LTile;
-template <> struct LTile<1> { static constexpr int TX = 64, RB = 64; };
-template <> struct LTile<2> { static constexpr int TX = 32, RB = 64; };
-template <> struct LTile<3> { static constexpr int TX = 32, RB = 64; };
-template <> struct LTile<4> { static constexpr int TX = 32, RB = 64; };
-
+// strip width (elements) per method and order: DG keeps g of every point in
+// smem, so narrower strips keep 2+ CTAs per SM (A/B on 4096^2: DG 16 > 32 by
+// 37 % at P3, 3-6 % at P2/P4; SD 32 > 16 by 10 % at P3, 16 > 32 by 13 % at P4)
+#ifndef H2D_DG_TX
+#define H2D_DG_TX 16
+#endif
+#ifndef H2D_SD_TX
+#define H2D_SD_TX (K == 3 ? 32 : 16)
+#endif
+#ifndef H2D_LMINB
+#define H2D_LMINB 1
+#endif
 enum { LM_DG = 2, LM_SD = 4 };
+template <int M, int K> struct LTile {
+  static constexpr int TX = K == 1 ? 64 : (M == LM_DG ? H2D_DG_TX : H2D_SD_TX), RB = 64;
+};
+
 constexpr int NSTG = 3;
 
 struct LMaps {
@@ -79,7 +89,7 @@ LTab make_ltab() {
 template <int M, int K>
 struct L {
   static constexpr int N = K + 1, NP = N * N;
-  static constexpr int TX = LTile<K>::TX, RB = LTile<K>::RB, NT = TX * N;
+  static constexpr int TX = LTile<M, K>::TX, RB = LTile<M, K>::RB, NT = TX * N;
   static constexpr bool SWZ = (NP == 16);
   static constexpr int NSL = TX + 2;
   static constexpr int CW = (NP + 1 + 1) & ~1;
@@ -159,7 +169,7 @@ __device__ __forceinline__ const void* piece_src(const double* src) {
 }  // namespace
 
 template <int M, int K>
-__global__ void __launch_bounds__(L<M, K>::NT) gl_stage_kernel(const StageArgs a, const LTab tab,
+__global__ void __launch_bounds__(L<M, K>::NT, H2D_LMINB) gl_stage_kernel(const StageArgs a, const LTab tab,
                                                                const __grid_constant__ LMaps maps) {
   using H = L<M, K>;
   using T = LOps<K>;
