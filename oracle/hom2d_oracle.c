@@ -20,8 +20,10 @@
  * SSP-RK3 driver (no fusion).  Readings of ambiguous passages follow SURVEY
  * section 8(c).2 (Q1..Q35) and are listed in DESIGN.md.
  *
- * Parity pins: see tests/test_oracle_*.py.  Parity unpinned: the absolute shock
- * tube centreline profile (Fig. 5; no reference data available).
+ * Parity pins: see tests/test_oracle_*.py.  The shock-tube centreline profile
+ * (Fig. 5; Toro's digitised curve is not available) is pinned by
+ * convergence to a radially symmetric 1-D reference (oracle/radial1d.py, itself
+ * pinned to the exact Riemann solution): tests/test_radial_reference.py.
  */
 #include <math.h>
 #include <stdint.h>
