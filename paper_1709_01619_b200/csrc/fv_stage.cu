@@ -31,16 +31,19 @@ constexpr int FW = FTX + 4;                    // ring row width: 2 halo cells e
 template <int ORDER>
 __device__ __forceinline__ void cell_faces(double qm, double q0, double qp, double& lo, double& hi, long long* dec,
                                            int w) {
+  // explicit rounding (no contraction freedom): a face state is bitwise the same
+  // wherever it is evaluated (prologue or carried), so results do not depend on
+  // how the rows are split over CTAs / launches / ranks
   if (ORDER == 1) {
     const double s = minmod2(q0 - qm, qp - q0, dec, w);
-    hi = q0 + 0.5 * s;
-    lo = q0 - 0.5 * s;
+    hi = __fma_rn(0.5, s, q0);
+    lo = __fma_rn(-0.5, s, q0);
   } else {  // kappa = 1/3, beta = (3 - kappa)/(1 - kappa) = 4
     constexpr double kap = 1.0 / 3.0, beta = (3.0 - kap) / (1.0 - kap);
     const double dm = q0 - qm, dp = qp - q0;
     const double A = minmod2(dm, beta * dp, dec, w), B = minmod2(dp, beta * dm, dec, w);
-    hi = q0 + 0.25 * ((1.0 - kap) * A + (1.0 + kap) * B);
-    lo = q0 - 0.25 * ((1.0 - kap) * B + (1.0 + kap) * A);
+    hi = __fma_rn(0.25, __fma_rn(1.0 - kap, A, __dmul_rn(1.0 + kap, B)), q0);
+    lo = __fma_rn(-0.25, __fma_rn(1.0 - kap, B, __dmul_rn(1.0 + kap, A)), q0);
   }
 }
 
@@ -72,8 +75,8 @@ __global__ void __launch_bounds__(FTX, H2D_FV_MINB) fv_stage_kernel(const StageA
     if (dtv == 0.0) return;
   }
   const int tid = threadIdx.x;
-  const int i0 = blockIdx.x * FTX, jb = blockIdx.y * a.rows;
-  const int TXv = min(FTX, a.nx - i0), RBv = min(a.rows, a.nrows - jb);
+  const int i0 = blockIdx.x * FTX, jb = a.row_lo + blockIdx.y * a.rows;
+  const int TXv = min(FTX, a.nx - i0), RBv = min(a.rows, a.row_hi - jb);
   const double gam = a.gamma, gm1 = a.gamma - 1.0;
   const bool own = tid < TXv;
 
@@ -262,8 +265,10 @@ int march_rows(int nrows, int strips, int rb_max) {
 int launch_fv_stage(int k, const StageArgs& a0, cudaStream_t s) {
   StageArgs a = a0;
   const int strips = (a.nx + FTX - 1) / FTX;
-  a.rows = march_rows(a.nrows, strips, FRB);
-  dim3 grid(strips, (a.nrows + a.rows - 1) / a.rows);
+  const int nr = row_range(a);
+  if (nr <= 0) return 0;
+  a.rows = march_rows(nr, strips, FRB);
+  dim3 grid(strips, (nr + a.rows - 1) / a.rows);
   if (a.dec) {
     if (k == 1) fv_stage_kernel<1, true><<<grid, FTX, 0, s>>>(a);
     else fv_stage_kernel<2, true><<<grid, FTX, 0, s>>>(a);

@@ -200,8 +200,8 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
     if (dtv == 0.0) return;  // clipped-out step (t == t_end): uniform across the grid
   }
   const int tid = threadIdx.x;
-  const int i0 = blockIdx.x * TX, jb = blockIdx.y * a.rows;
-  const int TXv = min(TX, a.nx - i0), RBv = min(a.rows, a.nrows - jb);
+  const int i0 = blockIdx.x * TX, jb = a.row_lo + blockIdx.y * a.rows;
+  const int TXv = min(TX, a.nx - i0), RBv = min(a.rows, a.row_hi - jb);
   const double gam = a.gamma, gm1 = a.gamma - 1.0;
   const int lx = tid / N, b = tid - lx * N;
   const bool own = lx < TXv;
@@ -604,8 +604,10 @@ static int launch_g(const StageArgs& a, cudaStream_t s) {
   }
   StageArgs b = a;
   const int strips = (a.nx + H::TX - 1) / H::TX;
-  b.rows = march_rows(a.nrows, strips, H::RB);
-  dim3 grid(strips, (a.nrows + b.rows - 1) / b.rows);
+  const int nr = row_range(b);
+  if (nr <= 0) return 0;
+  b.rows = march_rows(nr, strips, H::RB);
+  dim3 grid(strips, (nr + b.rows - 1) / b.rows);
   gll_stage_kernel<M, K><<<grid, H::NT, H::SMEM, s>>>(b, tab, maps);
   return (int)cudaPeekAtLastError();
 }

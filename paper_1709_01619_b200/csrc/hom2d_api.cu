@@ -19,6 +19,8 @@ struct hom2d {
   hom2d_config cfg;
   int rank = 0, nranks = 1, device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t xstream = nullptr;          // nranks > 1: halo exchange stream (highest priority)
+  cudaEvent_t ev_in = nullptr, ev_halo = nullptr;
   ncclComm_t comm = nullptr;
   int row0 = 0, nrows = 0, np = 1, G = 1;  // G ghost rows (HO 1, FV 2)
   long long nloc = 0;                      // values per component of the local strip
@@ -160,7 +162,7 @@ hom2d_strip_plan_t plan_of(const hom2d_config& c, int rank, int R) {
 // and "recv lo" before "recv hi", so that with 2 periodic ranks (peer_lo ==
 // peer_hi) NCCL's in-order matching pairs last->lo and first->hi.
 hom2d_status exchange(hom2d* h, const double* X, long long comp_stride, long long row_vals, const double** lo,
-                      const double** hi, long long* gcs, double* rlo, double* rhi, int G) {
+                      const double** hi, long long* gcs, double* rlo, double* rhi, int G, cudaStream_t xs) {
   const int R = h->nranks;
   if (h->ovr_active) {  // hom2d_residual_strip: caller-supplied ghost rows
     *gcs = (long long)G * row_vals;
@@ -181,10 +183,10 @@ hom2d_status exchange(hom2d* h, const double* X, long long comp_stride, long lon
   for (int c = 0; c < 4; ++c) {
     const double* first = X + c * comp_stride;
     const double* last = X + c * comp_stride + (long long)(h->nrows - G) * row_vals;
-    if (P.has_hi) NC(h, ncclSend(last, cnt, ncclDouble, P.peer_hi, h->comm, h->stream));
-    if (P.has_lo) NC(h, ncclSend(first, cnt, ncclDouble, P.peer_lo, h->comm, h->stream));
-    if (P.has_lo) NC(h, ncclRecv(rlo + c * cnt, cnt, ncclDouble, P.peer_lo, h->comm, h->stream));
-    if (P.has_hi) NC(h, ncclRecv(rhi + c * cnt, cnt, ncclDouble, P.peer_hi, h->comm, h->stream));
+    if (P.has_hi) NC(h, ncclSend(last, cnt, ncclDouble, P.peer_hi, h->comm, xs));
+    if (P.has_lo) NC(h, ncclSend(first, cnt, ncclDouble, P.peer_lo, h->comm, xs));
+    if (P.has_lo) NC(h, ncclRecv(rlo + c * cnt, cnt, ncclDouble, P.peer_lo, h->comm, xs));
+    if (P.has_hi) NC(h, ncclRecv(rhi + c * cnt, cnt, ncclDouble, P.peer_hi, h->comm, xs));
   }
   NC(h, ncclGroupEnd());
   const bool lo_ok = P.has_lo, hi_ok = P.has_hi;
@@ -194,12 +196,37 @@ hom2d_status exchange(hom2d* h, const double* X, long long comp_stride, long lon
   return HOM2D_OK;
 }
 
+int launch_stage(hom2d* h, const StageArgs& s) {
+  if (h->cfg.method == HOM2D_FV) return launch_fv_stage(h->cfg.k, s, h->stream);
+  int method = h->cfg.method;
+  if (method == HOM2D_CPR && !h->cfg.cpr_chain_rule) method = HOM2D_NDG;  // flux-differentiation CPR == NDG
+  return (method == HOM2D_CPR || method == HOM2D_NDG) ? launch_gll_stage(method, h->cfg.k, s, h->stream)
+                                                      : launch_gl_stage(method, h->cfg.k, s, h->stream);
+}
+
+// One RK stage.  nranks == 1: one launch over the strip.  nranks > 1 (SURVEY
+// 8(e) overlap): the G boundary rows of the stage input go to the neighbours on
+// the exchange stream while the compute stream updates the interior rows
+// [G, nrows-G) (which read no ghost row); the two boundary bands follow once the
+// ghost rows have arrived.  Per-element arithmetic does not depend on the
+// launch split, so the result is bitwise the single-launch one.
 hom2d_status run_stage(hom2d* h, const double* q, const double* q0, double* out, double a0, double a1, double b,
                        const double* dt, unsigned long long* lam, unsigned long long* bad) {
   StageArgs s{};
   const long long row_vals = (long long)h->cfg.nx * h->np;
-  hom2d_status st = exchange(h, q, h->nloc, row_vals, &s.ghost_lo, &s.ghost_hi, &s.gcs, h->glo, h->ghi, h->G);
+  const int G = h->G;
+  const bool split = h->nranks > 1 && h->nrows > 2 * G;
+  const bool async = split && h->comm && !h->ovr_active;
+  const bool timed = 2 * (h->ev_used + 1) <= (int)h->ev.size();
+  if (timed) cudaEventRecord(h->ev[2 * h->ev_used], h->stream);
+  if (async) {  // the exchange stream may read q only once its producer has finished
+    CU(h, cudaEventRecord(h->ev_in, h->stream));
+    CU(h, cudaStreamWaitEvent(h->xstream, h->ev_in, 0));
+  }
+  hom2d_status st = exchange(h, q, h->nloc, row_vals, &s.ghost_lo, &s.ghost_hi, &s.gcs, h->glo, h->ghi, G,
+                             async ? h->xstream : h->stream);
   if (st) return st;
+  if (async) CU(h, cudaEventRecord(h->ev_halo, h->xstream));
   s.q = q; s.q0 = q0; s.out = out; s.nx = h->cfg.nx; s.nrows = h->nrows; s.cs = h->nloc;
   s.bcx = h->cfg.bc;
   const double dx = (h->cfg.xmax - h->cfg.xmin) / h->cfg.nx, dy = (h->cfg.ymax - h->cfg.ymin) / h->cfg.ny;
@@ -209,19 +236,24 @@ hom2d_status run_stage(hom2d* h, const double* q, const double* q0, double* out,
   s.lam = lam; s.bad = bad;
   s.dec = h->cfg.record_decisions ? h->dec : nullptr;
   s.count_bot = (h->rank == 0);
-  int e;
-  const bool timed = 2 * (h->ev_used + 1) <= (int)h->ev.size();
-  if (timed) cudaEventRecord(h->ev[2 * h->ev_used], h->stream);
-  if (h->cfg.method == HOM2D_FV) {
-    e = launch_fv_stage(h->cfg.k, s, h->stream);
+  int e = 0;
+  if (!split) {
+    s.row_lo = 0; s.row_hi = h->nrows;
+    e = launch_stage(h, s);
+    h->launches++;
   } else {
-    int method = h->cfg.method;
-    if (method == HOM2D_CPR && !h->cfg.cpr_chain_rule) method = HOM2D_NDG;  // flux-differentiation CPR == NDG
-    e = (method == HOM2D_CPR || method == HOM2D_NDG) ? launch_gll_stage(method, h->cfg.k, s, h->stream)
-                                                      : launch_gl_stage(method, h->cfg.k, s, h->stream);
+    StageArgs in = s;  // interior rows: never read the ghost rows
+    in.row_lo = G; in.row_hi = h->nrows - G;
+    e = launch_stage(h, in);
+    if (!e && async) e = (int)cudaStreamWaitEvent(h->stream, h->ev_halo, 0);
+    StageArgs lo = s, hi = s;
+    lo.row_lo = 0; lo.row_hi = G;
+    hi.row_lo = h->nrows - G; hi.row_hi = h->nrows;
+    if (!e) e = launch_stage(h, lo);
+    if (!e) e = launch_stage(h, hi);
+    h->launches += 3;
   }
   if (timed) cudaEventRecord(h->ev[2 * h->ev_used++ + 1], h->stream);
-  h->launches++;
   if (e) return fail(h, HOM2D_ERR_CUDA, "stage kernel launch: %s", cudaGetErrorString((cudaError_t)e));
   return HOM2D_OK;
 }
@@ -235,7 +267,7 @@ hom2d_status run_limiter(hom2d* h, double* X, const double* dt = nullptr) {
   const long long ne = (long long)h->cfg.nx * h->nrows;
   const double *lo, *hi;
   long long gcs;
-  hom2d_status st = exchange(h, h->qbar, ne, h->cfg.nx, &lo, &hi, &gcs, h->qblo, h->qbhi, 1);
+  hom2d_status st = exchange(h, h->qbar, ne, h->cfg.nx, &lo, &hi, &gcs, h->qblo, h->qbhi, 1, h->stream);
   if (st) return st;
   launch_limit(A, X, h->qbar, lo, hi, gcs, h->cfg.bc, h->cfg.limiter_eps,
                h->cfg.record_decisions ? h->dec : nullptr, h->stream);
@@ -331,6 +363,14 @@ hom2d_status hom2d_create(const hom2d_config* cfg, const hom2d_dist* dist, void*
     ncclUniqueId id;
     memcpy(&id, dist->nccl_id, sizeof(id));
     if (ncclCommInitRank(&h->comm, R, id, h->rank) != ncclSuccess) { cudaFreeHost(h->t_host); delete h; return HOM2D_ERR_NCCL; }
+    int prio_lo = 0, prio_hi = 0;
+    cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+    if (cudaStreamCreateWithPriority(&h->xstream, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->ev_in, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->ev_halo, cudaEventDisableTiming) != cudaSuccess) {
+      hom2d_destroy(h);
+      return HOM2D_ERR_CUDA;
+    }
   }
   cudaMemsetAsync(h->lam, 0, 4 * sizeof(unsigned long long), h->stream);
   if (reset_clock(h, 0.0)) { hom2d_destroy(h); return HOM2D_ERR_CUDA; }
@@ -583,7 +623,11 @@ void hom2d_destroy(hom2d* h) {
   if (!h) return;
   if (h->stream) cudaStreamSynchronize(h->stream); else cudaDeviceSynchronize();
   for (cudaEvent_t e : h->ev) cudaEventDestroy(e);
+  if (h->xstream) cudaStreamSynchronize(h->xstream);
   if (h->comm) ncclCommDestroy(h->comm);
+  if (h->ev_in) cudaEventDestroy(h->ev_in);
+  if (h->ev_halo) cudaEventDestroy(h->ev_halo);
+  if (h->xstream) cudaStreamDestroy(h->xstream);
   if (h->t_host) cudaFreeHost(h->t_host);
   delete h;
 }

@@ -29,8 +29,16 @@ struct StageArgs {
   unsigned long long* bad; // optional: atomicMin of the first non-physical point index
   long long* dec;          // optional: decision counters [8]
   int count_bot;           // this strip owns the domain's bottom face row (decision counting)
+  int row_lo, row_hi;      // this launch updates strip rows [row_lo, row_hi) (row_hi == 0: all rows);
+                          // it may read rows row_lo-G .. row_hi+G-1 (ghost rows outside the strip)
   int rows;                // marching kernels: element rows per CTA (set by the launcher)
 };
+
+// normalise the launch's row range; returns its row count
+inline int row_range(StageArgs& a) {
+  if (a.row_hi <= 0) { a.row_lo = 0; a.row_hi = a.nrows; }
+  return a.row_hi - a.row_lo;
+}
 
 // rows per CTA for a marching kernel: enough CTAs to fill the GPU (>= 4 per SM),
 // at most rb_max, at least 4 (the march costs 1-2 prologue rows)

@@ -27,10 +27,14 @@ def P():
 @pytest.mark.parametrize("method,k", CASES)
 @pytest.mark.parametrize("G", [2, 4])
 @pytest.mark.parametrize("bc", [0, 1])
-def test_strips_bitwise(orc, P, method, k, G, bc):
+@pytest.mark.parametrize("thin", [False, True])
+def test_strips_bitwise(orc, P, method, k, G, bc, thin):
+    """thin=False: nrows > 2G, the stage runs as interior rows + two boundary
+    bands (the overlapped multi-GPU launch split); thin=True: nrows <= 2G, one
+    launch after the exchange."""
     import torch
     from paper_1709_01619_b200.inputs import perturb
-    rows = 8 if method == "fv" else 5
+    rows = (3 if thin else 8) if method == "fv" else (2 if thin else 5)
     nx, ny = 19, rows * G
     npe = 1 if method == "fv" else (k + 1) ** 2
     box = (-5.0, 5.0, -5.0, 5.0)
