@@ -8,11 +8,12 @@
 //  * traces are interpolated (DG: Alg. 2; SD: flux points 0 and n of a line),
 //    the W neighbour's E trace is interpolated by the thread on its right from
 //    the ring, the N/S traces from the element's columns;
-//  * DG is evaluated in its equivalent strong form with the Radau (g_DG)
-//    correction on GL points (the weak form's surface terms l_a(+-1)/w_a equal
-//    g'_R/L(xi_a), SBP identity -- pinned in tests/test_oracle_pins.py P7):
-//    R = -(2/dx)[D f + g'_L (F^W - f_W) + g'_R (F^E - f_E)] - (2/dy)[...] with
-//    f_W, f_E the INTERPOLATED flux at the edges (sum-factorised, no dense M^-1);
+//  * DG is evaluated in the weak form of Eq. (19) with n-point GL collocation
+//    (SURVEY C6), sum-factorised and divided by the diagonal mass w_a w_b:
+//    R = (2/dx)[sum_l (w_l/w_a) l'_a(xi_l) f_l - (l_a(1) F^E - l_a(-1) F^W)/w_a]
+//      + (2/dy)[... g, F^N, F^S ...]  -- only the Rusanov face fluxes enter, no
+//    interpolated edge flux and no jump pass (one barrier per row fewer than
+//    the equivalent strong form with the g_DG correction, SBP identity P7);
 //  * SD interpolates each line and each column to its n+1 flux points, evaluates
 //    the interior flux points and differentiates the flux polynomial at the
 //    solution points; the end flux points carry the Rusanov fluxes;
@@ -54,17 +55,17 @@ struct LMaps {
 template <int K>
 struct LOps {
   static constexpr int N = K + 1;
-  static constexpr int D = 0;                  // D_gl[N][N]
-  static constexpr int GL = D + N * N;         // g'_L at GL points
-  static constexpr int GR = GL + N;            // g'_R at GL points
-  static constexpr int EL = GR + N;            // l_l(-1)
+  static constexpr int EL = 0;                 // l_l(-1)
   static constexpr int ER = EL + N;            // l_l(+1)
   static constexpr int SI = ER + N;            // sd_I[N+1][N]
   static constexpr int SD = SI + (N + 1) * N;  // sd_D[N][N+1]
-  static constexpr int TOT = SD + N * (N + 1);
+  static constexpr int DV = SD + N * (N + 1);  // DG volume operator (w_l / w_a) l'_a(xi_l)  [N][N]
+  static constexpr int SR = DV + N * N;        // DG surface weights l_a(+1) / w_a
+  static constexpr int SL = SR + N;            // DG surface weights l_a(-1) / w_a
+  static constexpr int TOT = SL + N;
 };
 struct LTab {
-  double v[25 + 20 + 30 + 30];
+  double v[10 + 30 + 30 + 25 + 10];
 };
 template <int K>
 LTab make_ltab() {
@@ -73,15 +74,15 @@ LTab make_ltab() {
   constexpr int N = K + 1;
   LTab t{};
   for (int a = 0; a < N; ++a) {
-    for (int l = 0; l < N; ++l) t.v[T::D + a * N + l] = O::D_gl[a][l];
-    t.v[T::GL + a] = O::gLp_gl[a];
-    t.v[T::GR + a] = O::gRp_gl[a];
     t.v[T::EL + a] = O::eL_gl[a];
     t.v[T::ER + a] = O::eR_gl[a];
     for (int r = 0; r <= N; ++r) {
       t.v[T::SI + r * N + a] = O::sd_I[r][a];
       t.v[T::SD + a * (N + 1) + r] = O::sd_D[a][r];
     }
+    for (int l = 0; l < N; ++l) t.v[T::DV + a * N + l] = O::dg_vol[a][l];
+    t.v[T::SR + a] = O::dg_sR[a];
+    t.v[T::SL + a] = O::dg_sL[a];
   }
   return t;
 }
@@ -102,8 +103,7 @@ struct L {
   static constexpr int OR_ = 0;
   static constexpr int OFW = OR_ + NSTG * STGA;            // W-face fluxes [TX+1][N][4]
   static constexpr int OFN = OFW + (TX + 1) * N * 4;       // N-face fluxes, double-buffered [2][TX][N][4]
-  static constexpr int OJ = OFN + 2 * TX * N * 4;          // DG: y jumps [TX][2][N][4]
-  static constexpr int OG = OJ + (M == LM_DG ? TX * 2 * N * 4 : 0);  // DG: g at points [TX][NP][4]
+  static constexpr int OG = OFN + 2 * TX * N * 4;          // DG: g at points [TX][NP][4]
   // per-element strides padded to 2 mod 4 doubles: the column reads of 8
   // elements of a warp then fall into 8 different 16-B bank groups
   static constexpr int GS = NP * 4 + 2, PYS = N * (N - 1) * 4 + 2;
@@ -117,15 +117,28 @@ struct L {
 };
 
 // cp.async of this thread's q^n line into its private smem slots, one row ahead
+// (even N and 16-B aligned lines: 16-B pieces, layout [c][x/2][thread] of double2;
+// else 8-B pieces, layout [c][x][thread])
 template <int N, int NT>
-__device__ __forceinline__ void q0_prefetch(double* sq0, const double* q0, long long cs, long long base, int tid) {
+__device__ __forceinline__ void q0_prefetch(double* sq0, const double* q0, long long cs, long long base, int tid,
+                                            bool vec) {
 #pragma unroll
-  for (int c = 0; c < 4; ++c)
+  for (int c = 0; c < 4; ++c) {
+    const double* s = q0 + c * cs + base;
+    if (N % 2 == 0 && vec) {
 #pragma unroll
-    for (int x = 0; x < N; ++x)
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(sq0 + (c * N + x) * NT + tid)),
-                   "l"(q0 + c * cs + base + x)
-                   : "memory");
+      for (int x = 0; x < N; x += 2)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sq0 + (c * N + x) * NT + 2 * tid)),
+                     "l"(s + x)
+                     : "memory");
+    } else {
+#pragma unroll
+      for (int x = 0; x < N; ++x)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(sq0 + (c * N + x) * NT + tid)),
+                     "l"(s + x)
+                     : "memory");
+    }
+  }
   asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
@@ -180,7 +193,6 @@ __global__ void __launch_bounds__(L<M, K>::NT, H2D_LMINB) gl_stage_kernel(const 
   double* ring = sm + H::OR_;
   double* sFW = sm + H::OFW;
   double* sFN = sm + H::OFN;
-  double* sJ = sm + H::OJ;
   double* sG = sm + H::OG;
   double* sPY = sm + H::OPY;
   double* sT = sm + H::OT;
@@ -193,11 +205,15 @@ __global__ void __launch_bounds__(L<M, K>::NT, H2D_LMINB) gl_stage_kernel(const 
     if (dtv == 0.0) return;
   }
   const int tid = threadIdx.x;
-  const int i0 = blockIdx.x * TX, jb = blockIdx.y * a.rows;
-  const int TXv = min(TX, a.nx - i0), RBv = min(a.rows, a.nrows - jb);
+  const int i0 = blockIdx.x * TX, jb = a.row_lo + blockIdx.y * a.rows;
+  const int TXv = min(TX, a.nx - i0), RBv = min(a.rows, a.row_hi - jb);
   const double gam = a.gamma, gm1 = a.gamma - 1.0;
   const int lx = tid / N, b = tid - lx * N;
   const bool own = lx < TXv;
+  // vector global access: every line start 32-B (P3) / 16-B (P1) aligned in out and q^n
+  const unsigned long long amask = N == 4 ? 31ull : 15ull;
+  const bool vec = ((((unsigned long long)a.out | (unsigned long long)a.q0 |
+                      (unsigned long long)(a.cs * 8)) & amask) == 0);
   const bool mirW = (i0 == 0 && a.bcx), mirE = (i0 + TXv == a.nx && a.bcx);
   const bool wrapW = (i0 == 0 && !a.bcx), wrapE = (i0 + TXv == a.nx && !a.bcx);
   const int iw = i0 > 0 ? i0 - 1 : a.nx - 1;
@@ -313,7 +329,7 @@ __global__ void __launch_bounds__(L<M, K>::NT, H2D_LMINB) gl_stage_kernel(const 
 
   for (int Lr = 0; Lr < NSTG && Lr < nload; ++Lr) issue_row(Lr);
   if (a.q0 && own)  // q^n of the first own row
-    q0_prefetch<N, NT>(sQ0, a.q0, a.cs, ((long long)jb * a.nx + i0 + lx) * NP + b * N, tid);
+    q0_prefetch<N, NT>(sQ0, a.q0, a.cs, ((long long)jb * a.nx + i0 + lx) * NP + b * N, tid, vec);
 
   double lam = 0.0;
   const double bdt = a.bcoef * dtv;
@@ -331,17 +347,27 @@ __global__ void __launch_bounds__(L<M, K>::NT, H2D_LMINB) gl_stage_kernel(const 
     const long long jr = jb - 1 + Lr;
 
     double q[4][N];
-    double fW[4], fWi[4], fEi[4], jW[4];  // DG: trace flux / interpolated edge fluxes / W jump
     double phi[N + 1][4];           // SD: x flux-point fluxes (interior; [0] = F^W)
     double fl[4][N];                // DG: x fluxes of the line
     if (Lr > 0 && own) {
 #pragma unroll
       for (int c = 0; c < 4; ++c)
 #pragma unroll
-        for (int x = 0; x < N; ++x) q[c][x] = own_at(vc, c, lx + 1, b * N + x);
+        for (int x = 0; x < N; ++x) {
+          if constexpr (H::SWZ) {  // 16-B chunks: points (4b + 2h, 4b + 2h + 1)
+            if ((x & 1) == 0) {
+              const double2 u = *reinterpret_cast<const double2*>(
+                  vc.st + (c * H::RSW + lx + 1) * 16 + (((2 * b + (x >> 1)) ^ ((lx + 1) & 7)) << 1));
+              q[c][x] = u.x;
+              q[c][x + 1] = u.y;
+            }
+          } else {
+            q[c][x] = own_at(vc, c, lx + 1, b * N + x);
+          }
+        }
       const double* wl = (M == LM_DG) ? EL : SI0;
       const double* wr = (M == LM_DG) ? ER : SIN;
-      double qw[4], qe[4], sw, se, fE[4];
+      double qw[4], qe[4], sw, se, fW[4], fE[4];
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         double s0 = 0.0, s1 = 0.0;
@@ -352,7 +378,7 @@ __global__ void __launch_bounds__(L<M, K>::NT, H2D_LMINB) gl_stage_kernel(const 
       }
       node_eval<0>(qw, gm1, gam, fW, sw);
       node_eval<0>(qe, gm1, gam, fE, se);
-      if (M == LM_DG) {
+      if (M == LM_DG) {  // f (registers) and g (smem, for the columns) at every point of the line
 #pragma unroll
         for (int x = 0; x < N; ++x) {
           double v[4] = {q[0][x], q[1][x], q[2][x], q[3][x]}, f[4], g[4];
@@ -362,14 +388,6 @@ __global__ void __launch_bounds__(L<M, K>::NT, H2D_LMINB) gl_stage_kernel(const 
 #pragma unroll
           for (int c = 0; c < 4; ++c) fl[c][x] = f[c];
           st4(sG + lx * H::GS + (b * N + x) * 4, g);
-        }
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-          for (int l = 0; l < N; ++l) { s0 += EL[l] * fl[c][l]; s1 += ER[l] * fl[c][l]; }
-          fWi[c] = s0;
-          fEi[c] = s1;
         }
       } else {  // SD: interior x flux points
 #pragma unroll
@@ -397,10 +415,7 @@ __global__ void __launch_bounds__(L<M, K>::NT, H2D_LMINB) gl_stage_kernel(const 
       }
       st4(sFW + (lx * N + b) * 4, F);
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        phi[0][c] = F[c];
-        jW[c] = F[c] - fWi[c];
-      }
+      for (int c = 0; c < 4; ++c) phi[0][c] = F[c];
       if (lx == TXv - 1) {
         double G[4];
         if (mirE) {
@@ -443,69 +458,49 @@ __global__ void __launch_bounds__(L<M, K>::NT, H2D_LMINB) gl_stage_kernel(const 
     }
     __syncthreads();
 
-    double jE[4];
-    if (M == LM_DG) {  // jumps against the interpolated edge fluxes
-      if (Lr > 0 && own) {
-        double F[4];
-        ld4(sFW + ((lx + 1) * N + b) * 4, F);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) jE[c] = F[c] - fEi[c];
-        double gS[4] = {0, 0, 0, 0}, gN[4] = {0, 0, 0, 0};
-#pragma unroll
-        for (int l = 0; l < N; ++l) {
-          double g[4];
-          ld4(sG + lx * H::GS + (l * N + b) * 4, g);
-#pragma unroll
-          for (int c = 0; c < 4; ++c) { gS[c] += EL[l] * g[c]; gN[c] += ER[l] * g[c]; }
-        }
-        double FS[4], FN[4], j[4];
-        ld4(FSc + (lx * N + b) * 4, FS);
-        ld4(FNc + (lx * N + b) * 4, FN);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) j[c] = FS[c] - gS[c];
-        st4(sJ + ((lx * 2 + 0) * N + b) * 4, j);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) j[c] = FN[c] - gN[c];
-        st4(sJ + ((lx * 2 + 1) * N + b) * 4, j);
-      }
-      __syncthreads();
-    }
-
     if (Lr > 0 && own) {
       const long long base = (jr * a.nx + i0 + lx) * NP + b * N;
       if (a.q0) asm volatile("cp.async.wait_group 0;" ::: "memory");
+#define Q0V(c, x) (N % 2 == 0 && vec ? sQ0[((c) * N + ((x) & ~1)) * NT + 2 * tid + ((x) & 1)] \
+                                     : sQ0[((c) * N + (x)) * NT + tid])
+      double FW[4], FE[4];
+      ld4(sFW + (lx * N + b) * 4, FW);
+      ld4(sFW + ((lx + 1) * N + b) * 4, FE);
       if (M == LM_SD) {
-        double F[4];
-        ld4(sFW + ((lx + 1) * N + b) * 4, F);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) phi[N][c] = F[c];
+        for (int c = 0; c < 4; ++c) phi[N][c] = FE[c];
       }
+      double ov[4][N];
 #pragma unroll
       for (int x = 0; x < N; ++x) {
         double v[4] = {q[0][x], q[1][x], q[2][x], q[3][x]};
-        double R[4];
+        double R[4], FS[4], FN[4];
+        ld4(FSc + (lx * N + x) * 4, FS);
+        ld4(FNc + (lx * N + x) * 4, FN);
         if (M == LM_DG) {
-          double jS[4], jN[4];
-          ld4(sJ + ((lx * 2 + 0) * N + x) * 4, jS);
-          ld4(sJ + ((lx * 2 + 1) * N + x) * 4, jN);
-          const double gLa = tab.v[T::GL + x], gRa = tab.v[T::GR + x];
-          const double gLb = sT[T::GL + b], gRb = sT[T::GR + b];
+          // weak form, Eq. (19) / SURVEY C6 divided by w_a:
+          // (2/dx) [sum_l (w_l/w_a) l'_a(xi_l) f_l - (l_a(1) F^E - l_a(-1) F^W) / w_a] + (y likewise)
+          double gy[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+          for (int l = 0; l < N; ++l) {  // column x of the element: g of its points (16-B smem reads)
+            double g[4];
+            ld4(sG + lx * H::GS + (l * N + x) * 4, g);
+            const double dv = sT[T::DV + b * N + l];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) gy[c] += dv * g[c];
+          }
+          const double sRa = tab.v[T::SR + x], sLa = tab.v[T::SL + x];
+          const double sRb = sT[T::SR + b], sLb = sT[T::SL + b];
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
-            double fx = 0.0, gy = 0.0;
+            double fx = 0.0;
 #pragma unroll
-            for (int l = 0; l < N; ++l) {
-              fx += tab.v[T::D + x * N + l] * fl[c][l];
-              gy += sT[T::D + b * N + l] * sG[lx * H::GS + (l * N + x) * 4 + c];
-            }
-            fx += gLa * jW[c] + gRa * jE[c];
-            gy += gLb * jS[c] + gRb * jN[c];
-            R[c] = -a.rdx2 * fx - a.rdy2 * gy;
+            for (int l = 0; l < N; ++l) fx += tab.v[T::DV + x * N + l] * fl[c][l];
+            fx += sLa * FW[c] - sRa * FE[c];
+            const double g2 = gy[c] + sLb * FS[c] - sRb * FN[c];
+            R[c] = a.rdx2 * fx + a.rdy2 * g2;
           }
         } else {  // SD
-          double FS[4], FN[4];
-          ld4(FSc + (lx * N + x) * 4, FS);
-          ld4(FNc + (lx * N + x) * 4, FN);
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
             double fx = 0.0, gy = 0.0;
@@ -522,9 +517,9 @@ __global__ void __launch_bounds__(L<M, K>::NT, H2D_LMINB) gl_stage_kernel(const 
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           double val = a.a1 * v[c] + bdt * R[c];
-          if (a.q0) val += a.a0 * sQ0[(c * N + x) * NT + tid];
+          if (a.q0) val += a.a0 * Q0V(c, x);
           o[c] = val;
-          a.out[c * a.cs + base + x] = val;
+          ov[c][x] = val;
         }
         if (a.lam || a.bad) {
           const Prim w = prims(o, gm1);
@@ -532,8 +527,25 @@ __global__ void __launch_bounds__(L<M, K>::NT, H2D_LMINB) gl_stage_kernel(const 
           if (a.bad && !admissible(o[0], w.p)) atomicMin(a.bad, (unsigned long long)(base + x));
         }
       }
+#undef Q0V
+      // a thread's line of one component is N contiguous doubles: one 32-B (P3) or
+      // 16-B (P1) store per component when aligned
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        double* o = a.out + c * a.cs + base;
+        if (N == 4 && vec) {
+          asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(o), "d"(ov[c][0]), "d"(ov[c][1 % N]),
+                       "d"(ov[c][2 % N]), "d"(ov[c][3 % N])
+                       : "memory");
+        } else if (N == 2 && vec) {
+          asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(o), "d"(ov[c][0]), "d"(ov[c][1 % N]) : "memory");
+        } else {
+#pragma unroll
+          for (int x = 0; x < N; ++x) o[x] = ov[c][x];
+        }
+      }
       if (a.q0 && Lr < RBv)  // q^n of the next row into the consumed private slots
-        q0_prefetch<N, NT>(sQ0, a.q0, a.cs, base + (long long)a.nx * NP, tid);
+        q0_prefetch<N, NT>(sQ0, a.q0, a.cs, base + (long long)a.nx * NP, tid, vec);
     }
     __syncthreads();
     if (Lr + NSTG < nload) {
@@ -563,8 +575,10 @@ static int launch_l(const StageArgs& a, cudaStream_t s) {
   }
   StageArgs b = a;
   const int strips = (a.nx + H::TX - 1) / H::TX;
-  b.rows = march_rows(a.nrows, strips, H::RB);
-  dim3 grid(strips, (a.nrows + b.rows - 1) / b.rows);
+  const int nr = row_range(b);
+  if (nr <= 0) return 0;
+  b.rows = march_rows(nr, strips, H::RB);
+  dim3 grid(strips, (nr + b.rows - 1) / b.rows);
   gl_stage_kernel<M, K><<<grid, H::NT, H::SMEM, s>>>(b, tab, maps);
   return (int)cudaPeekAtLastError();
 }
