@@ -331,93 +331,100 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
     const long long jr = jb - 1 + L;                 // local strip row of this step
 
     double q[4][N], fW[4], fE[4], jW[4];
+    double fxl[4][N];  // NDG: x fluxes of the line
     Prim pW, pE;
-    if (L > 0 && own) {
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-#pragma unroll
-        for (int x = 0; x < N; ++x) {
-          if constexpr (H::SWZ) {  // 16-B chunks: points (4b + 2h, 4b + 2h + 1)
-            if ((x & 1) == 0) {
-              const double2 u = *reinterpret_cast<const double2*>(
-                  vc.st + (c * H::RSW + lx + 1) * 16 + (((2 * b + (x >> 1)) ^ ((lx + 1) & 7)) << 1));
-              q[c][x] = u.x;
-              q[c][x + 1] = u.y;
-            }
-          } else {
-            q[c][x] = own_at(vc, c, lx + 1, b * N + x);
-          }
-        }
-      // W face (computed by the element on its right) and the strip's last E face
-      double qw[4] = {q[0][0], q[1][0], q[2][0], q[3][0]}, sw;
-      double qe[4] = {q[0][N - 1], q[1][N - 1], q[2][N - 1], q[3][N - 1]}, se;
-      pW = prims(qw, gm1);  // kept for the chain rule at points 0 and n-1
-      pE = prims(qe, gm1);
-      flux<0>(qw, pW, fW);
-      flux<0>(qe, pE, fE);
-      sw = fabs(pW.u) + fsqrt(gam * pW.p * pW.ri);
-      se = fabs(pE.u) + fsqrt(gam * pE.p * pE.ri);
-      double F[4];
-      if (lx == 0 && mirW) {
-        rus(qw, fW, sw, qw, fW, sw, F);
-      } else {
-        double ql[4], fl[4], sl;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) ql[c] = any_at(vc, c, lx, b * N + N - 1);
-        node_eval<0>(ql, gm1, gam, fl, sl);
-        rus(ql, fl, sl, qw, fW, sw, F);
-      }
-      st4(sFW + (lx * N + b) * 4, F);
-#pragma unroll
-      for (int c = 0; c < 4; ++c) jW[c] = F[c] - fW[c];
-      if (lx == TXv - 1) {
-        if (mirE) {
-          rus(qe, fE, se, qe, fE, se, F);
-        } else {
-          double qr[4], fr[4], sr;
-#pragma unroll
-          for (int c = 0; c < 4; ++c) qr[c] = any_at(vc, c, TXv + 1, b * N);
-          node_eval<0>(qr, gm1, gam, fr, sr);
-          rus(qe, fE, se, qr, fr, sr, F);
-        }
-        st4(sFW + (TXv * N + b) * 4, F);
-      }
-      if (M == GM_NDG) {  // eta operands: g at the points of the line
-#pragma unroll
-        for (int x = 0; x < N; ++x) {
-          double v[4] = {q[0][x], q[1][x], q[2][x], q[3][x]}, g[4];
-          flux<1>(v, prims(v, gm1), g);
-          st4(sG + lx * H::GS + (b * N + x) * 4, g);
-        }
-      }
-    }
-    // N faces of row L, column x = b of each element (spread over the lines, no
-    // divergence): jumps for row L (jN) and for row L+1 (jS)
+    // Face work of the row, straight-line so that the independent node
+    // evaluations (reciprocal / square-root chains) interleave: the W face of
+    // each line (computed by the element on its right), the N face of column b
+    // of each element (spread over the lines: no divergence; its jump for the
+    // element above is carried to the next step); transmissive ends by selects.
     if (own) {
-      {
-        const int x = b;
-        double qd[4], gd[4], sd, qu[4], gu[4], su, Gf[4], j[4];
-        if (vc.have) {
+      double qd[4], qu[4];  // column b: own top point, next row's bottom point
 #pragma unroll
-          for (int c = 0; c < 4; ++c) qd[c] = own_at(vc, c, lx + 1, (N - 1) * N + x);
-          node_eval<1>(qd, gm1, gam, gd, sd);
-        }
-        if (vn.have) {
+      for (int c = 0; c < 4; ++c) {
+        const double d = own_at(vc, c, lx + 1, (N - 1) * N + b), u = own_at(vn, c, lx + 1, b);
+        qd[c] = vc.have ? d : u;
+        qu[c] = vn.have ? u : d;
+      }
+      if (L > 0) {
 #pragma unroll
-          for (int c = 0; c < 4; ++c) qu[c] = own_at(vn, c, lx + 1, x);
-          node_eval<1>(qu, gm1, gam, gu, su);
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int x = 0; x < N; ++x) {
+            if constexpr (H::SWZ) {  // 16-B chunks: points (4b + 2h, 4b + 2h + 1)
+              if ((x & 1) == 0) {
+                const double2 u = *reinterpret_cast<const double2*>(
+                    vc.st + (c * H::RSW + lx + 1) * 16 + (((2 * b + (x >> 1)) ^ ((lx + 1) & 7)) << 1));
+                q[c][x] = u.x;
+                q[c][x + 1] = u.y;
+              }
+            } else {
+              q[c][x] = own_at(vc, c, lx + 1, b * N + x);
+            }
+          }
+        double qw[4] = {q[0][0], q[1][0], q[2][0], q[3][0]}, sw;
+        double qe[4] = {q[0][N - 1], q[1][N - 1], q[2][N - 1], q[3][N - 1]}, se;
+        double ql[4];  // E point of the W neighbour's line (the domain's W end mirrors)
+        const bool mw = (lx == 0 && mirW);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const double v = any_at(vc, c, lx, b * N + N - 1);
+          ql[c] = mw ? qw[c] : v;
         }
-        if (!vc.have) { for (int c = 0; c < 4; ++c) { qd[c] = qu[c]; gd[c] = gu[c]; } sd = su; }
-        if (!vn.have) { for (int c = 0; c < 4; ++c) { qu[c] = qd[c]; gu[c] = gd[c]; } su = sd; }
+        pW = prims(qw, gm1);  // kept for the chain rule at points 0 and n-1
+        pE = prims(qe, gm1);
+        flux<0>(qw, pW, fW);
+        flux<0>(qe, pE, fE);
+        sw = fabs(pW.u) + fsqrt(gam * pW.p * pW.ri);
+        se = fabs(pE.u) + fsqrt(gam * pE.p * pE.ri);
+        double fl[4], sl, gd[4], sd, gu[4], su;
+        node_eval<0>(ql, gm1, gam, fl, sl);
+        node_eval<1>(qd, gm1, gam, gd, sd);
+        node_eval<1>(qu, gm1, gam, gu, su);
+        double F[4], Gf[4], j[4];
+        rus(ql, fl, sl, qw, fW, sw, F);
         rus(qd, gd, sd, qu, gu, su, Gf);
-        if (L > 0) {
+        st4(sFW + (lx * N + b) * 4, F);
 #pragma unroll
-          for (int c = 0; c < 4; ++c) j[c] = Gf[c] - gd[c];
-          st4(sJN + (lx * N + x) * 4, j);
-        }
+        for (int c = 0; c < 4; ++c) jW[c] = F[c] - fW[c];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) j[c] = Gf[c] - gd[c];
+        st4(sJN + (lx * N + b) * 4, j);
 #pragma unroll
         for (int c = 0; c < 4; ++c) j[c] = Gf[c] - gu[c];
-        st4(jSn + (lx * N + x) * 4, j);
+        st4(jSn + (lx * N + b) * 4, j);
+        if (lx == TXv - 1) {  // the strip's last E face
+          if (mirE) {
+            rus(qe, fE, se, qe, fE, se, F);
+          } else {
+            double qr[4], fr[4], sr;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) qr[c] = any_at(vc, c, TXv + 1, b * N);
+            node_eval<0>(qr, gm1, gam, fr, sr);
+            rus(qe, fE, se, qr, fr, sr, F);
+          }
+          st4(sFW + (TXv * N + b) * 4, F);
+        }
+        if (M == GM_NDG) {  // eta operands: g at the points of the line (smem); f kept in registers
+#pragma unroll
+          for (int x = 0; x < N; ++x) {
+            double v[4] = {q[0][x], q[1][x], q[2][x], q[3][x]}, f[4], g[4];
+            const Prim w = (x == 0) ? pW : (x == N - 1) ? pE : prims(v, gm1);
+            flux<0>(v, w, f);
+            flux<1>(v, w, g);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) fxl[c][x] = f[c];
+            st4(sG + lx * H::GS + (b * N + x) * 4, g);
+          }
+        }
+      } else {  // prologue row (below the march): only its N face, as the first row's S face
+        double gd[4], sd, gu[4], su, Gf[4], j[4];
+        node_eval<1>(qd, gm1, gam, gd, sd);
+        node_eval<1>(qu, gm1, gam, gu, su);
+        rus(qd, gd, sd, qu, gu, su, Gf);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) j[c] = Gf[c] - gu[c];
+        st4(jSn + (lx * N + b) * 4, j);
       }
     }
     __syncthreads();
@@ -454,16 +461,7 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
             }
         }
       }
-      double fxl[4][N], ov[4][N];
-      if (M == GM_NDG) {
-#pragma unroll
-        for (int x = 0; x < N; ++x) {
-          double v[4] = {q[0][x], q[1][x], q[2][x], q[3][x]}, f[4];
-          flux<0>(v, prims(v, gm1), f);
-#pragma unroll
-          for (int c = 0; c < 4; ++c) fxl[c][x] = f[c];
-        }
-      }
+      double ov[4][N];
 #pragma unroll
       for (int x = 0; x < N; ++x) {
         double v[4] = {q[0][x], q[1][x], q[2][x], q[3][x]};
