@@ -187,60 +187,57 @@ __global__ void __launch_bounds__(FTX, H2D_FV_MINB) fv_stage_kernel(const StageA
 #pragma unroll
       for (int c = 0; c < 4; ++c) q0v[c] = a.q0[c * a.cs + gidx];
     }
-    // x faces: the W face of each own cell, plus the strip's last E face, from
-    // the face states reconstructed one row earlier
+    // x faces (the W face of each own cell, from the face states reconstructed one
+    // row earlier) and the N face of the column (carried hi state of row r, lo
+    // state of row r+1 reconstructed now from rows r..r+2; its hi state is
+    // carried on): straight-line, so that both Rusanov evaluations interleave
+    double GN[4];
     if (own) {
       const int b = r & 1;
-      double qL[4], qR[4], F[4], fL[4], fR[4];
+      const int wn = (r + 1 < RBv) ? 2 : ((jb + RBv == a.nrows) ? 1 : 0);
+      double qL[4], qR[4], lo[4], hi[4], F[4], fL[4], fR[4], gL[4], gR[4];
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         qL[c] = sXH[b][c][tid];
         qR[c] = sXL[b][c][tid + 1];
+        cell_faces<ORDER>(ring[sc][c][tid + 2], ring[slot_of(r + 1)][c][tid + 2], ring[slot_of(r + 2)][c][tid + 2],
+                          lo[c], hi[c], dec, wn);
+      }
+      rusanov<0>(qL, qR, gm1, gam, F, fL, fR);
+      rusanov<1>(yHi, lo, gm1, gam, GN, gL, gR);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        sF[tid][c] = F[c];
+        yHi[c] = hi[c];
+      }
+    }
+    if (own && tid == TXv - 1) {  // the strip's last E face
+      const int b = r & 1;
+      double qL[4], qR[4], F[4], fL[4], fR[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        qL[c] = sXH[b][c][tid + 1];
+        qR[c] = sXL[b][c][tid + 2];
       }
       rusanov<0>(qL, qR, gm1, gam, F, fL, fR);
 #pragma unroll
-      for (int c = 0; c < 4; ++c) sF[tid][c] = F[c];
-      if (tid == TXv - 1) {
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          qL[c] = sXH[b][c][tid + 1];
-          qR[c] = sXL[b][c][tid + 2];
-        }
-        rusanov<0>(qL, qR, gm1, gam, F, fL, fR);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) sF[tid + 1][c] = F[c];
-      }
+      for (int c = 0; c < 4; ++c) sF[tid + 1][c] = F[c];
     }
     if (r + 1 < RBv) recon_x(slot_of(r + 1), (r + 1) & 1);
-    // N face of the column: carried hi state of row r, lo state of row r+1
-    // (reconstructed now from rows r..r+2; its hi state is carried on)
-    double GN[4];
-    if (own) {
-      const int wn = (r + 1 < RBv) ? 2 : ((jb + RBv == a.nrows) ? 1 : 0);
-      double lo[4], hi[4], fL[4], fR[4];
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-        cell_faces<ORDER>(ring[sc][c][tid + 2], ring[slot_of(r + 1)][c][tid + 2], ring[slot_of(r + 2)][c][tid + 2],
-                          lo[c], hi[c], dec, wn);
-      rusanov<1>(yHi, lo, gm1, gam, GN, fL, fR);
-#pragma unroll
-      for (int c = 0; c < 4; ++c) yHi[c] = hi[c];
-    }
     __syncthreads();
     if (own) {
       double o[4];
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         const double R = -(sF[tid + 1][c] - sF[tid][c]) * a.rdx2 - (GN[c] - GS[c]) * a.rdy2;
-        double v = a.a1 * ring[sc][c][tid + 2] + bdt * R;
-        if (a.q0) v += a.a0 * q0v[c];
+        const double v = fma(a.a0, q0v[c], fma(a.a1, ring[sc][c][tid + 2], bdt * R));
         o[c] = v;
         a.out[c * a.cs + gidx] = v;
         GS[c] = GN[c];
       }
       if (a.lam || a.bad) {
         const Prim w = prims(o, gm1);
-        if (a.lam) lam = fmax(lam, fmax(fabs(w.u), fabs(w.v)) + fsqrt(gam * w.p * w.ri));
+        lam = fmax(lam, fmax(fabs(w.u), fabs(w.v)) + fsqrt(gam * w.p * w.ri));
         if (a.bad && !admissible(o[0], w.p)) atomicMin(a.bad, (unsigned long long)gidx);
       }
     }

@@ -40,9 +40,13 @@ namespace {
 #ifndef H2D_LMINB
 #define H2D_LMINB 1
 #endif
+#ifndef H2D_LMINB1
+#define H2D_LMINB1 3  // P1 (128 threads): <= 168 registers, 3 CTAs/SM (smem allows 3-4)
+#endif
 enum { LM_DG = 2, LM_SD = 4 };
 template <int M, int K> struct LTile {
   static constexpr int TX = K == 1 ? 64 : (M == LM_DG ? H2D_DG_TX : H2D_SD_TX), RB = 64;
+  static constexpr int MINB = K == 1 ? H2D_LMINB1 : H2D_LMINB;
 };
 
 constexpr int NSTG = 3;
@@ -182,7 +186,7 @@ __device__ __forceinline__ const void* piece_src(const double* src) {
 }  // namespace
 
 template <int M, int K>
-__global__ void __launch_bounds__(L<M, K>::NT, H2D_LMINB) gl_stage_kernel(const StageArgs a, const LTab tab,
+__global__ void __launch_bounds__(L<M, K>::NT, LTile<M, K>::MINB) gl_stage_kernel(const StageArgs a, const LTab tab,
                                                                const __grid_constant__ LMaps maps) {
   using H = L<M, K>;
   using T = LOps<K>;
@@ -349,112 +353,119 @@ __global__ void __launch_bounds__(L<M, K>::NT, H2D_LMINB) gl_stage_kernel(const 
     double q[4][N];
     double phi[N + 1][4];           // SD: x flux-point fluxes (interior; [0] = F^W)
     double fl[4][N];                // DG: x fluxes of the line
-    if (Lr > 0 && own) {
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-#pragma unroll
-        for (int x = 0; x < N; ++x) {
-          if constexpr (H::SWZ) {  // 16-B chunks: points (4b + 2h, 4b + 2h + 1)
-            if ((x & 1) == 0) {
-              const double2 u = *reinterpret_cast<const double2*>(
-                  vc.st + (c * H::RSW + lx + 1) * 16 + (((2 * b + (x >> 1)) ^ ((lx + 1) & 7)) << 1));
-              q[c][x] = u.x;
-              q[c][x + 1] = u.y;
-            }
-          } else {
-            q[c][x] = own_at(vc, c, lx + 1, b * N + x);
-          }
-        }
-      const double* wl = (M == LM_DG) ? EL : SI0;
-      const double* wr = (M == LM_DG) ? ER : SIN;
-      double qw[4], qe[4], sw, se, fW[4], fE[4];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-        for (int l = 0; l < N; ++l) { s0 += wl[l] * q[c][l]; s1 += wr[l] * q[c][l]; }
-        qw[c] = s0;
-        qe[c] = s1;
-      }
-      node_eval<0>(qw, gm1, gam, fW, sw);
-      node_eval<0>(qe, gm1, gam, fE, se);
-      if (M == LM_DG) {  // f (registers) and g (smem, for the columns) at every point of the line
-#pragma unroll
-        for (int x = 0; x < N; ++x) {
-          double v[4] = {q[0][x], q[1][x], q[2][x], q[3][x]}, f[4], g[4];
-          const Prim w = prims(v, gm1);
-          flux<0>(v, w, f);
-          flux<1>(v, w, g);
-#pragma unroll
-          for (int c = 0; c < 4; ++c) fl[c][x] = f[c];
-          st4(sG + lx * H::GS + (b * N + x) * 4, g);
-        }
-      } else {  // SD: interior x flux points
-#pragma unroll
-        for (int r = 1; r < N; ++r) {
-          double v[4];
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            double s = 0.0;
-#pragma unroll
-            for (int l = 0; l < N; ++l) s += tab.v[T::SI + r * N + l] * q[c][l];
-            v[c] = s;
-          }
-          flux<0>(v, prims(v, gm1), phi[r]);
-        }
-      }
-      // W face (left neighbour's E trace interpolated here), strip's last E face
-      double F[4];
-      if (lx == 0 && mirW) {
-        rus(qw, fW, sw, qw, fW, sw, F);
-      } else {
-        double ql[4], flf[4], sl;
-        interp(vc, lx, 0, b, wr, ql, true);
-        node_eval<0>(ql, gm1, gam, flf, sl);
-        rus(ql, flf, sl, qw, fW, sw, F);
-      }
-      st4(sFW + (lx * N + b) * 4, F);
-#pragma unroll
-      for (int c = 0; c < 4; ++c) phi[0][c] = F[c];
-      if (lx == TXv - 1) {
-        double G[4];
-        if (mirE) {
-          rus(qe, fE, se, qe, fE, se, G);
-        } else {
-          double qr[4], fr[4], sr;
-          interp(vc, TXv + 1, 0, b, wl, qr, true);
-          node_eval<0>(qr, gm1, gam, fr, sr);
-          rus(qe, fE, se, qr, fr, sr, G);
-        }
-        st4(sFW + (TXv * N + b) * 4, G);
-      }
-    }
-    // column b: SD interior y flux points; N face (own N trace vs next row's S trace)
+    // Face work of the row, straight-line so that the independent node
+    // evaluations interleave: the W face of each line (its W neighbour's E trace
+    // interpolated here), the N face of column b of each element (own N trace vs
+    // the next row's S trace; carried as that row's S face); transmissive ends
+    // by selects.
     if (own) {
       const double* wl = (M == LM_DG) ? EL : SI0;
       const double* wr = (M == LM_DG) ? ER : SIN;
-      if (M == LM_SD && Lr > 0) {
+      double qd[4], qu[4];
+      {
+        double d[4], u[4];
+        interp(vc, lx + 1, 1, b, wr, d, false);
+        interp(vn, lx + 1, 1, b, wl, u, false);
 #pragma unroll
-        for (int r = 1; r < N; ++r) {
-          double v[4], g[4];
-          interp(vc, lx + 1, 1, b, tab.v + T::SI + r * N, v, false);
-          flux<1>(v, prims(v, gm1), g);
-          st4(sPY + lx * H::PYS + (b * (N - 1) + (r - 1)) * 4, g);
+        for (int c = 0; c < 4; ++c) {
+          qd[c] = vc.have ? d[c] : u[c];
+          qu[c] = vn.have ? u[c] : d[c];
         }
       }
-      double qd[4], gd[4], sd, qu[4], gu[4], su, G[4];
-      if (vc.have) {
-        interp(vc, lx + 1, 1, b, wr, qd, false);
+      if (Lr > 0) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int x = 0; x < N; ++x) {
+            if constexpr (H::SWZ) {  // 16-B chunks: points (4b + 2h, 4b + 2h + 1)
+              if ((x & 1) == 0) {
+                const double2 u = *reinterpret_cast<const double2*>(
+                    vc.st + (c * H::RSW + lx + 1) * 16 + (((2 * b + (x >> 1)) ^ ((lx + 1) & 7)) << 1));
+                q[c][x] = u.x;
+                q[c][x + 1] = u.y;
+              }
+            } else {
+              q[c][x] = own_at(vc, c, lx + 1, b * N + x);
+            }
+          }
+        double qw[4], qe[4], ql[4], sw, se, sl, fW[4], fE[4], flf[4], gd[4], sd, gu[4], su;
+        {
+          double v[4];
+          interp(vc, lx, 0, b, wr, v, true);  // E trace of the W neighbour's line
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+            for (int l = 0; l < N; ++l) { s0 += wl[l] * q[c][l]; s1 += wr[l] * q[c][l]; }
+            qw[c] = s0;
+            qe[c] = s1;
+          }
+          const bool mw = (lx == 0 && mirW);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) ql[c] = mw ? qw[c] : v[c];
+        }
+        node_eval<0>(qw, gm1, gam, fW, sw);
+        node_eval<0>(qe, gm1, gam, fE, se);
+        node_eval<0>(ql, gm1, gam, flf, sl);
         node_eval<1>(qd, gm1, gam, gd, sd);
-      }
-      if (vn.have) {
-        interp(vn, lx + 1, 1, b, wl, qu, false);
         node_eval<1>(qu, gm1, gam, gu, su);
+        if (M == LM_DG) {  // f (registers) and g (smem, for the columns) at every point of the line
+#pragma unroll
+          for (int x = 0; x < N; ++x) {
+            double v[4] = {q[0][x], q[1][x], q[2][x], q[3][x]}, f[4], g[4];
+            const Prim w = prims(v, gm1);
+            flux<0>(v, w, f);
+            flux<1>(v, w, g);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) fl[c][x] = f[c];
+            st4(sG + lx * H::GS + (b * N + x) * 4, g);
+          }
+        } else {  // SD: interior x flux points of the line, interior y flux points of column b
+#pragma unroll
+          for (int r = 1; r < N; ++r) {
+            double v[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              double s = 0.0;
+#pragma unroll
+              for (int l = 0; l < N; ++l) s += tab.v[T::SI + r * N + l] * q[c][l];
+              v[c] = s;
+            }
+            flux<0>(v, prims(v, gm1), phi[r]);
+          }
+#pragma unroll
+          for (int r = 1; r < N; ++r) {
+            double v[4], g[4];
+            interp(vc, lx + 1, 1, b, tab.v + T::SI + r * N, v, false);
+            flux<1>(v, prims(v, gm1), g);
+            st4(sPY + lx * H::PYS + (b * (N - 1) + (r - 1)) * 4, g);
+          }
+        }
+        double F[4], G[4];
+        rus(ql, flf, sl, qw, fW, sw, F);
+        rus(qd, gd, sd, qu, gu, su, G);
+        st4(sFW + (lx * N + b) * 4, F);
+        st4(FNc + (lx * N + b) * 4, G);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) phi[0][c] = F[c];
+        if (lx == TXv - 1) {  // the strip's last E face
+          if (mirE) {
+            rus(qe, fE, se, qe, fE, se, G);
+          } else {
+            double qr[4], fr[4], sr;
+            interp(vc, TXv + 1, 0, b, wl, qr, true);
+            node_eval<0>(qr, gm1, gam, fr, sr);
+            rus(qe, fE, se, qr, fr, sr, G);
+          }
+          st4(sFW + (TXv * N + b) * 4, G);
+        }
+      } else {  // prologue row (below the march): only its N face, as the first row's S face
+        double gd[4], sd, gu[4], su, G[4];
+        node_eval<1>(qd, gm1, gam, gd, sd);
+        node_eval<1>(qu, gm1, gam, gu, su);
+        rus(qd, gd, sd, qu, gu, su, G);
+        st4(FNc + (lx * N + b) * 4, G);
       }
-      if (!vc.have) { for (int c = 0; c < 4; ++c) { qd[c] = qu[c]; gd[c] = gu[c]; } sd = su; }
-      if (!vn.have) { for (int c = 0; c < 4; ++c) { qu[c] = qd[c]; gu[c] = gd[c]; } su = sd; }
-      rus(qd, gd, sd, qu, gu, su, G);
-      st4(FNc + (lx * N + b) * 4, G);
     }
     __syncthreads();
 
@@ -470,7 +481,11 @@ __global__ void __launch_bounds__(L<M, K>::NT, H2D_LMINB) gl_stage_kernel(const 
 #pragma unroll
         for (int c = 0; c < 4; ++c) phi[N][c] = FE[c];
       }
-      double ov[4][N];
+      double ov[4][N], q0v[4][N];  // q^n of the line (0 in stage 1: a0 = 0)
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int x = 0; x < N; ++x) q0v[c][x] = a.q0 ? Q0V(c, x) : 0.0;
 #pragma unroll
       for (int x = 0; x < N; ++x) {
         double v[4] = {q[0][x], q[1][x], q[2][x], q[3][x]};
@@ -513,19 +528,19 @@ __global__ void __launch_bounds__(L<M, K>::NT, H2D_LMINB) gl_stage_kernel(const 
             R[c] = -a.rdx2 * fx - a.rdy2 * gy;
           }
         }
-        double o[4];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          double val = a.a1 * v[c] + bdt * R[c];
-          if (a.q0) val += a.a0 * Q0V(c, x);
-          o[c] = val;
-          ov[c][x] = val;
-        }
-        if (a.lam || a.bad) {
+        for (int c = 0; c < 4; ++c) ov[c][x] = fma(a.a0, q0v[c][x], fma(a.a1, v[c], bdt * R[c]));
+      }
+      if (a.lam || a.bad) {  // dt wave speed and non-physical check (straight-line)
+        unsigned long long bidx = ~0ull;
+#pragma unroll
+        for (int x = 0; x < N; ++x) {
+          const double o[4] = {ov[0][x], ov[1][x], ov[2][x], ov[3][x]};
           const Prim w = prims(o, gm1);
-          if (a.lam) lam = fmax(lam, fmax(fabs(w.u), fabs(w.v)) + fsqrt(gam * w.p * w.ri));
-          if (a.bad && !admissible(o[0], w.p)) atomicMin(a.bad, (unsigned long long)(base + x));
+          lam = fmax(lam, fmax(fabs(w.u), fabs(w.v)) + fsqrt(gam * w.p * w.ri));
+          if (!admissible(o[0], w.p)) bidx = min(bidx, (unsigned long long)(base + x));
         }
+        if (a.bad && bidx != ~0ull) atomicMin(a.bad, bidx);
       }
 #undef Q0V
       // a thread's line of one component is N contiguous doubles: one 32-B (P3) or

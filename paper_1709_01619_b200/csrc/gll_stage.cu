@@ -36,8 +36,20 @@ namespace h2d {
 namespace {
 
 template <int K> struct GTile;
-template <> struct GTile<1> { static constexpr int TX = 64, RB = 64, MINB = 2; };  // 128 threads
-template <> struct GTile<2> { static constexpr int TX = 32, RB = 64, MINB = 2; };  //  96 threads
+#ifndef H2D_MINB1
+#define H2D_MINB1 2
+#endif
+#ifndef H2D_MINB2
+#define H2D_MINB2 2
+#endif
+#ifndef H2D_TX4
+#define H2D_TX4 32
+#endif
+#ifndef H2D_MINB4
+#define H2D_MINB4 1
+#endif
+template <> struct GTile<1> { static constexpr int TX = 64, RB = 64, MINB = H2D_MINB1; };  // 128 threads
+template <> struct GTile<2> { static constexpr int TX = 32, RB = 64, MINB = H2D_MINB2; };  //  96 threads
 #ifndef H2D_MINB3
 #define H2D_MINB3 4
 #endif
@@ -45,7 +57,7 @@ template <> struct GTile<2> { static constexpr int TX = 32, RB = 64, MINB = 2; }
 #define H2D_TX3 16  // 64 threads: 4 CTAs/SM interleave their barrier phases (A/B: +2.5 % over 32)
 #endif
 template <> struct GTile<3> { static constexpr int TX = H2D_TX3, RB = 64, MINB = H2D_MINB3; };  // 128 threads
-template <> struct GTile<4> { static constexpr int TX = 32, RB = 64, MINB = 1; };  // 160 threads
+template <> struct GTile<4> { static constexpr int TX = H2D_TX4, RB = 64, MINB = H2D_MINB4; };  // 5 TX threads
 
 enum { GM_CPR = 1, GM_NDG = 3 };
 constexpr int NSTG = 3;  // ring depth (rows): current, N neighbour, one in flight
@@ -461,7 +473,11 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
             }
         }
       }
-      double ov[4][N];
+      double ov[4][N], q0v[4][N];  // q^n of the line (0 in stage 1: a0 = 0)
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int x = 0; x < N; ++x) q0v[c][x] = a.q0 ? Q0V(c, x) : 0.0;
 #pragma unroll
       for (int x = 0; x < N; ++x) {
         double v[4] = {q[0][x], q[1][x], q[2][x], q[3][x]};
@@ -508,22 +524,24 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
         ld4(jSc + (lx * N + x) * 4, jS);
         ld4(sJN + (lx * N + x) * 4, jN);
         const double gLa = tab.v[N * N + x], gRa = tab.v[N * N + N + x];
-        double o[4];
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           const double fx = Fx[c] + gLa * jW[c] + gRa * jE[c];
           const double gy = Gy[c] + gLb * jS[c] + gRb * jN[c];
           const double R = -a.rdx2 * fx - a.rdy2 * gy;
-          double val = a.a1 * v[c] + bdt * R;
-          if (a.q0) val += a.a0 * Q0V(c, x);
-          o[c] = val;
-          ov[c][x] = val;
+          ov[c][x] = fma(a.a0, q0v[c][x], fma(a.a1, v[c], bdt * R));
         }
-        if (a.lam || a.bad) {  // dt wave speed and non-physical check share one reciprocal
+      }
+      if (a.lam || a.bad) {  // dt wave speed and non-physical check share one reciprocal (straight-line)
+        unsigned long long bidx = ~0ull;
+#pragma unroll
+        for (int x = 0; x < N; ++x) {
+          const double o[4] = {ov[0][x], ov[1][x], ov[2][x], ov[3][x]};
           const Prim w = prims(o, gm1);
-          if (a.lam) lam = fmax(lam, fmax(fabs(w.u), fabs(w.v)) + fsqrt(gam * w.p * w.ri));
-          if (a.bad && !admissible(o[0], w.p)) atomicMin(a.bad, (unsigned long long)(base + x));
+          lam = fmax(lam, fmax(fabs(w.u), fabs(w.v)) + fsqrt(gam * w.p * w.ri));
+          if (!admissible(o[0], w.p)) bidx = min(bidx, (unsigned long long)(base + x));
         }
+        if (a.bad && bidx != ~0ull) atomicMin(a.bad, bidx);
       }
       // a thread's line of one component is N contiguous doubles: one 32-B (P3) or
       // 16-B (P1) store per component when aligned

@@ -12,6 +12,10 @@
       after every stage (HO) / MUSCL (FV), at the paper's DoF levels (Table 4:
       P1 160k / 640k, P2 360k / 1440k) with Table-4 CFLs: total device seconds,
       steps, seconds per step.
+  python tools/sweep.py cfl | cfl-shock
+      the paper's max-CFL protocol driven over the GPU path at the
+      DoF levels of Table 1 (vortex; plus P3/P4, which the paper does not list)
+      and Table 4 (shock tube, residual-based), next to the printed values.
 
 Times are CUDA-event device times of hom2d_step (t and dt stay on the device;
 the host syncs once per 64 steps).  CFL values: Table 1 and Table 4
@@ -116,9 +120,106 @@ def shock_sweep(P, torch, out):
         json.dump({"case": "radial shock tube t=0.25, limiter on", "results": res}, f, indent=1)
 
 
+# --------------------------------------------------------------------------
+# Max-CFL protocol: "At the end of a simulation,
+# the error is recorded. A new simulation is completed at a value of 0.5*CFL of
+# the previous. ... If the percent error between these two errors is less than
+# 0.1 %, the CFL is termed the maximum CFL."  Read here as: the largest CFL on a
+# 0.01 grid (Table 1/4 print two digits) whose run is stable and whose error
+# differs from the run at half that CFL by < 0.1 %, scanning down from a value
+# above the stability limit.  Smooth problem: L2(rho) error at t = 1 (R8).
+# Discontinuous problem ("the residual error is used"): the L2
+# norm of the density residual R(q) of the state at t_end = 0.25.
+# --------------------------------------------------------------------------
+def protocol_metric(P, torch, method, k, n, cfl, case):
+    box, bc, lim, t_end = ((-5.0, 5.0, -5.0, 5.0), 0, 0, 1.0) if case == "vortex" else ((-1.0, 1.0, -1.0, 1.0), 1, 1, 0.25)
+    cfg = P.make_config(n, n, method=method, k=k, cfl=cfl, box=box, bc=bc, limiter=0 if method == "fv" else lim)
+    s = P.Solver(cfg)
+    try:
+        s.init_case(P.VORTEX if case == "vortex" else P.SHOCK)
+        s.step(10 ** 7, t_end)
+        if case == "vortex":
+            m = s.error(P.VORTEX, 0)[1]
+        else:
+            q = s.get_state(torch.empty(s.n_values, dtype=torch.float64, device="cuda"))
+            r = s.residual(q).view(4, -1)[0]
+            m = float(torch.sqrt(torch.mean(r * r)))
+    except P.NonPhysicalState:
+        m = None
+    finally:
+        s.close()
+    if m is not None and not math.isfinite(m):
+        m = None
+    return m
+
+
+def max_cfl(P, torch, method, k, n, case, c_hi):
+    cache = {}
+
+    def metric(c100):
+        if c100 not in cache:
+            cache[c100] = protocol_metric(P, torch, method, k, n, c100 / 100.0, case)
+        return cache[c100]
+
+    def metric_half(c100):
+        key = ("half", c100)
+        if key not in cache:
+            cache[key] = protocol_metric(P, torch, method, k, n, c100 / 200.0, case)
+        return cache[key]
+
+    for c100 in range(int(round(c_hi * 100)), 0, -1):
+        e1 = metric(c100)
+        if e1 is None:
+            continue
+        e2 = metric_half(c100)
+        if e2 is None or e2 == 0.0:
+            continue
+        change = abs(e1 - e2) / abs(e2)
+        if change < 1e-3:
+            return {"cfl": c100 / 100.0, "metric": e1, "metric_half": e2, "change": change, "runs": len(cache)}
+    return {"cfl": None, "runs": len(cache)}
+
+
+# Table 1 and Table 4 as printed, for the comparison
+TABLE1 = {1: {"dof": [1600, 3600, 6400, 10000, 14400],
+              "cpr": [0.24] * 5, "ndg": [0.24] * 5, "sd": [0.3] * 5, "dg": [0.24] * 5,
+              "fv": [0.4, 0.4, 0.38, 0.38, 0.37]},
+          2: {"dof": [3600, 8100, 14400, 22500, 32400],
+              "cpr": [0.14, 0.13, 0.13, 0.13, 0.13], "ndg": [0.14, 0.13, 0.13, 0.13, 0.13],
+              "sd": [0.2] * 5, "dg": [0.14, 0.13, 0.13, 0.13, 0.13], "fv": [0.4, 0.4, 0.38, 0.37, 0.37]}}
+TABLE4 = {1: {"dof": [160000, 640000], "cpr": [0.2, 0.2], "ndg": [0.2, 0.2], "sd": [0.3, 0.27],
+              "dg": [0.22, 0.2], "fv": [0.58, 0.58]},
+          2: {"dof": [360000, 1440000], "cpr": [0.1, 0.1], "ndg": [0.1, 0.1], "sd": [0.18, 0.18],
+              "dg": [0.08, 0.08], "fv": [0.54, 0.54]}}
+
+
+def cfl_protocol(P, torch, out, case):
+    res = []
+    if case == "vortex":
+        plan = [(k, i, dof) for k in (1, 2) for i, dof in enumerate(TABLE1[k]["dof"])]
+        plan += [(k, None, (k + 1) ** 2 * n * n) for k in (3, 4) for n in (20, 30, 40)]
+        table = TABLE1
+    else:
+        plan = [(k, i, dof) for k in (1, 2) for i, dof in enumerate(TABLE4[k]["dof"])]
+        table = TABLE4
+    for k, i, dof in plan:
+        for method in ("cpr", "ndg", "sd", "dg", "fv"):
+            if method == "fv" and k > 2:
+                continue
+            n = int(round(math.sqrt(dof if method == "fv" else dof / (k + 1) ** 2)))
+            c_hi = 1.0 if method == "fv" else 0.5
+            r = max_cfl(P, torch, method, k, n, case, c_hi)
+            r.update({"case": case, "method": method, "k": k, "n": n, "dof": dof,
+                      "paper": table[k][method][i] if i is not None else None})
+            res.append(r)
+            print(json.dumps(r), flush=True)
+    with open(out, "w") as f:
+        json.dump({"protocol": "max CFL, P:875-878", "case": case, "results": res}, f, indent=1)
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("what", choices=["order", "shock"])
+    ap.add_argument("what", choices=["order", "shock", "cfl", "cfl-shock"])
     ap.add_argument("--out", default=None)
     args = ap.parse_args()
     import torch
@@ -127,11 +228,13 @@ def main():
     from paper_1709_01619_b200 import build
     build.build()
     torch.cuda.set_device(0)
-    out = args.out or os.path.join(ROOT, "profiles", f"round1_sweep_{args.what}.json")
+    out = args.out or os.path.join(ROOT, "profiles", f"round1_sweep_{args.what.replace('-', '_')}.json")
     if args.what == "order":
         order_sweep(P, torch, out)
-    else:
+    elif args.what == "shock":
         shock_sweep(P, torch, out)
+    else:
+        cfl_protocol(P, torch, out, "vortex" if args.what == "cfl" else "shock")
 
 
 if __name__ == "__main__":
