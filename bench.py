@@ -55,7 +55,20 @@ WORKLOADS = {
     "sd_p4_4096": ("sd", 4, 4096, 4096, 0.08, False),
     "fv2_16384": ("fv", 1, 16384, 16384, 0.37, False),
     "fv3_16384": ("fv", 2, 16384, 16384, 0.37, False),
+    # limiter-on throughput: the radial shock tube scaled up,
+    # transmissive, minmod detection + limiting after every stage, Table 4 CFLs
+    "cpr_p1_shock_4096": ("cpr", 1, 4096, 4096, 0.2, False, "shock"),
+    "cpr_p2_shock_4096": ("cpr", 2, 4096, 4096, 0.1, False, "shock"),
+    "dg_p1_shock_4096": ("dg", 1, 4096, 4096, 0.2, False, "shock"),
+    "sd_p1_shock_4096": ("sd", 1, 4096, 4096, 0.27, False, "shock"),
+    "fv2_shock_8192": ("fv", 1, 8192, 8192, 0.58, False, "shock"),
 }
+
+
+def workload(wl):
+    """(method, k, nx, ny, cfl, weak, case) of a bench workload."""
+    w = WORKLOADS[wl]
+    return (*w[:6], w[6] if len(w) > 6 else "vortex")
 BYTES_PER_DOF_STEP = 256.0   # algorithmic HBM bytes: stage 1 64 B, stages 2/3 96 B (SURVEY 8(d))
 
 
@@ -123,11 +136,20 @@ def cpu_info():
     return "unknown"
 
 
-def oracle_rate(method, k, nx, ny, cfl, steps, seed_box=(-5.0, 5.0, -5.0, 5.0)):
+DATA = {"vortex": "synthetic (closed-form isentropic vortex, P:897-913)",
+        "shock": "synthetic (radial shock tube, P:1043-1047, scaled up; limiter on)"}
+
+
+def oracle_rate(method, k, nx, ny, cfl, steps, case="vortex"):
     """The CPU oracle as it stands (single thread), DOF-stage/s on a sample grid."""
     import oracle
-    cfg = oracle.config(nx=nx, ny=ny, method=method, k=k, cfl=cfl, box=seed_box)
-    q = oracle.init_case(cfg)
+    if case == "shock":
+        cfg = oracle.config(nx=nx, ny=ny, method=method, k=k, cfl=cfl, bc=oracle.TRANSMISSIVE,
+                            box=(-1.0, 1.0, -1.0, 1.0), limiter=1)
+        q = oracle.init_case(cfg, oracle.SHOCK)
+    else:
+        cfg = oracle.config(nx=nx, ny=ny, method=method, k=k, cfl=cfl)
+        q = oracle.init_case(cfg)
     t0 = time.perf_counter()
     oracle.run(cfg, q, steps)
     dt = time.perf_counter() - t0
@@ -141,10 +163,15 @@ def reference_arm(args, wl):
     if rank != 0:
         return
     import oracle
-    method, k, nx, ny, cfl, weak = WORKLOADS[wl]
+    method, k, nx, ny, cfl, weak, case = workload(wl)
     sn = 256 if method != "fv" else 1024
-    cfg = oracle.config(nx=sn, ny=sn, method=method, k=k, cfl=cfl)
-    q = oracle.init_case(cfg)
+    if case == "shock":
+        cfg = oracle.config(nx=sn, ny=sn, method=method, k=k, cfl=cfl, bc=oracle.TRANSMISSIVE,
+                            box=(-1.0, 1.0, -1.0, 1.0), limiter=1)
+        q = oracle.init_case(cfg, oracle.SHOCK)
+    else:
+        cfg = oracle.config(nx=sn, ny=sn, method=method, k=k, cfl=cfl)
+        q = oracle.init_case(cfg)
     for _ in range(args.warmup):
         q, _, _ = oracle.run(cfg, q, 1)
     t0 = time.perf_counter()
@@ -153,11 +180,11 @@ def reference_arm(args, wl):
     el = time.perf_counter() - t0
     ndof = sn * sn * (1 if method == "fv" else (k + 1) ** 2)
     v = ndof * 3 * args.steps / el
-    sample = f"{method.upper()} P{k} vortex {sn}x{sn} (sample of {nx}x{ny}), 1 SSP-RK3 step per bench step"
+    sample = f"{method.upper()} P{k} {case} {sn}x{sn} (sample of {nx}x{ny}), 1 SSP-RK3 step per bench step"
     line = {"impl": "reference", "metric": "fp64 DOF-stage updates/s", "value": v, "unit": "DOF-stage/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
             "higher_is_better": True, "scaling": "weak" if weak else "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (closed-form isentropic vortex, P:897-913)",
+            "data": DATA[case],
             "config": {"workload": f"{wl} (oracle sample {sn}x{sn})", "method": method, "k": k, "nx": sn, "ny": sn},
             "cpu_baseline": {"value": v, "unit": "DOF-stage/s", "cores": 1, "kind": "oracle", "sample": sample,
                              "cpu": cpu_info()},
@@ -205,7 +232,7 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
         dist.barrier()
-    method, k, nx, ny, cfl, weak = WORKLOADS[wl]
+    method, k, nx, ny, cfl, weak, case = workload(wl)
     if weak:
         ny = ny * world
     nid = None
@@ -214,9 +241,13 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         nid = obj[0]
     stream = torch.cuda.current_stream()
-    cfg = P.make_config(nx, ny, method=method, k=k, cfl=cfl)
+    if case == "shock":
+        cfg = P.make_config(nx, ny, method=method, k=k, cfl=cfl, bc=P.TRANSMISSIVE, box=(-1.0, 1.0, -1.0, 1.0),
+                            limiter=0 if method == "fv" else 1)
+    else:
+        cfg = P.make_config(nx, ny, method=method, k=k, cfl=cfl)
     s = P.Solver(cfg, rank=rank, nranks=world, device=local, stream=stream, nccl_id=nid)
-    s.init_case(P.VORTEX)
+    s.init_case(P.SHOCK if case == "shock" else P.VORTEX)
     npe = 1 if method == "fv" else (k + 1) ** 2
     ndof_global = nx * ny * npe
     ndof_local = nx * s.nrows * npe
@@ -286,19 +317,21 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         sn = 768 if method != "fv" else 3072   # ~15 s of single-core oracle work
-        v, el = oracle_rate(method, k, sn, sn, cfl, 6)
+        v, el = oracle_rate(method, k, sn, sn, cfl, 6, case)
         cpu = {"value": v, "unit": "DOF-stage/s", "cores": 1, "kind": "oracle",
-               "sample": f"{method.upper()} P{k} vortex {sn}x{sn} elements, 6 SSP-RK3 steps ({el:.1f} s)",
+               "sample": f"{method.upper()} P{k} {case} {sn}x{sn} elements, 6 SSP-RK3 steps ({el:.1f} s)",
                "cpu": cpu_info()}
 
     if rank == 0:
         line = {"metric": "fp64 DOF-stage updates/s", "value": value, "unit": "DOF-stage/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
                 "higher_is_better": True, "scaling": "weak" if weak else "strong", "vs_baseline": None,
-                "dtype": "f64", "data": "synthetic (closed-form isentropic vortex, P:897-913)",
+                "dtype": "f64", "data": DATA[case],
                 "config": {"workload": wl, "method": method, "k": k, "nx": nx, "ny": ny, "dof": ndof_global,
-                           "case": "isentropic vortex, periodic", "cfl": cfl, "parallelism": f"ystrip{world}",
-                           "l2_flush": "none needed: 8.6 GB/state array >> 126 MB L2"},
+                           "case": ("isentropic vortex, periodic" if case == "vortex" else
+                                    "radial shock tube, transmissive, minmod limiter every stage"),
+                           "cfl": cfl, "parallelism": f"ystrip{world}",
+                           "l2_flush": f"none needed: {4 * ndof_global * 8 / 1e9:.2f} GB/state array >> 126 MB L2"},
                 "e2e": e2e, "gpu_launches": gpu_launches, "roofline": roofline, "cpu_baseline": cpu,
                 "clocks": clocks,
                 "hbm_frac_end_to_end": value * BYTES_PER_DOF_STEP / 3.0 / 1e9 / world / peak}

@@ -181,10 +181,10 @@ __device__ __forceinline__ void count_dec(long long* dec, int which, int w = 1) 
 // (w: how many of the paper's face evaluations this one call stands for)
 __device__ __forceinline__ double minmod2(double a, double b, long long* dec, int w = 1) {
   // value without branches: the argument of smaller magnitude when both have the
-  // same strict sign (equal magnitudes: equal values), else 0
-  const bool same = (a > 0.0 && b > 0.0) || (a < 0.0 && b < 0.0);
+  // same strict sign (equal magnitudes: equal values), else 0.  Equal sign BITS
+  // suffice: a zero argument has the smaller magnitude, so m is then +-0 anyway.
   const double m = fabs(a) <= fabs(b) ? a : b;
-  const double r = __longlong_as_double(same ? __double_as_longlong(m) : 0ll);  // 9 SASS ops
+  const double r = (__double2hiint(a) ^ __double2hiint(b)) >= 0 ? m : 0.0;
   if (dec) {
     int which = 1;
     if ((a > 0.0 && b > 0.0) || (a < 0.0 && b < 0.0)) which = (fabs(a) <= fabs(b)) ? 2 : 3;

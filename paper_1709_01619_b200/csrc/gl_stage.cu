@@ -32,7 +32,7 @@ namespace {
 // smem, so narrower strips keep 2+ CTAs per SM (A/B on 4096^2: DG 16 > 32 by
 // 37 % at P3, 3-6 % at P2/P4; SD 32 > 16 by 10 % at P3, 16 > 32 by 13 % at P4)
 #ifndef H2D_DG_TX
-#define H2D_DG_TX 16
+#define H2D_DG_TX (K == 3 ? 14 : 16)  // P3: 14-element strips = 16-slot TMA rows, 4 CTAs/SM (+7.5 % over 16)
 #endif
 #ifndef H2D_SD_TX
 #define H2D_SD_TX (K == 3 ? 32 : 16)
@@ -40,13 +40,21 @@ namespace {
 #ifndef H2D_LMINB
 #define H2D_LMINB 1
 #endif
+// A/B on 8192^2 / 4096^2 (round 1): P1 at 4 CTAs/SM (<= 128 registers; SD +7 %),
+// P2 32-element strips at 4 CTAs/SM (DG +20 %, SD +36 % over 16 at 1)
 #ifndef H2D_LMINB1
-#define H2D_LMINB1 3  // P1 (128 threads): <= 168 registers, 3 CTAs/SM (smem allows 3-4)
+#define H2D_LMINB1 4
+#endif
+#ifndef H2D_LTX2
+#define H2D_LTX2 32
+#endif
+#ifndef H2D_LMINB2
+#define H2D_LMINB2 4
 #endif
 enum { LM_DG = 2, LM_SD = 4 };
 template <int M, int K> struct LTile {
-  static constexpr int TX = K == 1 ? 64 : (M == LM_DG ? H2D_DG_TX : H2D_SD_TX), RB = 64;
-  static constexpr int MINB = K == 1 ? H2D_LMINB1 : H2D_LMINB;
+  static constexpr int TX = K == 1 ? 64 : K == 2 ? H2D_LTX2 : (M == LM_DG ? H2D_DG_TX : H2D_SD_TX), RB = 64;
+  static constexpr int MINB = K == 1 ? H2D_LMINB1 : K == 2 ? H2D_LMINB2 : H2D_LMINB;
 };
 
 constexpr int NSTG = 3;

@@ -34,11 +34,11 @@ sys.path.insert(0, ROOT)
 
 CFL_SMOOTH = {("cpr", 1): 0.24, ("ndg", 1): 0.24, ("dg", 1): 0.24, ("sd", 1): 0.3,
               ("cpr", 2): 0.13, ("ndg", 2): 0.13, ("dg", 2): 0.13, ("sd", 2): 0.2,
-              # P3/P4: not in Table 1; SURVEY Q23's 1/(2k+1) fit (0.10 / 0.08) is unstable for
-              # CPR P3 on the vortex, so start lower; an unstable run halves the CFL (max-CFL
-              # protocol direction) and is reported
-              ("cpr", 3): 0.08, ("ndg", 3): 0.08, ("dg", 3): 0.08, ("sd", 3): 0.10,
-              ("cpr", 4): 0.05, ("ndg", 4): 0.05, ("dg", 4): 0.05, ("sd", 4): 0.06,
+              # P3/P4: not in Table 1; the max-CFL protocol over the GPU path (`sweep.py cfl`,
+              # profiles/round1_cfl_protocol.md), smallest value over its DoF levels.  An
+              # unstable run still halves the CFL and is reported
+              ("cpr", 3): 0.09, ("ndg", 3): 0.09, ("dg", 3): 0.09, ("sd", 3): 0.09,
+              ("cpr", 4): 0.05, ("ndg", 4): 0.06, ("dg", 4): 0.04, ("sd", 4): 0.03,
               ("fv", 1): 0.37, ("fv", 2): 0.37}
 LADDER = [20, 28, 40, 57, 80, 113, 160, 226, 320, 453, 640, 905, 1280, 1810, 2560]
 TARGETS = (1e-4, 2e-5)
