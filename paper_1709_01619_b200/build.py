@@ -66,14 +66,29 @@ def build(force: bool = False, verbose: bool = False, out: str = LIB, extra=()) 
     if out == LIB and not force and not stale():
         return LIB
     nd = nccl_dir()
-    cmd = [NVCC, *ARCH, *FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-I", os.path.join(nd, "include"),
-           "-o", out,
-           *sources(), "-L", os.path.join(nd, "lib"), "-l:libnccl.so.2", "-Xlinker",
-           "-rpath=" + os.path.join(nd, "lib")]
-    if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-        print(" ".join(cmd), flush=True)
-    subprocess.check_call(cmd)
+    inc = ["-I", os.path.join(ROOT, "include"), "-I", os.path.join(nd, "include")]
+    # one nvcc per translation unit, in parallel; then one link
+    import concurrent.futures
+    import tempfile
+    tmp = tempfile.mkdtemp(prefix="hom2d_build_")
+    objs = [os.path.join(tmp, os.path.basename(src) + ".o") for src in sources()]
+    cflags = [f for f in FLAGS if f != "-shared"]
+    cmds = []
+    for src, obj in zip(sources(), objs):
+        c = [NVCC, *ARCH, *cflags, *extra, *inc, "-c", "-o", obj, src]
+        if verbose:
+            c.insert(1, "-Xptxas=-v")
+        cmds.append(c)
+    with concurrent.futures.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
+        for c in ex.map(lambda c: (subprocess.check_call(c), c)[1], cmds):
+            if verbose:
+                print(" ".join(c), flush=True)
+    link = [NVCC, *ARCH, "-shared", "-o", out, *objs, "-L", os.path.join(nd, "lib"), "-l:libnccl.so.2",
+            "-Xlinker", "-rpath=" + os.path.join(nd, "lib")]
+    subprocess.check_call(link)
+    for o in objs:
+        os.remove(o)
+    os.rmdir(tmp)
     if out == LIB:
         with open(LIB + ".srchash", "w") as f:
             f.write(src_hash())

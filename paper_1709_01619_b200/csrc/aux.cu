@@ -229,56 +229,90 @@ __global__ void k_avg(const AuxArgs A, Nodes nd, const double* __restrict__ q, d
   }
 }
 
-// one thread per element: detect on density at every edge point, limit if marked
-__global__ void k_limit(const AuxArgs A, Nodes nd, double* q, const double* __restrict__ qbar,
-                        const double* qbar_lo, const double* qbar_hi, long long gcs, int bcx, double eps,
-                        long long* dec) {
-  if (A.dt && *A.dt == 0.0) return;
-  const int n = nd.n, np = n * n;
-  const long long ne = (long long)A.nx * A.nrows;
+// one thread per element (2-D grid: x = element column, y = element row, no
+// index division): detect on density at every edge point (Alg. 10: all 4N edge
+// values evaluated, straight-line), limit all four components if marked (Alg. 11,
+// Eq. (35) in 2-D)
+template <int N, bool GLLP>
+__device__ __forceinline__ void limit_element(const AuxArgs& A, const Nodes& nd, double* q,
+                                              const double* __restrict__ qbar, const double* qbar_lo,
+                                              const double* qbar_hi, long long gcs, int bcx, double eps,
+                                              long long* dec, int i, int j) {
+  constexpr int NP = N * N;
+  const long long ne = (long long)A.nx * A.nrows, m = (long long)j * A.nx + i;
   const double dx = (A.xmax - A.xmin) / A.nx, dy = (A.ymax - A.ymin) / A.ny_global;
-  for (long long m = blockIdx.x * (long long)blockDim.x + threadIdx.x; m < ne; m += (long long)gridDim.x * blockDim.x) {
-    const int i = (int)(m % A.nx), j = (int)(m / A.nx);
-    long long iw = i - 1, ie = i + 1;
-    bool hw = true, he = true;
-    if (iw < 0) { if (bcx) hw = false; else iw += A.nx; }
-    if (ie >= A.nx) { if (bcx) he = false; else ie -= A.nx; }
-    auto nb = [&](int c, int dir) -> double {  // neighbour averages (own if transmissive boundary)
-      const double own = qbar[c * ne + m];
-      if (dir == 0) return hw ? qbar[c * ne + (long long)j * A.nx + iw] : own;
-      if (dir == 1) return he ? qbar[c * ne + (long long)j * A.nx + ie] : own;
-      if (dir == 2) {
-        if (j > 0) return qbar[c * ne + (long long)(j - 1) * A.nx + i];
-        return qbar_lo ? qbar_lo[c * gcs + i] : own;
+  int iw = i - 1, ie = i + 1;
+  bool hw = true, he = true;
+  if (iw < 0) { if (bcx) hw = false; else iw += A.nx; }
+  if (ie >= A.nx) { if (bcx) he = false; else ie -= A.nx; }
+  // neighbour averages of component c (own average at a transmissive boundary)
+  auto nbr = [&](int c, double own, double& W, double& E, double& S, double& Nn) {
+    W = hw ? qbar[c * ne + (long long)j * A.nx + iw] : own;
+    E = he ? qbar[c * ne + (long long)j * A.nx + ie] : own;
+    if (j > 0) S = qbar[c * ne + m - A.nx];
+    else S = qbar_lo ? qbar_lo[c * gcs + i] : own;
+    if (j < A.nrows - 1) Nn = qbar[c * ne + m + A.nx];
+    else Nn = qbar_hi ? qbar_hi[c * gcs + i] : own;
+  };
+  const double qb = qbar[m];
+  double rW, rE, rS, rN;
+  nbr(0, qb, rW, rE, rS, rN);
+  double r[NP];
+  const double* Q0 = q + m * NP;
+#pragma unroll
+  for (int p = 0; p < NP; ++p) r[p] = Q0[p];
+  bool trip = false;
+#pragma unroll
+  for (int t = 0; t < N; ++t) {
+    double qw, qe_, qs, qn;
+    if (GLLP) {  // GLL edge nodes are solution points
+      qw = r[t * N];
+      qe_ = r[t * N + N - 1];
+      qs = r[t];
+      qn = r[(N - 1) * N + t];
+    } else {     // GL: interpolated traces of row t / column t
+      qw = qe_ = qs = qn = 0.0;
+#pragma unroll
+      for (int l = 0; l < N; ++l) {
+        qw += nd.eL[l] * r[t * N + l];
+        qe_ += nd.eR[l] * r[t * N + l];
+        qs += nd.eL[l] * r[l * N + t];
+        qn += nd.eR[l] * r[l * N + t];
       }
-      if (j < A.nrows - 1) return qbar[c * ne + (long long)(j + 1) * A.nx + i];
-      return qbar_hi ? qbar_hi[c * gcs + i] : own;
-    };
-    const double qb = qbar[m];
-    const double rW = nb(0, 0), rE = nb(0, 1), rS = nb(0, 2), rN = nb(0, 3);
-    const double* Q0 = q + m * np;
-    bool trip = false;
-    for (int s = 0; s < 4 && !trip; ++s)
-      for (int t = 0; t < n; ++t) {
-        const double* e = (s == 0 || s == 2) ? nd.eL : nd.eR;
-        double ql = 0.0;
-        for (int l = 0; l < n; ++l) ql += e[l] * Q0[s <= 1 ? t * n + l : l * n + t];
-        const double qp = s <= 1 ? rE : rN, qm = s <= 1 ? rW : rS;
-        const double qe = (s == 1 || s == 3) ? qb + minmod3(ql - qb, qp - qb, qb - qm)
-                                             : qb - minmod3(qb - ql, qp - qb, qb - qm);
-        if (fabs(ql - qe) > eps) { trip = true; break; }
-      }
-    if (!trip) continue;
-    if (dec) atomicAdd((unsigned long long*)&dec[0], 1ull);
-    for (int c = 0; c < 4; ++c) {
-      const double qc = qbar[c * ne + m];
-      const double sx = minmod2((nb(c, 1) - qc) / dx, (qc - nb(c, 0)) / dx, nullptr);
-      const double sy = minmod2((nb(c, 3) - qc) / dy, (qc - nb(c, 2)) / dy, nullptr);
-      for (int b = 0; b < n; ++b)
-        for (int a = 0; a < n; ++a)
-          q[c * A.cs + m * np + b * n + a] = qc + (0.5 * dx) * nd.xi[a] * sx + (0.5 * dy) * nd.xi[b] * sy;
     }
+    // right/top side: q_e = qbar + mm(q_l - qbar, ...); left/bottom: qbar - mm(qbar - q_l, ...)
+    const double ew = qb - minmod3(qb - qw, rE - qb, qb - rW);
+    const double ee = qb + minmod3(qe_ - qb, rE - qb, qb - rW);
+    const double es = qb - minmod3(qb - qs, rN - qb, qb - rS);
+    const double en = qb + minmod3(qn - qb, rN - qb, qb - rS);
+    trip |= (fabs(qw - ew) > eps) | (fabs(qe_ - ee) > eps) | (fabs(qs - es) > eps) | (fabs(qn - en) > eps);
   }
+  if (!trip) return;
+  if (dec) atomicAdd((unsigned long long*)&dec[0], 1ull);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const double qc = c == 0 ? qb : qbar[c * ne + m];
+    double W, E, S, Nn;
+    if (c == 0) { W = rW; E = rE; S = rS; Nn = rN; } else nbr(c, qc, W, E, S, Nn);
+    const double sx = minmod2((E - qc) / dx, (qc - W) / dx, nullptr);
+    const double sy = minmod2((Nn - qc) / dy, (qc - S) / dy, nullptr);
+    double* Qc = q + c * A.cs + m * NP;
+#pragma unroll
+    for (int b = 0; b < N; ++b)
+#pragma unroll
+      for (int a = 0; a < N; ++a) Qc[b * N + a] = qc + (0.5 * dx) * nd.xi[a] * sx + (0.5 * dy) * nd.xi[b] * sy;
+  }
+}
+
+template <int N, bool GLLP>
+__global__ void __launch_bounds__(128) k_limit(const AuxArgs A, Nodes nd, double* q, const double* __restrict__ qbar,
+                                               const double* qbar_lo, const double* qbar_hi, long long gcs, int bcx,
+                                               double eps, long long* dec) {
+  if (A.dt && *A.dt == 0.0) return;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= A.nx) return;
+  for (int j = blockIdx.y; j < A.nrows; j += gridDim.y)
+    limit_element<N, GLLP>(A, nd, q, qbar, qbar_lo, qbar_hi, gcs, bcx, eps, dec, i, j);
 }
 }  // namespace
 
@@ -313,11 +347,27 @@ void launch_averages(const AuxArgs& a, const double* q, double* qbar, cudaStream
   k_avg<<<grid_for(ne, 128), 128, 0, s>>>(a, nodes_for(a.method, a.k), q, qbar);
 }
 
+template <int N, bool GLLP>
+void launch_limit_t(const AuxArgs& a, double* q, const double* qbar, const double* qbar_lo, const double* qbar_hi,
+                    long long qbar_gcs, int bcx, double eps, long long* dec, cudaStream_t s) {
+  dim3 grid((a.nx + 127) / 128, a.nrows < 65535 ? a.nrows : 65535);
+  k_limit<N, GLLP><<<grid, 128, 0, s>>>(a, nodes_for(a.method, a.k), q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps,
+                                         dec);
+}
+
 void launch_limit(const AuxArgs& a, double* q, const double* qbar, const double* qbar_lo, const double* qbar_hi,
                   long long qbar_gcs, int bcx, double eps, long long* dec, cudaStream_t s) {
-  const long long ne = (long long)a.nx * a.nrows;
-  k_limit<<<grid_for(ne, 128), 128, 0, s>>>(a, nodes_for(a.method, a.k), q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx,
-                                            eps, dec);
+  const bool gll = (a.method == 1 || a.method == 3);
+#define H2D_LIM(NN)                                                                                     \
+  return gll ? launch_limit_t<NN, true>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, dec, s)       \
+             : launch_limit_t<NN, false>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, dec, s)
+  switch (a.k) {
+    case 1: H2D_LIM(2);
+    case 2: H2D_LIM(3);
+    case 3: H2D_LIM(4);
+    default: H2D_LIM(5);
+  }
+#undef H2D_LIM
 }
 
 }  // namespace h2d

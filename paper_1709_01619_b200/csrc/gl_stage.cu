@@ -74,10 +74,11 @@ struct LOps {
   static constexpr int DV = SD + N * (N + 1);  // DG volume operator (w_l / w_a) l'_a(xi_l)  [N][N]
   static constexpr int SR = DV + N * N;        // DG surface weights l_a(+1) / w_a
   static constexpr int SL = SR + N;            // DG surface weights l_a(-1) / w_a
-  static constexpr int TOT = SL + N;
+  static constexpr int W = SL + N;             // GL weights (element averages, Alg. 9)
+  static constexpr int TOT = W + N;
 };
 struct LTab {
-  double v[10 + 30 + 30 + 25 + 10];
+  double v[10 + 30 + 30 + 25 + 10 + 5];
 };
 template <int K>
 LTab make_ltab() {
@@ -95,6 +96,7 @@ LTab make_ltab() {
     for (int l = 0; l < N; ++l) t.v[T::DV + a * N + l] = O::dg_vol[a][l];
     t.v[T::SR + a] = O::dg_sR[a];
     t.v[T::SL + a] = O::dg_sL[a];
+    t.v[T::W + a] = O::w_gl[a];
   }
   return t;
 }
@@ -361,6 +363,7 @@ __global__ void __launch_bounds__(L<M, K>::NT, LTile<M, K>::MINB) gl_stage_kerne
     double q[4][N];
     double phi[N + 1][4];           // SD: x flux-point fluxes (interior; [0] = F^W)
     double fl[4][N];                // DG: x fluxes of the line
+    double lpart[4] = {0.0, 0.0, 0.0, 0.0};  // limiter runs: the line's share of the element average
     // Face work of the row, straight-line so that the independent node
     // evaluations interleave: the W face of each line (its W neighbour's E trace
     // interpolated here), the N face of column b of each element (own N trace vs
@@ -569,6 +572,41 @@ __global__ void __launch_bounds__(L<M, K>::NT, LTile<M, K>::MINB) gl_stage_kerne
       }
       if (a.q0 && Lr < RBv)  // q^n of the next row into the consumed private slots
         q0_prefetch<N, NT>(sQ0, a.q0, a.cs, base + (long long)a.nx * NP, tid, vec);
+      if (a.qbar) {  // this line's share of the element average: w_b sum_x w_x q
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          double sx = 0.0;
+#pragma unroll
+          for (int x = 0; x < N; ++x) sx += tab.v[T::W + x] * ov[c][x];
+          lpart[c] = sT[T::W + b] * sx;
+        }
+      }
+    }
+    if (a.qbar && (N == 2 || N == 4)) {  // element averages: the element's N lines are N aligned lanes
+      // lanes of this warp that exist (NT need not be a multiple of 32; element lane groups are whole)
+      const unsigned wmask = (NT % 32 == 0 || (tid >> 5) < NT / 32) ? 0xffffffffu : ((1u << (NT % 32)) - 1u);
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int o = 1; o < N; o <<= 1) lpart[c] += __shfl_xor_sync(wmask, lpart[c], o);
+      if (Lr > 0 && own && b == 0) {
+        const long long m = jr * a.nx + i0 + lx, ne = (long long)a.nx * a.nrows;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) a.qbar[c * ne + m] = 0.25 * lpart[c];
+      }
+    } else if (a.qbar) {  // element averages (N = 3, 5: through the W-face buffer)
+      __syncthreads();
+      if (Lr > 0 && own) st4(sFW + (lx * N + b) * 4, lpart);
+      __syncthreads();
+      if (Lr > 0 && own) {
+        const long long m = jr * a.nx + i0 + lx, ne = (long long)a.nx * a.nrows;
+        for (int c = b; c < 4; c += N) {
+          double s = 0.0;
+#pragma unroll
+          for (int bb = 0; bb < N; ++bb) s += sFW[(lx * N + bb) * 4 + c];
+          a.qbar[c * ne + m] = 0.25 * s;
+        }
+      }
     }
     __syncthreads();
     if (Lr + NSTG < nload) {

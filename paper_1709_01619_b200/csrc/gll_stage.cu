@@ -36,22 +36,28 @@ namespace h2d {
 namespace {
 
 template <int K> struct GTile;
+// CTAs per SM (register cap 64K / (MINB x threads)) and strip widths, A/B-timed on
+// 4096^2 / 8192^2 (round 1): P1 MINB 4 (+9 % over 2), P2 MINB 4 (+41 % over 2),
+// P4 16-element strips at 2 CTAs/SM (+25 % over 32 at 1 CTA/SM)
 #ifndef H2D_MINB1
-#define H2D_MINB1 2
+#define H2D_MINB1 4
 #endif
 #ifndef H2D_MINB2
-#define H2D_MINB2 2
+#define H2D_MINB2 4
 #endif
 #ifndef H2D_TX4
-#define H2D_TX4 32
+#define H2D_TX4 16
 #endif
 #ifndef H2D_MINB4
-#define H2D_MINB4 1
+#define H2D_MINB4 2
 #endif
 template <> struct GTile<1> { static constexpr int TX = 64, RB = 64, MINB = H2D_MINB1; };  // 128 threads
 template <> struct GTile<2> { static constexpr int TX = 32, RB = 64, MINB = H2D_MINB2; };  //  96 threads
 #ifndef H2D_MINB3
 #define H2D_MINB3 4
+#endif
+#ifndef H2D_NDG_TX3
+#define H2D_NDG_TX3 14  // A/B: +8.5 % over 16 (3 -> 4 CTAs/SM)
 #endif
 #ifndef H2D_TX3
 #define H2D_TX3 16  // 64 threads: 4 CTAs/SM interleave their barrier phases (A/B: +2.5 % over 32)
@@ -69,7 +75,9 @@ struct GMaps {   // P3: 3-D tensor maps {16 points, TX+2 elements, 4 components}
 template <int M, int K>
 struct G {
   static constexpr int N = K + 1, NP = N * N;
-  static constexpr int TX = GTile<K>::TX, RB = GTile<K>::RB, NT = TX * N;
+  // NDG P3 keeps g of every point in smem: 14-element strips (16-slot TMA rows)
+  // keep it at 4 CTAs/SM
+  static constexpr int TX = (M == GM_NDG && K == 3) ? H2D_NDG_TX3 : GTile<K>::TX, RB = GTile<K>::RB, NT = TX * N;
   static constexpr bool SWZ = (NP == 16);           // element row of one component == 128 B
   static constexpr int NSL = TX + 2;                 // W halo, TX elements, E halo
   // 1-D path: W piece | main piece | E piece per component (aligned supersets)
@@ -90,7 +98,7 @@ struct G {
   static constexpr int OG = OJS + 2 * TX * N * 4;     // NDG: g at every point [TX][NP][4]
   static constexpr int GS = NP * 4 + 2;  // padded element stride (conflict-free column reads)
   static constexpr int OT = OG + (M == GM_NDG ? TX * GS : 0);
-  static constexpr int ORD = OT + ((N * N + 2 * N + 1) & ~1);
+  static constexpr int ORD = OT + ((N * N + 3 * N + 1) & ~1);
   static constexpr int OB = ORD + 32;                 // mbarriers (as doubles)
   static constexpr int LP = (N + 1) & ~1;             // q^n line slot (16-B multiple)
   static constexpr int OQ0 = OB + ((NSTG + 1) & ~1);  // q^n prefetch [4][NT][LP], thread-private
@@ -125,7 +133,7 @@ __device__ __forceinline__ void q0_prefetch(double* sq0, const double* q0, long 
 }
 
 struct GTab {
-  double v[25 + 10];
+  double v[25 + 10 + 5];  // D [N][N], g'_L, g'_R, GLL weights
 };
 
 template <int K>
@@ -137,6 +145,7 @@ GTab make_gtab() {
     for (int l = 0; l < N; ++l) t.v[a * N + l] = O::D_gll[a][l];
     t.v[N * N + a] = O::gLp_gll[a];
     t.v[N * N + N + a] = O::gRp_gll[a];
+    t.v[N * N + 2 * N + a] = O::w_gll[a];
   }
   return t;
 }
@@ -227,7 +236,7 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
   const int ie = i0 + TXv < a.nx ? i0 + TXv : 0;  // E halo element
   const int nload = RBv + 2;                      // rows jb-1 .. jb+RBv
 
-  for (int i = tid; i < N * N + 2 * N; i += NT) sT[i] = tab.v[i];
+  for (int i = tid; i < N * N + 3 * N; i += NT) sT[i] = tab.v[i];
   if (tid == 0) {
     for (int s = 0; s < NSTG; ++s) mbar_init(&bar[s], 1);
     mbar_fence_init();
@@ -344,6 +353,7 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
 
     double q[4][N], fW[4], fE[4], jW[4];
     double fxl[4][N];  // NDG: x fluxes of the line
+    double lpart[4] = {0.0, 0.0, 0.0, 0.0};  // limiter runs: the line's share of the element average
     Prim pW, pE;
     // Face work of the row, straight-line so that the independent node
     // evaluations (reciprocal / square-root chains) interleave: the W face of
@@ -561,6 +571,41 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
       }
       if (a.q0 && L < RBv)  // q^n of the next row into the (now consumed) private slots
         q0_prefetch<N, NT, H::LP>(sQ0, a.q0, a.cs, base + (long long)a.nx * NP, tid, vec);
+      if (a.qbar) {  // this line's share of the element average: w_b sum_x w_x q
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          double sx = 0.0;
+#pragma unroll
+          for (int x = 0; x < N; ++x) sx += tab.v[N * N + 2 * N + x] * ov[c][x];
+          lpart[c] = sT[N * N + 2 * N + b] * sx;
+        }
+      }
+    }
+    if (a.qbar && (N == 2 || N == 4)) {  // element averages: the element's N lines are N aligned lanes
+      // lanes of this warp that exist (NT need not be a multiple of 32; element lane groups are whole)
+      const unsigned wmask = (NT % 32 == 0 || (tid >> 5) < NT / 32) ? 0xffffffffu : ((1u << (NT % 32)) - 1u);
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int o = 1; o < N; o <<= 1) lpart[c] += __shfl_xor_sync(wmask, lpart[c], o);
+      if (L > 0 && own && b == 0) {
+        const long long m = jr * a.nx + i0 + lx, ne = (long long)a.nx * a.nrows;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) a.qbar[c * ne + m] = 0.25 * lpart[c];
+      }
+    } else if (a.qbar) {  // element averages (N = 3, 5: through the W-face buffer)
+      __syncthreads();
+      if (L > 0 && own) st4(sFW + (lx * N + b) * 4, lpart);
+      __syncthreads();
+      if (L > 0 && own) {
+        const long long m = jr * a.nx + i0 + lx, ne = (long long)a.nx * a.nrows;
+        for (int c = b; c < 4; c += N) {
+          double s = 0.0;
+#pragma unroll
+          for (int bb = 0; bb < N; ++bb) s += sFW[(lx * N + bb) * 4 + c];
+          a.qbar[c * ne + m] = 0.25 * s;
+        }
+      }
     }
     __syncthreads();  // stage L % NSTG and the face buffers are free again
     if (L + NSTG < nload) {

@@ -211,7 +211,7 @@ int launch_stage(hom2d* h, const StageArgs& s) {
 // ghost rows have arrived.  Per-element arithmetic does not depend on the
 // launch split, so the result is bitwise the single-launch one.
 hom2d_status run_stage(hom2d* h, const double* q, const double* q0, double* out, double a0, double a1, double b,
-                       const double* dt, unsigned long long* lam, unsigned long long* bad) {
+                       const double* dt, unsigned long long* lam, unsigned long long* bad, double* qbar = nullptr) {
   StageArgs s{};
   const long long row_vals = (long long)h->cfg.nx * h->np;
   const int G = h->G;
@@ -236,6 +236,7 @@ hom2d_status run_stage(hom2d* h, const double* q, const double* q0, double* out,
   s.lam = lam; s.bad = bad;
   s.dec = h->cfg.record_decisions ? h->dec : nullptr;
   s.count_bot = (h->rank == 0);
+  s.qbar = qbar;
   int e = 0;
   if (!split) {
     s.row_lo = 0; s.row_hi = h->nrows;
@@ -258,12 +259,16 @@ hom2d_status run_stage(hom2d* h, const double* q, const double* q0, double* out,
   return HOM2D_OK;
 }
 
-// HO limiter on X in place: averages, (exchange average rows), detect + limit.
+// HO limiter on X in place: averages (unless the stage kernel that produced X
+// already wrote them, avg_done), (exchange average rows), detect + limit.
 // dt != nullptr: skipped on the device when the step was clipped out (*dt == 0).
-hom2d_status run_limiter(hom2d* h, double* X, const double* dt = nullptr) {
+hom2d_status run_limiter(hom2d* h, double* X, const double* dt = nullptr, bool avg_done = false) {
   AuxArgs A = aux(h);
   A.dt = dt;
-  launch_averages(A, X, h->qbar, h->stream);
+  if (!avg_done) {
+    launch_averages(A, X, h->qbar, h->stream);
+    h->launches++;
+  }
   const long long ne = (long long)h->cfg.nx * h->nrows;
   const double *lo, *hi;
   long long gcs;
@@ -271,7 +276,7 @@ hom2d_status run_limiter(hom2d* h, double* X, const double* dt = nullptr) {
   if (st) return st;
   launch_limit(A, X, h->qbar, lo, hi, gcs, h->cfg.bc, h->cfg.limiter_eps,
                h->cfg.record_decisions ? h->dec : nullptr, h->stream);
-  h->launches += 2;
+  h->launches++;
   CU(h, cudaPeekAtLastError());
   return HOM2D_OK;
 }
@@ -505,15 +510,18 @@ hom2d_status hom2d_step(hom2d* h, int32_t max_steps, double t_end, double* t_out
       h->launches++;
       const double* dt = h->clock + 1;
       // SSP-RK3 (Shu-Osher)
-      if ((st = run_stage(h, h->Qn, nullptr, h->Q1, 0.0, 1.0, 1.0, dt, nullptr, nullptr))) return st;
-      if (lim && (st = run_limiter(h, h->Q1, dt))) return st;
-      if ((st = run_stage(h, h->Q1, h->Qn, h->Q2, 0.75, 0.25, 0.25, dt, nullptr, nullptr))) return st;
-      if (lim && (st = run_limiter(h, h->Q2, dt))) return st;
+      // limiter runs: the stage kernels also write the element averages of their output
+      double* qb = lim ? h->qbar : nullptr;
+      if ((st = run_stage(h, h->Qn, nullptr, h->Q1, 0.0, 1.0, 1.0, dt, nullptr, nullptr, qb))) return st;
+      if (lim && (st = run_limiter(h, h->Q1, dt, true))) return st;
+      if ((st = run_stage(h, h->Q1, h->Qn, h->Q2, 0.75, 0.25, 0.25, dt, nullptr, nullptr, qb))) return st;
+      if (lim && (st = run_limiter(h, h->Q2, dt, true))) return st;
       if (!lim) {
         if ((st = run_stage(h, h->Q2, h->Qn, h->Qn, 1.0 / 3.0, 2.0 / 3.0, 2.0 / 3.0, dt, h->lam, h->bad))) return st;
       } else {
-        if ((st = run_stage(h, h->Q2, h->Qn, h->Qn, 1.0 / 3.0, 2.0 / 3.0, 2.0 / 3.0, dt, nullptr, nullptr))) return st;
-        if ((st = run_limiter(h, h->Qn, dt))) return st;
+        if ((st = run_stage(h, h->Q2, h->Qn, h->Qn, 1.0 / 3.0, 2.0 / 3.0, 2.0 / 3.0, dt, nullptr, nullptr, qb)))
+          return st;
+        if ((st = run_limiter(h, h->Qn, dt, true))) return st;
         launch_lambda(aux(h), h->Qn, h->lam, h->bad, h->stream);  // dt of the limited state
         h->launches++;
       }

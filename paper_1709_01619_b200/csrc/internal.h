@@ -29,6 +29,8 @@ struct StageArgs {
   unsigned long long* bad; // optional: atomicMin of the first non-physical point index
   long long* dec;          // optional: decision counters [8]
   int count_bot;           // this strip owns the domain's bottom face row (decision counting)
+  double* qbar;            // optional (HO limiter runs): element averages of `out`, [4][nx*nrows]
+                           // (Alg. 9: 1/4 sum_ab w_a w_b q_ab), fused into the stage epilogue
   int row_lo, row_hi;      // this launch updates strip rows [row_lo, row_hi) (row_hi == 0: all rows);
                           // it may read rows row_lo-G .. row_hi+G-1 (ghost rows outside the strip)
   int rows;                // marching kernels: element rows per CTA (set by the launcher)
