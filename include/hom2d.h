@@ -74,6 +74,13 @@ typedef struct {
   double limiter_eps;         /* detection threshold, P:357 (1e-3) */
   int32_t cpr_chain_rule;     /* CPR: 1 = chain-rule divergence; 0 = flux differentiation */
   int32_t record_decisions;   /* 1 = count branch decisions (minmod outcomes, marks); slower */
+  /* Method variants where the paper is silent (0 = the DESIGN.md reading):   */
+  int32_t limiter_per_step;   /* HO: 1 = limit once per SSP-RK3 step (after stage 3) instead of after
+                                 every stage ("The updated solution is interpolated..."; Q13) */
+  int32_t limiter_all_vars;   /* HO: 1 = trouble detection on all four conserved components instead of
+                                 density only (Alg. 10 P:802-836 names no variable; Q12) */
+  int32_t fv_unlimited;       /* FV: 1 = unlimited kappa-scheme (kappa = 0 for k = 1, 1/3 for k = 2),
+                                 i.e. MUSCL without the minmod of P:346-351 (Q10) */
 } hom2d_config;
 
 typedef struct {
@@ -141,7 +148,10 @@ hom2d_status hom2d_compute_dt(hom2d* h, double* dt);
 
 /* March with SSP-RK3 until *steps_out == max_steps or t == t_end (last dt
  * clipped).  dt is recomputed from the state every step.  Syncs the host once
- * per batch of steps.  Returns HOM2D_ERR_NONPHYSICAL if a bad state appeared. */
+ * per batch of up to 64 steps.  Returns HOM2D_ERR_NONPHYSICAL if a bad state
+ * appeared.  Single GPU: batches replay cached CUDA graphs of 2^i steps (captured
+ * on first use on an internal stream, fenced to the handle's stream by events;
+ * environment HOM2D_NO_GRAPH=1 or per-stage timing switch to eager launches). */
 hom2d_status hom2d_step(hom2d* h, int32_t max_steps, double t_end, double* t_out, int64_t* steps_out);
 
 /* Error of component var (0..3) against the exact vortex at the current t

@@ -36,6 +36,7 @@ class OrcConfig(C.Structure):
         ("cpr_chain_rule", C.c_int32),
         ("physics", C.c_int32), ("adv_a", C.c_double), ("adv_b", C.c_double),
         ("dt_fixed", C.c_double),
+        ("limiter_per_step", C.c_int32), ("limiter_all_vars", C.c_int32), ("fv_unlimited", C.c_int32),
     ]
 
 
@@ -76,6 +77,7 @@ def lib():
         L.orc_minmod3.argtypes = [d, d, d]
         L.orc_minmod3.restype = d
         L.orc_muscl_face.argtypes = [C.c_int, vp, vp, vp, vp, vp, vp]
+        L.orc_muscl_face_unlimited.argtypes = [C.c_int, vp, vp, vp, vp, vp, vp]
         L.orc_residual.argtypes = [cfgp, vp, vp, vp]
         L.orc_averages.argtypes = [cfgp, vp, vp]
         L.orc_limit.argtypes = [cfgp, vp, vp, vp]
@@ -101,10 +103,11 @@ def _p(a: np.ndarray):
 
 def config(nx=10, ny=10, method="cpr", k=1, bc=PERIODIC, box=(-5.0, 5.0, -5.0, 5.0), gamma=1.4,
            cfl=0.24, limiter=0, limiter_eps=1e-3, cpr_chain_rule=1, physics=0, adv=(1.0, 0.5),
-           dt_fixed=0.0) -> OrcConfig:
+           dt_fixed=0.0, limiter_per_step=0, limiter_all_vars=0, fv_unlimited=0) -> OrcConfig:
     m = METHODS[method] if isinstance(method, str) else int(method)
     return OrcConfig(nx, ny, box[0], box[1], box[2], box[3], bc, m, k, gamma, cfl, limiter,
-                     limiter_eps, cpr_chain_rule, physics, adv[0], adv[1], dt_fixed)
+                     limiter_eps, cpr_chain_rule, physics, adv[0], adv[1], dt_fixed,
+                     limiter_per_step, limiter_all_vars, fv_unlimited)
 
 
 def npts(cfg: OrcConfig) -> int:
@@ -182,9 +185,10 @@ def minmod3(a, b, c):
     return lib().orc_minmod3(float(a), float(b), float(c))
 
 
-def muscl_face(order, qm1, q0, q1, q2):
+def muscl_face(order, qm1, q0, q1, q2, unlimited=False):
     qW, qE = np.zeros(4), np.zeros(4)
-    lib().orc_muscl_face(order, _p(_v4(qm1)), _p(_v4(q0)), _p(_v4(q1)), _p(_v4(q2)), _p(qW), _p(qE))
+    fn = lib().orc_muscl_face_unlimited if unlimited else lib().orc_muscl_face
+    fn(order, _p(_v4(qm1)), _p(_v4(q0)), _p(_v4(q1)), _p(_v4(q2)), _p(qW), _p(qE))
     return qW, qE
 
 

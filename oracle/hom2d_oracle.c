@@ -54,6 +54,10 @@ typedef struct {
   int32_t physics;        /* test-only: 0 = Euler, 1 = linear advection */
   double adv_a, adv_b;    /* test-only: advection velocity for physics == 1 */
   double dt_fixed;        /* test-only: > 0 replaces the CFL dt of Eq. (36) */
+  /* method variants (the defaults 0 are the readings Q10, Q12, Q13) */
+  int32_t limiter_per_step;  /* HO: 1 = limit once per step (after stage 3) instead of every stage (Q13) */
+  int32_t limiter_all_vars;  /* HO: 1 = detect on all four conserved components, not rho only (Q12) */
+  int32_t fv_unlimited;      /* FV: 1 = unlimited kappa-scheme (kappa = 0 / 1/3), no minmod (Q10) */
 } orc_config;
 
 /* decision counters (parity of branch decisions); a minmod whose
@@ -573,11 +577,20 @@ static int fv_idx(int i, int n, int bc) {
   return i < 0 ? 0 : (i >= n ? n - 1 : i);
 }
 
-/* face states at face between cells q0 (=i) and q1 (=i+1), stencil qm1, q0, q1, q2 */
+/* face states at face between cells q0 (=i) and q1 (=i+1), stencil qm1, q0, q1, q2.
+ * unlim = 1: the same kappa-schemes without the limiter (Q10 alternative, f3):
+ * MUSCL-2 kappa = 0, q_W = q_i + (dm + dp)/4; MUSCL-3 kappa = 1/3 with the raw
+ * differences in place of the two minmods (van Leer's kappa-scheme). */
 static void muscl_face(int order, const double *qm1, const double *q0, const double *q1, const double *q2,
-                       double *qW, double *qE, int64_t *cnt) {
+                       double *qW, double *qE, int64_t *cnt, int unlim) {
   for (int c = 0; c < 4; ++c) {
-    if (order == 1) {
+    if (unlim) {
+      const double kap = order == 1 ? 0.0 : 1.0 / 3.0;
+      double dm0 = q0[c] - qm1[c], dp0 = q1[c] - q0[c];   /* cell i   */
+      double dm1 = q1[c] - q0[c], dp1 = q2[c] - q1[c];    /* cell i+1 */
+      qW[c] = q0[c] + 0.25 * ((1.0 - kap) * dm0 + (1.0 + kap) * dp0);
+      qE[c] = q1[c] - 0.25 * ((1.0 - kap) * dp1 + (1.0 + kap) * dm1);
+    } else if (order == 1) {
       double s0 = mm2(q0[c] - qm1[c], q1[c] - q0[c], cnt);
       double s1 = mm2(q1[c] - q0[c], q2[c] - q1[c], cnt);
       qW[c] = q0[c] + 0.5 * s0;
@@ -594,7 +607,12 @@ static void muscl_face(int order, const double *qm1, const double *q0, const dou
 
 void orc_muscl_face(int order, const double *qm1, const double *q0, const double *q1, const double *q2,
                     double *qW, double *qE) {
-  muscl_face(order, qm1, q0, q1, q2, qW, qE, NULL);
+  muscl_face(order, qm1, q0, q1, q2, qW, qE, NULL, 0);
+}
+
+void orc_muscl_face_unlimited(int order, const double *qm1, const double *q0, const double *q1, const double *q2,
+                              double *qW, double *qE) {
+  muscl_face(order, qm1, q0, q1, q2, qW, qE, NULL, 1);
 }
 
 static void residual_fv(const orc_config *cf, const double *Q, double *R, int64_t *cnt) {
@@ -609,7 +627,7 @@ static void residual_fv(const orc_config *cf, const double *Q, double *R, int64_
     for (int f = 0; f <= nx; ++f) {   /* face f between cells f-1 and f */
       double s[4][4], qW[4], qE[4], F[4];
       for (int t = 0; t < 4; ++t) getq(Q, N, (int64_t)j * nx + fv_idx(f - 2 + t, nx, cf->bc), 1, 0, s[t]);
-      muscl_face(cf->k, s[0], s[1], s[2], s[3], qW, qE, cnt);
+      muscl_face(cf->k, s[0], s[1], s[2], s[3], qW, qE, cnt, cf->fv_unlimited);
       rusanov(&P, 0, qW, qE, F);
       for (int c = 0; c < 4; ++c) Fx[((size_t)j * (nx + 1) + f) * 4 + c] = F[c];
     }
@@ -617,7 +635,7 @@ static void residual_fv(const orc_config *cf, const double *Q, double *R, int64_
     for (int i = 0; i < nx; ++i) {
       double s[4][4], qW[4], qE[4], F[4];
       for (int t = 0; t < 4; ++t) getq(Q, N, (int64_t)fv_idx(f - 2 + t, ny, cf->bc) * nx + i, 1, 0, s[t]);
-      muscl_face(cf->k, s[0], s[1], s[2], s[3], qW, qE, cnt);
+      muscl_face(cf->k, s[0], s[1], s[2], s[3], qW, qE, cnt, cf->fv_unlimited);
       rusanov(&P, 1, qW, qE, F);
       for (int c = 0; c < 4; ++c) Gy[((size_t)f * nx + i) * 4 + c] = F[c];
     }
@@ -685,31 +703,35 @@ int orc_limit(const orc_config *cf, double *Q, int32_t *marks, int64_t *cnt) {
   double *Qbar = (double *)malloc(sizeof(double) * 4 * Ne);
   int32_t *mk = (int32_t *)calloc((size_t)Ne, sizeof(int32_t));
   orc_averages(cf, Q, Qbar);
-  /* step 2: detect on density at every edge point */
+  /* step 2: detect on density (limiter_all_vars: on every conserved component)
+   * at every edge point */
+  const int nvar = cf->limiter_all_vars ? 4 : 1;
   for (int j = 0; j < ny; ++j)
     for (int i = 0; i < nx; ++i) {
       int64_t m = (int64_t)j * nx + i;
       int iw = nb_index(i, -1, nx, cf->bc), ie = nb_index(i, 1, nx, cf->bc);
       int js = nb_index(j, -1, ny, cf->bc), jn = nb_index(j, 1, ny, cf->bc);
-      double qb = Qbar[m];
-      double qW = iw >= 0 ? Qbar[(int64_t)j * nx + iw] : qb;
-      double qE = ie >= 0 ? Qbar[(int64_t)j * nx + ie] : qb;
-      double qS = js >= 0 ? Qbar[(int64_t)js * nx + i] : qb;
-      double qN = jn >= 0 ? Qbar[(int64_t)jn * nx + i] : qb;
       int trip = 0;
-      for (int s = 0; s < 4; ++s)
-        for (int t = 0; t < n; ++t) {
-          double qt[4];
-          trace(&o, gll, Q, N, m, s, t, qt);
-          double ql = qt[0], qe;
-          double qp = (s <= 1) ? qE : qN, qm = (s <= 1) ? qW : qS;
-          if (s == 1 || s == 3) {           /* right / top side */
-            qe = qb + mm3(ql - qb, qp - qb, qb - qm);
-          } else {                          /* left / bottom side */
-            qe = qb - mm3(qb - ql, qp - qb, qb - qm);
+      for (int c = 0; c < nvar; ++c) {
+        double qb = Qbar[c * Ne + m];
+        double qW = iw >= 0 ? Qbar[c * Ne + (int64_t)j * nx + iw] : qb;
+        double qE = ie >= 0 ? Qbar[c * Ne + (int64_t)j * nx + ie] : qb;
+        double qS = js >= 0 ? Qbar[c * Ne + (int64_t)js * nx + i] : qb;
+        double qN = jn >= 0 ? Qbar[c * Ne + (int64_t)jn * nx + i] : qb;
+        for (int s = 0; s < 4; ++s)
+          for (int t = 0; t < n; ++t) {
+            double qt[4];
+            trace(&o, gll, Q, N, m, s, t, qt);
+            double ql = qt[c], qe;
+            double qp = (s <= 1) ? qE : qN, qm = (s <= 1) ? qW : qS;
+            if (s == 1 || s == 3) {           /* right / top side */
+              qe = qb + mm3(ql - qb, qp - qb, qb - qm);
+            } else {                          /* left / bottom side */
+              qe = qb - mm3(qb - ql, qp - qb, qb - qm);
+            }
+            if (fabs(ql - qe) > eps) trip = 1;
           }
-          if (fabs(ql - qe) > eps) trip = 1;
-        }
+      }
       mk[m] = trip;
     }
   /* step 3: rebuild marked elements from neighbour averages (Eq. (35), Q14) */
@@ -767,8 +789,15 @@ typedef void (*orc_rhs_fn)(const double *q, double *r, void *ctx);
 typedef void (*orc_post_fn)(double *q, void *ctx);
 
 /* One SSP-RK3 (Shu-Osher) step of q' = L(q), with the stage operator Lambda
- * (limiter, or identity when post == NULL) after every stage. */
+ * (limiter, or identity when post == NULL) after every stage; with post_last
+ * only (limiter_per_step, f3) after the last stage. */
+static void ssprk3_post(double *q, int64_t n, double dt, orc_rhs_fn rhs, orc_post_fn post, orc_post_fn post_last,
+                        void *ctx);
 void orc_ssprk3(double *q, int64_t n, double dt, orc_rhs_fn rhs, orc_post_fn post, void *ctx) {
+  ssprk3_post(q, n, dt, rhs, post, post, ctx);
+}
+static void ssprk3_post(double *q, int64_t n, double dt, orc_rhs_fn rhs, orc_post_fn post, orc_post_fn post_last,
+                        void *ctx) {
   double *q0 = (double *)malloc(sizeof(double) * n);
   double *r = (double *)malloc(sizeof(double) * n);
   memcpy(q0, q, sizeof(double) * n);
@@ -780,7 +809,7 @@ void orc_ssprk3(double *q, int64_t n, double dt, orc_rhs_fn rhs, orc_post_fn pos
   if (post) post(q, ctx);
   rhs(q, r, ctx);
   for (int64_t i = 0; i < n; ++i) q[i] = q0[i] / 3.0 + (2.0 / 3.0) * (q[i] + dt * r[i]); /* q^{n+1} */
-  if (post) post(q, ctx);
+  if (post_last) post_last(q, ctx);
   free(q0);
   free(r);
 }
@@ -821,7 +850,8 @@ int orc_run(const orc_config *cf, double *Q, int32_t max_steps, double t_end, do
   while (s < max_steps && *t < t_end) {
     double dt = orc_dt(cf, Q);
     if (dt > t_end - *t) dt = t_end - *t;
-    orc_ssprk3(Q, n, dt, run_rhs, use_lim ? run_post : NULL, &ctx);
+    ssprk3_post(Q, n, dt, run_rhs, use_lim && !cf->limiter_per_step ? run_post : NULL, use_lim ? run_post : NULL,
+                &ctx);
     *t += dt;
     ++s;
     if (first_nonphysical(cf, Q) >= 0) { if (steps) *steps = s; return ORC_ERR_NONPHYSICAL; }

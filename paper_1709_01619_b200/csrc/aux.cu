@@ -104,12 +104,14 @@ __global__ void k_lambda(const AuxArgs A, const double* __restrict__ q, long lon
 }
 
 // clock: [0] t, [1] dt, [2] steps, [3] stepped flag;  lam: [0] accumulator, [1] current
-__global__ void k_dt(double* clk, unsigned long long* lam, double cfl, double hmin, double t_end) {
+// clk = {t, dt, steps, stepped, t_end}: t_end comes from device memory so that a
+// captured CUDA graph of steps does not depend on it
+__global__ void k_dt(double* clk, unsigned long long* lam, double cfl, double hmin) {
   if (clk[3] != 0.0) lam[1] = lam[0];
   lam[0] = 0ull;
   const double l = __longlong_as_double((long long)lam[1]);
   double dt = cfl * hmin / l;
-  const double rem = t_end - clk[0];
+  const double rem = clk[4] - clk[0];
   if (!(rem > 0.0)) dt = 0.0;
   else if (dt > rem) dt = rem;
   clk[1] = dt;
@@ -233,7 +235,7 @@ __global__ void k_avg(const AuxArgs A, Nodes nd, const double* __restrict__ q, d
 // index division): detect on density at every edge point (Alg. 10: all 4N edge
 // values evaluated, straight-line), limit all four components if marked (Alg. 11,
 // Eq. (35) in 2-D)
-template <int N, bool GLLP>
+template <int N, bool GLLP, bool ALL>
 __device__ __forceinline__ void limit_element(const AuxArgs& A, const Nodes& nd, double* q,
                                               const double* __restrict__ qbar, const double* qbar_lo,
                                               const double* qbar_hi, long long gcs, int bcx, double eps,
@@ -257,35 +259,43 @@ __device__ __forceinline__ void limit_element(const AuxArgs& A, const Nodes& nd,
   const double qb = qbar[m];
   double rW, rE, rS, rN;
   nbr(0, qb, rW, rE, rS, rN);
-  double r[NP];
-  const double* Q0 = q + m * NP;
-#pragma unroll
-  for (int p = 0; p < NP; ++p) r[p] = Q0[p];
   bool trip = false;
 #pragma unroll
-  for (int t = 0; t < N; ++t) {
-    double qw, qe_, qs, qn;
-    if (GLLP) {  // GLL edge nodes are solution points
-      qw = r[t * N];
-      qe_ = r[t * N + N - 1];
-      qs = r[t];
-      qn = r[(N - 1) * N + t];
-    } else {     // GL: interpolated traces of row t / column t
-      qw = qe_ = qs = qn = 0.0;
-#pragma unroll
-      for (int l = 0; l < N; ++l) {
-        qw += nd.eL[l] * r[t * N + l];
-        qe_ += nd.eR[l] * r[t * N + l];
-        qs += nd.eL[l] * r[l * N + t];
-        qn += nd.eR[l] * r[l * N + t];
-      }
+  for (int c = 0; c < (ALL ? 4 : 1); ++c) {  // density (Q12); ALL: every conserved component (f3)
+    double cb = qb, cW = rW, cE = rE, cS = rS, cN = rN;
+    if (c > 0) {
+      cb = qbar[c * ne + m];
+      nbr(c, cb, cW, cE, cS, cN);
     }
-    // right/top side: q_e = qbar + mm(q_l - qbar, ...); left/bottom: qbar - mm(qbar - q_l, ...)
-    const double ew = qb - minmod3(qb - qw, rE - qb, qb - rW);
-    const double ee = qb + minmod3(qe_ - qb, rE - qb, qb - rW);
-    const double es = qb - minmod3(qb - qs, rN - qb, qb - rS);
-    const double en = qb + minmod3(qn - qb, rN - qb, qb - rS);
-    trip |= (fabs(qw - ew) > eps) | (fabs(qe_ - ee) > eps) | (fabs(qs - es) > eps) | (fabs(qn - en) > eps);
+    double r[NP];
+    const double* Qc = q + c * A.cs + m * NP;
+#pragma unroll
+    for (int p = 0; p < NP; ++p) r[p] = Qc[p];
+#pragma unroll
+    for (int t = 0; t < N; ++t) {
+      double qw, qe_, qs, qn;
+      if (GLLP) {  // GLL edge nodes are solution points
+        qw = r[t * N];
+        qe_ = r[t * N + N - 1];
+        qs = r[t];
+        qn = r[(N - 1) * N + t];
+      } else {     // GL: interpolated traces of row t / column t
+        qw = qe_ = qs = qn = 0.0;
+#pragma unroll
+        for (int l = 0; l < N; ++l) {
+          qw += nd.eL[l] * r[t * N + l];
+          qe_ += nd.eR[l] * r[t * N + l];
+          qs += nd.eL[l] * r[l * N + t];
+          qn += nd.eR[l] * r[l * N + t];
+        }
+      }
+      // right/top side: q_e = qbar + mm(q_l - qbar, ...); left/bottom: qbar - mm(qbar - q_l, ...)
+      const double ew = cb - minmod3(cb - qw, cE - cb, cb - cW);
+      const double ee = cb + minmod3(qe_ - cb, cE - cb, cb - cW);
+      const double es = cb - minmod3(cb - qs, cN - cb, cb - cS);
+      const double en = cb + minmod3(qn - cb, cN - cb, cb - cS);
+      trip |= (fabs(qw - ew) > eps) | (fabs(qe_ - ee) > eps) | (fabs(qs - es) > eps) | (fabs(qn - en) > eps);
+    }
   }
   if (!trip) return;
   if (dec) atomicAdd((unsigned long long*)&dec[0], 1ull);
@@ -304,7 +314,7 @@ __device__ __forceinline__ void limit_element(const AuxArgs& A, const Nodes& nd,
   }
 }
 
-template <int N, bool GLLP>
+template <int N, bool GLLP, bool ALL>
 __global__ void __launch_bounds__(128) k_limit(const AuxArgs A, Nodes nd, double* q, const double* __restrict__ qbar,
                                                const double* qbar_lo, const double* qbar_hi, long long gcs, int bcx,
                                                double eps, long long* dec) {
@@ -312,7 +322,7 @@ __global__ void __launch_bounds__(128) k_limit(const AuxArgs A, Nodes nd, double
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= A.nx) return;
   for (int j = blockIdx.y; j < A.nrows; j += gridDim.y)
-    limit_element<N, GLLP>(A, nd, q, qbar, qbar_lo, qbar_hi, gcs, bcx, eps, dec, i, j);
+    limit_element<N, GLLP, ALL>(A, nd, q, qbar, qbar_lo, qbar_hi, gcs, bcx, eps, dec, i, j);
 }
 }  // namespace
 
@@ -322,8 +332,8 @@ void launch_lambda(const AuxArgs& a, const double* q, unsigned long long* lam, u
   k_lambda<<<grid_for(npts, 256), 256, 0, s>>>(a, q, npts, lam, bad);
 }
 
-void launch_dt(double* clock, unsigned long long* lam, double cfl, double hmin, double t_end, cudaStream_t s) {
-  k_dt<<<1, 1, 0, s>>>(clock, lam, cfl, hmin, t_end);
+void launch_dt(double* clock, unsigned long long* lam, double cfl, double hmin, cudaStream_t s) {
+  k_dt<<<1, 1, 0, s>>>(clock, lam, cfl, hmin);
 }
 
 void launch_init_case(const AuxArgs& a, int case_id, double* q, cudaStream_t s) {
@@ -347,27 +357,32 @@ void launch_averages(const AuxArgs& a, const double* q, double* qbar, cudaStream
   k_avg<<<grid_for(ne, 128), 128, 0, s>>>(a, nodes_for(a.method, a.k), q, qbar);
 }
 
-template <int N, bool GLLP>
+template <int N, bool GLLP, bool ALL>
 void launch_limit_t(const AuxArgs& a, double* q, const double* qbar, const double* qbar_lo, const double* qbar_hi,
                     long long qbar_gcs, int bcx, double eps, long long* dec, cudaStream_t s) {
   dim3 grid((a.nx + 127) / 128, a.nrows < 65535 ? a.nrows : 65535);
-  k_limit<N, GLLP><<<grid, 128, 0, s>>>(a, nodes_for(a.method, a.k), q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps,
-                                         dec);
+  k_limit<N, GLLP, ALL><<<grid, 128, 0, s>>>(a, nodes_for(a.method, a.k), q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx,
+                                              eps, dec);
+}
+
+template <int N>
+void launch_limit_n(const AuxArgs& a, double* q, const double* qbar, const double* qbar_lo, const double* qbar_hi,
+                    long long qbar_gcs, int bcx, double eps, int all_vars, long long* dec, cudaStream_t s) {
+  const bool gll = (a.method == 1 || a.method == 3);
+  if (gll && all_vars) launch_limit_t<N, true, true>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, dec, s);
+  else if (gll) launch_limit_t<N, true, false>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, dec, s);
+  else if (all_vars) launch_limit_t<N, false, true>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, dec, s);
+  else launch_limit_t<N, false, false>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, dec, s);
 }
 
 void launch_limit(const AuxArgs& a, double* q, const double* qbar, const double* qbar_lo, const double* qbar_hi,
-                  long long qbar_gcs, int bcx, double eps, long long* dec, cudaStream_t s) {
-  const bool gll = (a.method == 1 || a.method == 3);
-#define H2D_LIM(NN)                                                                                     \
-  return gll ? launch_limit_t<NN, true>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, dec, s)       \
-             : launch_limit_t<NN, false>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, dec, s)
+                  long long qbar_gcs, int bcx, double eps, int all_vars, long long* dec, cudaStream_t s) {
   switch (a.k) {
-    case 1: H2D_LIM(2);
-    case 2: H2D_LIM(3);
-    case 3: H2D_LIM(4);
-    default: H2D_LIM(5);
+    case 1: return launch_limit_n<2>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, all_vars, dec, s);
+    case 2: return launch_limit_n<3>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, all_vars, dec, s);
+    case 3: return launch_limit_n<4>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, all_vars, dec, s);
+    default: return launch_limit_n<5>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, all_vars, dec, s);
   }
-#undef H2D_LIM
 }
 
 }  // namespace h2d

@@ -34,7 +34,16 @@ __device__ __forceinline__ void cell_faces(double qm, double q0, double qp, doub
   // explicit rounding (no contraction freedom): a face state is bitwise the same
   // wherever it is evaluated (prologue or carried), so results do not depend on
   // how the rows are split over CTAs / launches / ranks
-  if (ORDER == 1) {
+  if (ORDER == 3) {  // unlimited kappa = 0 (f3 variant of MUSCL-2)
+    const double d = (q0 - qm) + (qp - q0);
+    hi = __fma_rn(0.25, d, q0);
+    lo = __fma_rn(-0.25, d, q0);
+  } else if (ORDER == 4) {  // unlimited kappa = 1/3 (f3 variant of MUSCL-3)
+    constexpr double kap = 1.0 / 3.0;
+    const double dm = q0 - qm, dp = qp - q0;
+    hi = __fma_rn(0.25, __fma_rn(1.0 - kap, dm, __dmul_rn(1.0 + kap, dp)), q0);
+    lo = __fma_rn(-0.25, __fma_rn(1.0 - kap, dp, __dmul_rn(1.0 + kap, dm)), q0);
+  } else if (ORDER == 1) {
     const double s = minmod2(q0 - qm, qp - q0, dec, w);
     hi = __fma_rn(0.5, s, q0);
     lo = __fma_rn(-0.5, s, q0);
@@ -266,12 +275,23 @@ int launch_fv_stage(int k, const StageArgs& a0, cudaStream_t s) {
   if (nr <= 0) return 0;
   a.rows = march_rows(nr, strips, FRB);
   dim3 grid(strips, (nr + a.rows - 1) / a.rows);
+  // reconstruction: 1 MUSCL-2, 2 MUSCL-3 (minmod-limited); 3 / 4 the same
+  // kappa-schemes unlimited (hom2d_config.fv_unlimited, f3)
+  const int rec = k + (a.fv_unlimited ? 2 : 0);
   if (a.dec) {
-    if (k == 1) fv_stage_kernel<1, true><<<grid, FTX, 0, s>>>(a);
-    else fv_stage_kernel<2, true><<<grid, FTX, 0, s>>>(a);
+    switch (rec) {
+      case 1: fv_stage_kernel<1, true><<<grid, FTX, 0, s>>>(a); break;
+      case 2: fv_stage_kernel<2, true><<<grid, FTX, 0, s>>>(a); break;
+      case 3: fv_stage_kernel<3, true><<<grid, FTX, 0, s>>>(a); break;
+      default: fv_stage_kernel<4, true><<<grid, FTX, 0, s>>>(a); break;
+    }
   } else {
-    if (k == 1) fv_stage_kernel<1, false><<<grid, FTX, 0, s>>>(a);
-    else fv_stage_kernel<2, false><<<grid, FTX, 0, s>>>(a);
+    switch (rec) {
+      case 1: fv_stage_kernel<1, false><<<grid, FTX, 0, s>>>(a); break;
+      case 2: fv_stage_kernel<2, false><<<grid, FTX, 0, s>>>(a); break;
+      case 3: fv_stage_kernel<3, false><<<grid, FTX, 0, s>>>(a); break;
+      default: fv_stage_kernel<4, false><<<grid, FTX, 0, s>>>(a); break;
+    }
   }
   return (int)cudaPeekAtLastError();
 }

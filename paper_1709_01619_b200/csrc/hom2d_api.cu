@@ -4,6 +4,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -21,6 +22,12 @@ struct hom2d {
   cudaStream_t stream = nullptr;
   cudaStream_t xstream = nullptr;          // nranks > 1: halo exchange stream (highest priority)
   cudaEvent_t ev_in = nullptr, ev_halo = nullptr;
+  // CUDA graphs of 2^i steps (single GPU, untimed): launch-bound small grids
+  cudaStream_t gstream = nullptr;
+  cudaEvent_t gev_a = nullptr, gev_b = nullptr;
+  cudaGraphExec_t gexec[7] = {};
+  long long glaunch[7] = {};
+  bool graph_off = false;
   ncclComm_t comm = nullptr;
   int row0 = 0, nrows = 0, np = 1, G = 1;  // G ghost rows (HO 1, FV 2)
   long long nloc = 0;                      // values per component of the local strip
@@ -85,6 +92,8 @@ hom2d_status check_cfg(const hom2d_config* c, int nranks) {
   const int G = c->method == HOM2D_FV ? 2 : 1;
   if (c->ny / nranks < G) return HOM2D_ERR_MESH;
   if (!(c->gamma > 1.0) || !(c->cfl > 0.0)) return HOM2D_ERR_ARG;
+  if ((unsigned)c->limiter_per_step > 1u || (unsigned)c->limiter_all_vars > 1u || (unsigned)c->fv_unlimited > 1u)
+    return HOM2D_ERR_ARG;
   return HOM2D_OK;
 }
 
@@ -237,6 +246,7 @@ hom2d_status run_stage(hom2d* h, const double* q, const double* q0, double* out,
   s.dec = h->cfg.record_decisions ? h->dec : nullptr;
   s.count_bot = (h->rank == 0);
   s.qbar = qbar;
+  s.fv_unlimited = h->cfg.fv_unlimited;
   int e = 0;
   if (!split) {
     s.row_lo = 0; s.row_hi = h->nrows;
@@ -274,7 +284,7 @@ hom2d_status run_limiter(hom2d* h, double* X, const double* dt = nullptr, bool a
   long long gcs;
   hom2d_status st = exchange(h, h->qbar, ne, h->cfg.nx, &lo, &hi, &gcs, h->qblo, h->qbhi, 1, h->stream);
   if (st) return st;
-  launch_limit(A, X, h->qbar, lo, hi, gcs, h->cfg.bc, h->cfg.limiter_eps,
+  launch_limit(A, X, h->qbar, lo, hi, gcs, h->cfg.bc, h->cfg.limiter_eps, h->cfg.limiter_all_vars,
                h->cfg.record_decisions ? h->dec : nullptr, h->stream);
   h->launches++;
   CU(h, cudaPeekAtLastError());
@@ -360,6 +370,10 @@ hom2d_status hom2d_create(const hom2d_config* cfg, const hom2d_dist* dist, void*
   h->nrows = cfg->ny / R;
   h->row0 = h->rank * h->nrows;
   h->nloc = (long long)cfg->nx * h->nrows * h->np;
+  {
+    const char* ng = getenv("HOM2D_NO_GRAPH");  // A/B: eager launches instead of CUDA graphs
+    h->graph_off = ng && ng[0] == '1';
+  }
   cudaError_t ce = cudaSetDevice(h->device);
   if (ce != cudaSuccess) { delete h; return HOM2D_ERR_CUDA; }
   carve(h, *cfg, R, (char*)workspace);
@@ -492,40 +506,102 @@ hom2d_status hom2d_compute_dt(hom2d* h, double* dt) {
   return HOM2D_OK;
 }
 
-hom2d_status hom2d_step(hom2d* h, int32_t max_steps, double t_end, double* t_out, int64_t* steps_out) {
+}  // extern "C"
+
+namespace {
+
+// one SSP-RK3 step on h->stream: dt (device), three stages, the
+// limiter (if on) and the lambda allreduce (nranks > 1)
+hom2d_status enqueue_step(hom2d* h) {
+  const double dx = (h->cfg.xmax - h->cfg.xmin) / h->cfg.nx, dy = (h->cfg.ymax - h->cfg.ymin) / h->cfg.ny;
+  const bool lim = h->cfg.limiter && h->cfg.method != HOM2D_FV;
+  hom2d_status st;
+  launch_dt(h->clock, h->lam, h->cfg.cfl, fmin(dx, dy), h->stream);
+  h->launches++;
+  const double* dt = h->clock + 1;
+  // limiter runs: the stage kernels also write the element averages of their output;
+  // limiter_per_step (f3): only after stage 3
+  const bool lim12 = lim && !h->cfg.limiter_per_step;
+  double* qb = lim ? h->qbar : nullptr;
+  double* qb12 = lim12 ? h->qbar : nullptr;
+  if ((st = run_stage(h, h->Qn, nullptr, h->Q1, 0.0, 1.0, 1.0, dt, nullptr, nullptr, qb12))) return st;
+  if (lim12 && (st = run_limiter(h, h->Q1, dt, true))) return st;
+  if ((st = run_stage(h, h->Q1, h->Qn, h->Q2, 0.75, 0.25, 0.25, dt, nullptr, nullptr, qb12))) return st;
+  if (lim12 && (st = run_limiter(h, h->Q2, dt, true))) return st;
+  if (!lim) {
+    if ((st = run_stage(h, h->Q2, h->Qn, h->Qn, 1.0 / 3.0, 2.0 / 3.0, 2.0 / 3.0, dt, h->lam, h->bad))) return st;
+  } else {
+    if ((st = run_stage(h, h->Q2, h->Qn, h->Qn, 1.0 / 3.0, 2.0 / 3.0, 2.0 / 3.0, dt, nullptr, nullptr, qb))) return st;
+    if ((st = run_limiter(h, h->Qn, dt, true))) return st;
+    launch_lambda(aux(h), h->Qn, h->lam, h->bad, h->stream);  // dt of the limited state
+    h->launches++;
+  }
+  return allreduce_max_lam(h);
+}
+
+// n steps through cached CUDA graphs of 2^i steps (binary decomposition of n)
+hom2d_status graph_steps(hom2d* h, int n) {
+  if (!h->gstream) {
+    CU(h, cudaStreamCreateWithFlags(&h->gstream, cudaStreamNonBlocking));
+    CU(h, cudaEventCreateWithFlags(&h->gev_a, cudaEventDisableTiming));
+    CU(h, cudaEventCreateWithFlags(&h->gev_b, cudaEventDisableTiming));
+  }
+  CU(h, cudaEventRecord(h->gev_a, h->stream));
+  CU(h, cudaStreamWaitEvent(h->gstream, h->gev_a, 0));
+  for (int i = 6; i >= 0; --i) {
+    if (!(n & (1 << i))) continue;
+    if (!h->gexec[i]) {  // capture 2^i steps once
+      cudaStream_t user = h->stream;
+      const long long l0 = h->launches;
+      h->stream = h->gstream;
+      CU(h, cudaStreamBeginCapture(h->gstream, cudaStreamCaptureModeThreadLocal));
+      hom2d_status st = HOM2D_OK;
+      for (int k = 0; k < (1 << i) && !st; ++k) st = enqueue_step(h);
+      cudaGraph_t g = nullptr;
+      const cudaError_t ce = cudaStreamEndCapture(h->gstream, &g);
+      h->stream = user;
+      h->glaunch[i] = h->launches - l0;
+      h->launches = l0;
+      if (st) { if (g) cudaGraphDestroy(g); return st; }
+      CU(h, ce);
+      const cudaError_t ie = cudaGraphInstantiate(&h->gexec[i], g, 0);
+      cudaGraphDestroy(g);
+      CU(h, ie);
+    }
+    CU(h, cudaGraphLaunch(h->gexec[i], h->gstream));
+    h->launches += h->glaunch[i];
+  }
+  CU(h, cudaEventRecord(h->gev_b, h->gstream));
+  CU(h, cudaStreamWaitEvent(h->stream, h->gev_b, 0));
+  return HOM2D_OK;
+}
+
+}  // namespace
+
+extern "C" hom2d_status hom2d_step(hom2d* h, int32_t max_steps, double t_end, double* t_out, int64_t* steps_out) {
   GUARD(h);
   if (max_steps < 0) return fail(h, HOM2D_ERR_ARG, "max_steps < 0");
-  const double dx = (h->cfg.xmax - h->cfg.xmin) / h->cfg.nx, dy = (h->cfg.ymax - h->cfg.ymin) / h->cfg.ny;
-  const double hmin = fmin(dx, dy);
-  const bool lim = h->cfg.limiter && h->cfg.method != HOM2D_FV;
+  // graphs: single GPU (NCCL calls stay eagerly enqueued), no per-stage timing events
+  const bool graphs = !h->graph_off && !h->comm && h->ev.empty();
+  h->t_host[5] = t_end;
+  CU(h, cudaMemcpyAsync(h->clock + 4, h->t_host + 5, sizeof(double), cudaMemcpyHostToDevice, h->stream));
   CU(h, cudaMemcpyAsync(h->t_host, h->clock, 4 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
   CU(h, cudaStreamSynchronize(h->stream));
   const double steps0 = h->t_host[2];
   int done = 0;
   hom2d_status st = HOM2D_OK;
   while (done < max_steps) {
-    const int batch = (max_steps - done) < 64 ? (max_steps - done) : 64;
-    for (int s = 0; s < batch; ++s) {
-      launch_dt(h->clock, h->lam, h->cfg.cfl, hmin, t_end, h->stream);
-      h->launches++;
-      const double* dt = h->clock + 1;
-      // SSP-RK3 (Shu-Osher)
-      // limiter runs: the stage kernels also write the element averages of their output
-      double* qb = lim ? h->qbar : nullptr;
-      if ((st = run_stage(h, h->Qn, nullptr, h->Q1, 0.0, 1.0, 1.0, dt, nullptr, nullptr, qb))) return st;
-      if (lim && (st = run_limiter(h, h->Q1, dt, true))) return st;
-      if ((st = run_stage(h, h->Q1, h->Qn, h->Q2, 0.75, 0.25, 0.25, dt, nullptr, nullptr, qb))) return st;
-      if (lim && (st = run_limiter(h, h->Q2, dt, true))) return st;
-      if (!lim) {
-        if ((st = run_stage(h, h->Q2, h->Qn, h->Qn, 1.0 / 3.0, 2.0 / 3.0, 2.0 / 3.0, dt, h->lam, h->bad))) return st;
-      } else {
-        if ((st = run_stage(h, h->Q2, h->Qn, h->Qn, 1.0 / 3.0, 2.0 / 3.0, 2.0 / 3.0, dt, nullptr, nullptr, qb)))
-          return st;
-        if ((st = run_limiter(h, h->Qn, dt, true))) return st;
-        launch_lambda(aux(h), h->Qn, h->lam, h->bad, h->stream);  // dt of the limited state
-        h->launches++;
-      }
-      if ((st = allreduce_max_lam(h))) return st;
+    int batch = (max_steps - done) < 64 ? (max_steps - done) : 64;
+    // near t_end: no more steps than the clock needs (+1; clipped-out steps are no-ops)
+    if (std::isfinite(t_end) && h->t_host[1] > 0.0) {
+      const double est = std::ceil((t_end - h->t_host[0]) / h->t_host[1]) + 1.0;
+      if (est < batch) batch = est < 1.0 ? 1 : (int)est;
+    }
+    if (graphs) {
+      if ((st = graph_steps(h, batch))) return st;
+    } else {
+      for (int s = 0; s < batch; ++s)
+        if ((st = enqueue_step(h))) return st;
     }
     done += batch;
     CU(h, cudaPeekAtLastError());
@@ -547,6 +623,8 @@ hom2d_status hom2d_step(hom2d* h, int32_t max_steps, double t_end, double* t_out
   if (steps_out) *steps_out = (int64_t)(h->t_host[2] - steps0);
   return HOM2D_OK;
 }
+
+extern "C" {
 
 hom2d_status hom2d_error(hom2d* h, int32_t case_id, int32_t var, double* l1, double* l2, double* linf) {
   GUARD(h);
@@ -632,6 +710,12 @@ void hom2d_destroy(hom2d* h) {
   if (h->stream) cudaStreamSynchronize(h->stream); else cudaDeviceSynchronize();
   for (cudaEvent_t e : h->ev) cudaEventDestroy(e);
   if (h->xstream) cudaStreamSynchronize(h->xstream);
+  if (h->gstream) cudaStreamSynchronize(h->gstream);
+  for (cudaGraphExec_t& g : h->gexec)
+    if (g) cudaGraphExecDestroy(g);
+  if (h->gev_a) cudaEventDestroy(h->gev_a);
+  if (h->gev_b) cudaEventDestroy(h->gev_b);
+  if (h->gstream) cudaStreamDestroy(h->gstream);
   if (h->comm) ncclCommDestroy(h->comm);
   if (h->ev_in) cudaEventDestroy(h->ev_in);
   if (h->ev_halo) cudaEventDestroy(h->ev_halo);

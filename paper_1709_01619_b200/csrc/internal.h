@@ -31,6 +31,7 @@ struct StageArgs {
   int count_bot;           // this strip owns the domain's bottom face row (decision counting)
   double* qbar;            // optional (HO limiter runs): element averages of `out`, [4][nx*nrows]
                            // (Alg. 9: 1/4 sum_ab w_a w_b q_ab), fused into the stage epilogue
+  int fv_unlimited;        // FV: unlimited kappa-scheme (hom2d_config.fv_unlimited)
   int row_lo, row_hi;      // this launch updates strip rows [row_lo, row_hi) (row_hi == 0: all rows);
                           // it may read rows row_lo-G .. row_hi+G-1 (ghost rows outside the strip)
   int rows;                // marching kernels: element rows per CTA (set by the launcher)
@@ -66,7 +67,8 @@ struct AuxArgs {
 void launch_lambda(const AuxArgs& a, const double* q, unsigned long long* lam, unsigned long long* bad,
                    cudaStream_t s);
 // dt bookkeeping: see aux.cu
-void launch_dt(double* clock, unsigned long long* lam_acc, double cfl, double hmin, double t_end, cudaStream_t s);
+// clock = {t, dt, steps, stepped, t_end} (device): one step's dt, clipped to t_end - t
+void launch_dt(double* clock, unsigned long long* lam_acc, double cfl, double hmin, cudaStream_t s);
 void launch_init_case(const AuxArgs& a, int case_id, double* q, cudaStream_t s);
 // per-block partial sums {sum w|d|, sum w d^2, max|d|} -> part[3*nblocks]; returns nblocks
 int launch_error_partials(const AuxArgs& a, const double* q, int var, const double* clock, double* part,
@@ -75,6 +77,6 @@ void launch_error_final(const double* part, int nblocks, double* out3, cudaStrea
 // averages Qbar[4][nx*nrows] and the detect+limit pass (HO)
 void launch_averages(const AuxArgs& a, const double* q, double* qbar, cudaStream_t s);
 void launch_limit(const AuxArgs& a, double* q, const double* qbar, const double* qbar_lo, const double* qbar_hi,
-                  long long qbar_gcs, int bcx, double eps, long long* dec, cudaStream_t s);
+                  long long qbar_gcs, int bcx, double eps, int all_vars, long long* dec, cudaStream_t s);
 
 }  // namespace h2d
