@@ -149,9 +149,10 @@ hom2d_status hom2d_compute_dt(hom2d* h, double* dt);
 /* March with SSP-RK3 until *steps_out == max_steps or t == t_end (last dt
  * clipped).  dt is recomputed from the state every step.  Syncs the host once
  * per batch of up to 64 steps.  Returns HOM2D_ERR_NONPHYSICAL if a bad state
- * appeared.  Single GPU: batches replay cached CUDA graphs of 2^i steps (captured
- * on first use on an internal stream, fenced to the handle's stream by events;
- * environment HOM2D_NO_GRAPH=1 or per-stage timing switch to eager launches). */
+ * appeared.  Single GPU, long runs (after 256 eager steps on the handle): full
+ * 64-step batches replay a cached CUDA graph (captured once on an internal
+ * stream, fenced to the handle's stream by events; environment HOM2D_NO_GRAPH=1
+ * or per-stage timing keep eager launches). */
 hom2d_status hom2d_step(hom2d* h, int32_t max_steps, double t_end, double* t_out, int64_t* steps_out);
 
 /* Error of component var (0..3) against the exact vortex at the current t

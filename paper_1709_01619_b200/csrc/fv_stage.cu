@@ -264,7 +264,7 @@ int march_rows(int nrows, int strips, int rb_max) {
   const long long target = 4LL * nsm;
   long long rows = ((long long)nrows * strips + target - 1) / target;
   if (rows > rb_max) rows = rb_max;
-  if (rows < 4) rows = 4;
+  if (rows < 1) rows = 1;  // small grids: short marches, more CTAs (latency-bound sizes)
   return (int)rows;
 }
 

@@ -314,16 +314,19 @@ __global__ void __launch_bounds__(L<M, K>::NT, LTile<M, K>::MINB) gl_stage_kerne
       return v.st[c * CREG + CW + (v.dM ^ (c & v.csodd)) + (e - 1) * NP + p];
     }
   };
+  // value (c, p) of any slot e (0 W halo, TXv+1 E halo): the index is selected,
+  // not branched on (no divergent regions in the face work)
   auto any_at = [&](const RowView& v, int c, int e, int p) -> double {
     if constexpr (H::SWZ) {
-      const double* fix = v.st + H::FIXO;
-      if (e == 0 && wrapW) return fix[(0 * 4 + c) * 16 + p];
-      if (e == TXv + 1 && wrapE) return fix[(1 * 4 + c) * 16 + p];
-      return own_at(v, c, e, p);
+      const bool fw = (e == 0 && wrapW), fe = (e == TXv + 1 && wrapE);
+      const int iS = (c * H::RSW + e) * 16 + ((((p >> 1) ^ (e & 7)) << 1) | (p & 1));
+      const int iF = H::FIXO + ((fe ? 4 : 0) + c) * 16 + p;
+      return v.st[(fw || fe) ? iF : iS];
     } else {
-      if (e == 0) return v.st[c * CREG + (v.dW ^ (c & v.csodd)) + p];
-      if (e == TXv + 1) return v.st[c * CREG + CW + CM + (v.dE ^ (c & v.csodd)) + p];
-      return own_at(v, c, e, p);
+      const int iW = c * CREG + (v.dW ^ (c & v.csodd)) + p;
+      const int iE = c * CREG + CW + CM + (v.dE ^ (c & v.csodd)) + p;
+      const int iM = c * CREG + CW + (v.dM ^ (c & v.csodd)) + (e - 1) * NP + p;
+      return v.st[e == 0 ? iW : (e == TXv + 1 ? iE : iM)];
     }
   };
   // interpolation of a line (dir 0: row bb of slot e) or column (dir 1: column bb)

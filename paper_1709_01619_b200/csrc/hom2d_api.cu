@@ -21,6 +21,7 @@ struct hom2d {
   int rank = 0, nranks = 1, device = 0;
   cudaStream_t stream = nullptr;
   cudaStream_t xstream = nullptr;          // nranks > 1: halo exchange stream (highest priority)
+  bool self_x = false;                     // HOM2D_SELF_EXCHANGE test mode (see self_exchange_env)
   cudaEvent_t ev_in = nullptr, ev_halo = nullptr;
   // CUDA graphs of 2^i steps (single GPU, untimed): launch-bound small grids
   cudaStream_t gstream = nullptr;
@@ -28,6 +29,7 @@ struct hom2d {
   cudaGraphExec_t gexec[7] = {};
   long long glaunch[7] = {};
   bool graph_off = false;
+  long long eager_steps = 0;
   ncclComm_t comm = nullptr;
   int row0 = 0, nrows = 0, np = 1, G = 1;  // G ghost rows (HO 1, FV 2)
   long long nloc = 0;                      // values per component of the local strip
@@ -83,6 +85,15 @@ hom2d_status fail(hom2d* h, hom2d_status st, const char* fmt, ...) {
 
 int points_per_elem(const hom2d_config& c) { return c.method == HOM2D_FV ? 1 : (c.k + 1) * (c.k + 1); }
 
+// Test mode (HOM2D_SELF_EXCHANGE=1, one rank, periodic): the overlapped multi-GPU
+// stage path -- exchange stream, events, interior / boundary launches, ghost
+// buffers -- with the NCCL send/recv replaced by device copies of the strip's own
+// wrap rows, so the stream plumbing is exercised (bitwise) on one GPU.
+bool self_exchange_env(const hom2d_config& c, int nranks) {
+  const char* v = getenv("HOM2D_SELF_EXCHANGE");
+  return nranks == 1 && c.bc == HOM2D_PERIODIC && v && v[0] == '1';
+}
+
 hom2d_status check_cfg(const hom2d_config* c, int nranks) {
   if (!c) return HOM2D_ERR_ARG;
   if (c->method < 0 || c->method > 4 || (c->bc != 0 && c->bc != 1)) return HOM2D_ERR_ARG;
@@ -128,7 +139,7 @@ size_t carve(hom2d* h, const hom2d_config& c, int nranks, char* base) {
   double* err3 = cv.take<double>(4);
   double* qbar = (c.method != HOM2D_FV) ? cv.take<double>(4 * (size_t)c.nx * nrows) : nullptr;
   double *glo = nullptr, *ghi = nullptr, *qblo = nullptr, *qbhi = nullptr;
-  if (nranks > 1) {
+  if (nranks > 1 || self_exchange_env(c, nranks)) {
     glo = cv.take<double>(4 * (size_t)G * c.nx * np);
     ghi = cv.take<double>(4 * (size_t)G * c.nx * np);
     if (c.method != HOM2D_FV) {
@@ -179,6 +190,18 @@ hom2d_status exchange(hom2d* h, const double* X, long long comp_stride, long lon
     *hi = h->ovr_hi;
     return HOM2D_OK;
   }
+  if (R == 1 && h->self_x) {  // test mode: the periodic wrap rows through the ghost buffers, on xs
+    const long long cnt = (long long)G * row_vals;
+    for (int c = 0; c < 4; ++c) {
+      CU(h, cudaMemcpyAsync(rlo + c * cnt, X + c * comp_stride + (long long)(h->nrows - G) * row_vals,
+                            cnt * sizeof(double), cudaMemcpyDeviceToDevice, xs));
+      CU(h, cudaMemcpyAsync(rhi + c * cnt, X + c * comp_stride, cnt * sizeof(double), cudaMemcpyDeviceToDevice, xs));
+    }
+    *gcs = cnt;
+    *lo = rlo;
+    *hi = rhi;
+    return HOM2D_OK;
+  }
   if (R == 1) {
     *gcs = comp_stride;
     *lo = (h->cfg.bc == HOM2D_PERIODIC) ? X + (long long)(h->nrows - G) * row_vals : nullptr;
@@ -224,8 +247,8 @@ hom2d_status run_stage(hom2d* h, const double* q, const double* q0, double* out,
   StageArgs s{};
   const long long row_vals = (long long)h->cfg.nx * h->np;
   const int G = h->G;
-  const bool split = h->nranks > 1 && h->nrows > 2 * G;
-  const bool async = split && h->comm && !h->ovr_active;
+  const bool split = (h->nranks > 1 || h->self_x) && h->nrows > 2 * G;
+  const bool async = split && (h->comm || h->self_x) && !h->ovr_active;
   const bool timed = 2 * (h->ev_used + 1) <= (int)h->ev.size();
   if (timed) cudaEventRecord(h->ev[2 * h->ev_used], h->stream);
   if (async) {  // the exchange stream may read q only once its producer has finished
@@ -378,10 +401,17 @@ hom2d_status hom2d_create(const hom2d_config* cfg, const hom2d_dist* dist, void*
   if (ce != cudaSuccess) { delete h; return HOM2D_ERR_CUDA; }
   carve(h, *cfg, R, (char*)workspace);
   if (cudaMallocHost(&h->t_host, 8 * sizeof(double)) != cudaSuccess) { delete h; return HOM2D_ERR_CUDA; }
-  if (R > 1 && dist->nccl_id) {  // (no id: strip-only handle, see hom2d_residual_strip)
-    ncclUniqueId id;
-    memcpy(&id, dist->nccl_id, sizeof(id));
-    if (ncclCommInitRank(&h->comm, R, id, h->rank) != ncclSuccess) { cudaFreeHost(h->t_host); delete h; return HOM2D_ERR_NCCL; }
+  h->self_x = self_exchange_env(*cfg, R);
+  if ((R > 1 && dist->nccl_id) || h->self_x) {  // (no id: strip-only handle, see hom2d_residual_strip)
+    if (R > 1) {
+      ncclUniqueId id;
+      memcpy(&id, dist->nccl_id, sizeof(id));
+      if (ncclCommInitRank(&h->comm, R, id, h->rank) != ncclSuccess) {
+        cudaFreeHost(h->t_host);
+        delete h;
+        return HOM2D_ERR_NCCL;
+      }
+    }
     int prio_lo = 0, prio_hi = 0;
     cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
     if (cudaStreamCreateWithPriority(&h->xstream, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
@@ -582,7 +612,7 @@ extern "C" hom2d_status hom2d_step(hom2d* h, int32_t max_steps, double t_end, do
   GUARD(h);
   if (max_steps < 0) return fail(h, HOM2D_ERR_ARG, "max_steps < 0");
   // graphs: single GPU (NCCL calls stay eagerly enqueued), no per-stage timing events
-  const bool graphs = !h->graph_off && !h->comm && h->ev.empty();
+  const bool graphs = !h->graph_off && !h->comm && !h->self_x && h->ev.empty();
   h->t_host[5] = t_end;
   CU(h, cudaMemcpyAsync(h->clock + 4, h->t_host + 5, sizeof(double), cudaMemcpyHostToDevice, h->stream));
   CU(h, cudaMemcpyAsync(h->t_host, h->clock, 4 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
@@ -597,11 +627,14 @@ extern "C" hom2d_status hom2d_step(hom2d* h, int32_t max_steps, double t_end, do
       const double est = std::ceil((t_end - h->t_host[0]) / h->t_host[1]) + 1.0;
       if (est < batch) batch = est < 1.0 ? 1 : (int)est;
     }
-    if (graphs) {
+    // graphs pay for their capture only on long runs: full 64-step batches once the
+    // handle has marched 256 steps eagerly
+    if (graphs && batch == 64 && h->eager_steps >= 256) {
       if ((st = graph_steps(h, batch))) return st;
     } else {
       for (int s = 0; s < batch; ++s)
         if ((st = enqueue_step(h))) return st;
+      h->eager_steps += batch;
     }
     done += batch;
     CU(h, cudaPeekAtLastError());

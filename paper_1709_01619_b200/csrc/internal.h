@@ -44,7 +44,8 @@ inline int row_range(StageArgs& a) {
 }
 
 // rows per CTA for a marching kernel: enough CTAs to fill the GPU (>= 4 per SM),
-// at most rb_max, at least 4 (the march costs 1-2 prologue rows)
+// at most rb_max (each march re-reads 1-2 prologue rows: long marches on big
+// grids, short ones -- down to 1 row -- on the latency-bound small grids)
 int march_rows(int nrows, int strips, int rb_max);
 
 // host: 3-D TMA tensor map {16 points, nelem elements, 4 components} (fp64,

@@ -61,3 +61,24 @@ def test_strips_bitwise(orc, P, method, k, G, bc, thin):
         s.close()
     np.testing.assert_array_equal(np.concatenate(parts, axis=1), r_glob)
     whole.close()
+
+
+@pytest.mark.parametrize("method,k,limiter", [("cpr", 3, 0), ("ndg", 4, 0), ("dg", 2, 0), ("sd", 1, 0),
+                                              ("fv", 1, 0), ("fv", 2, 0), ("cpr", 1, 1), ("dg", 1, 1)])
+def test_overlapped_stage_path_bitwise(P, monkeypatch, method, k, limiter):
+    """The multi-GPU stage path on one GPU (HOM2D_SELF_EXCHANGE=1): the periodic
+    wrap rows go through the ghost buffers on the high-priority exchange stream
+    while the interior rows run, the boundary bands wait on its event, and the
+    limiter's average rows take the same route.  30 steps (90 stages) must equal
+    the single-launch path bitwise; the exchange stream's copies racing a kernel
+    that writes its source or the ghost buffers would break this."""
+    out = []
+    for sx in ("0", "1"):
+        monkeypatch.setenv("HOM2D_SELF_EXCHANGE", sx)
+        cfg = P.make_config(23, 14, method=method, k=k, cfl=0.05, limiter=limiter)
+        s = P.Solver(cfg)
+        s.init_case(P.VORTEX)
+        s.step(30)
+        out.append(s.get_state())
+        s.close()
+    np.testing.assert_array_equal(out[0], out[1])

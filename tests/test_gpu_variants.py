@@ -79,9 +79,9 @@ def test_shock_limiter_variants(orc, P, method, k, cfl, variant):
 
 @pytest.mark.parametrize("method,k,limiter", [("cpr", 3, 0), ("dg", 2, 0), ("fv", 1, 0), ("sd", 1, 1)])
 def test_graph_replay_bitwise_equals_eager(orc, P, monkeypatch, method, k, limiter):
-    """hom2d_step replays cached CUDA graphs of 2^i steps on one GPU; the state,
-    t and step count equal the eager launch sequence bitwise, including the
-    t_end-clipped last batch."""
+    """hom2d_step replays a cached 64-step CUDA graph on long single-GPU runs; the
+    state, t and step count equal the eager launch sequence bitwise, including
+    the t_end-clipped last batch."""
     box, bc, case, cfl = ((-1.0, 1.0, -1.0, 1.0), 1, P.SHOCK, 0.2) if limiter else ((-5.0, 5.0, -5.0, 5.0), 0,
                                                                                    P.VORTEX, 0.08)
     out = []
@@ -89,8 +89,8 @@ def test_graph_replay_bitwise_equals_eager(orc, P, monkeypatch, method, k, limit
         monkeypatch.setenv("HOM2D_NO_GRAPH", no_graph)
         s = P.Solver(P.make_config(20, 16, method=method, k=k, bc=bc, box=box, cfl=cfl, limiter=limiter))
         s.init_case(case)
-        t1, n1 = s.step(37)                      # 32 + 4 + 1
-        t2, n2 = s.step(10 ** 6, t1 + 0.05)      # clipped at t_end
+        t1, n1 = s.step(400)                     # 256 eager steps, 2 graph batches, 16 eager
+        t2, n2 = s.step(10 ** 6, t1 + 0.3)       # clipped at t_end
         out.append((s.get_state(), t1, n1, t2, n2, s.launch_count()))
         s.close()
     (qa, *ra), (qb, *rb) = out
