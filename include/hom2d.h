@@ -81,6 +81,9 @@ typedef struct {
                                  density only (Alg. 10 P:802-836 names no variable; Q12) */
   int32_t fv_unlimited;       /* FV: 1 = unlimited kappa-scheme (kappa = 0 for k = 1, 1/3 for k = 2),
                                  i.e. MUSCL without the minmod of P:346-351 (Q10) */
+  int32_t limiter_characteristic; /* HO: 1 = the Eq. (35) slopes limited per characteristic
+                                 field of the element average (Cockburn-Shu) instead of per
+                                 conserved component (Q12) */
 } hom2d_config;
 
 typedef struct {

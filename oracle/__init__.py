@@ -37,6 +37,7 @@ class OrcConfig(C.Structure):
         ("physics", C.c_int32), ("adv_a", C.c_double), ("adv_b", C.c_double),
         ("dt_fixed", C.c_double),
         ("limiter_per_step", C.c_int32), ("limiter_all_vars", C.c_int32), ("fv_unlimited", C.c_int32),
+        ("limiter_characteristic", C.c_int32),
     ]
 
 
@@ -78,6 +79,7 @@ def lib():
         L.orc_minmod3.restype = d
         L.orc_muscl_face.argtypes = [C.c_int, vp, vp, vp, vp, vp, vp]
         L.orc_muscl_face_unlimited.argtypes = [C.c_int, vp, vp, vp, vp, vp, vp]
+        L.orc_char_vectors.argtypes = [cfgp, C.c_int, vp, vp, vp]
         L.orc_residual.argtypes = [cfgp, vp, vp, vp]
         L.orc_averages.argtypes = [cfgp, vp, vp]
         L.orc_limit.argtypes = [cfgp, vp, vp, vp]
@@ -103,11 +105,12 @@ def _p(a: np.ndarray):
 
 def config(nx=10, ny=10, method="cpr", k=1, bc=PERIODIC, box=(-5.0, 5.0, -5.0, 5.0), gamma=1.4,
            cfl=0.24, limiter=0, limiter_eps=1e-3, cpr_chain_rule=1, physics=0, adv=(1.0, 0.5),
-           dt_fixed=0.0, limiter_per_step=0, limiter_all_vars=0, fv_unlimited=0) -> OrcConfig:
+           dt_fixed=0.0, limiter_per_step=0, limiter_all_vars=0, fv_unlimited=0,
+           limiter_characteristic=0) -> OrcConfig:
     m = METHODS[method] if isinstance(method, str) else int(method)
     return OrcConfig(nx, ny, box[0], box[1], box[2], box[3], bc, m, k, gamma, cfl, limiter,
                      limiter_eps, cpr_chain_rule, physics, adv[0], adv[1], dt_fixed,
-                     limiter_per_step, limiter_all_vars, fv_unlimited)
+                     limiter_per_step, limiter_all_vars, fv_unlimited, limiter_characteristic)
 
 
 def npts(cfg: OrcConfig) -> int:
@@ -161,6 +164,13 @@ def rusanov(cfg, dir, qL, qR):
     qL, qR = _v4(qL), _v4(qR); F = np.zeros(4)
     lib().orc_rusanov(C.byref(cfg), dir, _p(qL), _p(qR), _p(F))
     return F
+
+
+def char_vectors(cfg, dir, q):
+    """(R, L) 4x4: right / left eigenvectors of the flux Jacobian along axis dir at q."""
+    R, Lm = np.zeros(16), np.zeros(16)
+    lib().orc_char_vectors(C.byref(cfg), dir, _p(_v4(q)), _p(R), _p(Lm))
+    return R.reshape(4, 4), Lm.reshape(4, 4)
 
 
 def jacobian_apply(cfg, dir, q, d):

@@ -58,6 +58,8 @@ typedef struct {
   int32_t limiter_per_step;  /* HO: 1 = limit once per step (after stage 3) instead of every stage (Q13) */
   int32_t limiter_all_vars;  /* HO: 1 = detect on all four conserved components, not rho only (Q12) */
   int32_t fv_unlimited;      /* FV: 1 = unlimited kappa-scheme (kappa = 0 / 1/3), no minmod (Q10) */
+  int32_t limiter_characteristic; /* HO: 1 = Eq. (35) slopes limited in the characteristic fields of
+                                     the element average (Cockburn-Shu), not componentwise (Q12) */
 } orc_config;
 
 /* decision counters (parity of branch decisions); a minmod whose
@@ -310,6 +312,39 @@ void orc_rusanov(const orc_config *c, int dir, const double *qL, const double *q
 void orc_jacobian_apply(const orc_config *c, int dir, const double *q, const double *d, double *o) { phys_t P = mkphys(c); jac_apply(&P, dir, q, d, o); }
 double orc_wave_speed(const orc_config *c, const double *q) { phys_t P = mkphys(c); return wave_speed(&P, q); }
 double orc_pressure(const orc_config *c, const double *q) { phys_t P = mkphys(c); return pressure(&P, q); }
+
+/* Right / left eigenvectors of the Euler flux Jacobian along axis dir (dir 0:
+ * A(q), dir 1: B(q)) at the state q: A = R diag(un-c, un, un, un+c) L,
+ * columns of R = (1, u - c nx, v - c ny, H - c un), (1, u, v, |u|^2/2),
+ * (0, ny..., tangential), (1, u + c nx, v + c ny, H + c un); L = R^-1 in closed
+ * form with b1 = (gamma-1)/c^2, b2 = b1 |u|^2/2 (textbook, e.g. Toro ch. 3 /
+ * Hesthaven-Warburton).  Pinned: L R = I and L A R diagonal (tests). */
+static void char_vectors(const phys_t *P, int dir, const double *q, double R[4][4], double L[4][4]) {
+  double g = P->g, u = q[1] / q[0], v = q[2] / q[0];
+  double p = pressure(P, q), H = (q[3] + p) / q[0], c = sqrt(g * p / q[0]);
+  double nx = dir == 0 ? 1.0 : 0.0, ny = 1.0 - nx;
+  double un = u * nx + v * ny, ut = -u * ny + v * nx;   /* normal / tangential velocity */
+  double q2 = 0.5 * (u * u + v * v), b1 = (g - 1.0) / (c * c), b2 = b1 * q2;
+  /* columns: acoustic -, entropy, shear, acoustic + */
+  double r[4][4] = {{1.0, u - c * nx, v - c * ny, H - c * un},
+                    {1.0, u, v, q2},
+                    {0.0, -ny, nx, ut},
+                    {1.0, u + c * nx, v + c * ny, H + c * un}};
+  for (int i = 0; i < 4; ++i)
+    for (int k = 0; k < 4; ++k) R[i][k] = r[k][i];
+  double l[4][4] = {{0.5 * (b2 + un / c), -0.5 * (b1 * u + nx / c), -0.5 * (b1 * v + ny / c), 0.5 * b1},
+                    {1.0 - b2, b1 * u, b1 * v, -b1},
+                    {-ut, -ny, nx, 0.0},
+                    {0.5 * (b2 - un / c), -0.5 * (b1 * u - nx / c), -0.5 * (b1 * v - ny / c), 0.5 * b1}};
+  for (int i = 0; i < 4; ++i)
+    for (int k = 0; k < 4; ++k) L[i][k] = l[i][k];
+}
+void orc_char_vectors(const orc_config *cf, int dir, const double *q, double *R16, double *L16) {
+  phys_t P = mkphys(cf);
+  double R[4][4], L[4][4];
+  char_vectors(&P, dir, q, R, L);
+  for (int i = 0; i < 16; ++i) { R16[i] = R[i / 4][i % 4]; L16[i] = L[i / 4][i % 4]; }
+}
 
 /* ------------------------------------------------------------------------- */
 /* minmod (Q17)                                                         */
@@ -744,18 +779,40 @@ int orc_limit(const orc_config *cf, double *Q, int32_t *marks, int64_t *cnt) {
       ++nmarked;
       int iw = nb_index(i, -1, nx, cf->bc), ie = nb_index(i, 1, nx, cf->bc);
       int js = nb_index(j, -1, ny, cf->bc), jn = nb_index(j, 1, ny, cf->bc);
+      double qb[4], dE[4], dW[4], dN[4], dS[4], sx[4], sy[4];
       for (int c = 0; c < 4; ++c) {
-        double qb = Qbar[c * Ne + m];
-        double qW = iw >= 0 ? Qbar[c * Ne + (int64_t)j * nx + iw] : qb;
-        double qE = ie >= 0 ? Qbar[c * Ne + (int64_t)j * nx + ie] : qb;
-        double qS = js >= 0 ? Qbar[c * Ne + (int64_t)js * nx + i] : qb;
-        double qN = jn >= 0 ? Qbar[c * Ne + (int64_t)jn * nx + i] : qb;
-        double sx = mm2((qE - qb) / dx, (qb - qW) / dx, NULL);
-        double sy = mm2((qN - qb) / dy, (qb - qS) / dy, NULL);
+        qb[c] = Qbar[c * Ne + m];
+        double qW = iw >= 0 ? Qbar[c * Ne + (int64_t)j * nx + iw] : qb[c];
+        double qE = ie >= 0 ? Qbar[c * Ne + (int64_t)j * nx + ie] : qb[c];
+        double qS = js >= 0 ? Qbar[c * Ne + (int64_t)js * nx + i] : qb[c];
+        double qN = jn >= 0 ? Qbar[c * Ne + (int64_t)jn * nx + i] : qb[c];
+        dE[c] = (qE - qb[c]) / dx; dW[c] = (qb[c] - qW) / dx;
+        dN[c] = (qN - qb[c]) / dy; dS[c] = (qb[c] - qS) / dy;
+      }
+      if (!cf->limiter_characteristic) {   /* componentwise (Q12 reading) */
+        for (int c = 0; c < 4; ++c) { sx[c] = mm2(dE[c], dW[c], NULL); sy[c] = mm2(dN[c], dS[c], NULL); }
+      } else {                             /* minmod of the characteristic fields at qbar, mapped back */
+        phys_t P = mkphys(cf);
+        for (int dir = 0; dir < 2; ++dir) {
+          double R[4][4], L[4][4], wp[4], wm[4], sw[4];
+          char_vectors(&P, dir, qb, R, L);
+          const double *dp = dir == 0 ? dE : dN, *dm = dir == 0 ? dW : dS;
+          for (int k = 0; k < 4; ++k) {
+            wp[k] = 0.0; wm[k] = 0.0;
+            for (int c = 0; c < 4; ++c) { wp[k] += L[k][c] * dp[c]; wm[k] += L[k][c] * dm[c]; }
+            sw[k] = mm2(wp[k], wm[k], NULL);
+          }
+          double *so = dir == 0 ? sx : sy;
+          for (int c = 0; c < 4; ++c) {
+            so[c] = 0.0;
+            for (int k = 0; k < 4; ++k) so[c] += R[c][k] * sw[k];
+          }
+        }
+      }
+      for (int c = 0; c < 4; ++c)
         for (int b = 0; b < n; ++b)
           for (int a = 0; a < n; ++a)
-            Q[c * N + m * np + b * n + a] = qb + (0.5 * dx) * o.xi[a] * sx + (0.5 * dy) * o.xi[b] * sy;
-      }
+            Q[c * N + m * np + b * n + a] = qb[c] + (0.5 * dx) * o.xi[a] * sx[c] + (0.5 * dy) * o.xi[b] * sy[c];
     }
   if (cnt) cnt[DEC_MARKED] += nmarked;
   free(Qbar);

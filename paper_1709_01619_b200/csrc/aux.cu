@@ -235,7 +235,42 @@ __global__ void k_avg(const AuxArgs A, Nodes nd, const double* __restrict__ q, d
 // index division): detect on density at every edge point (Alg. 10: all 4N edge
 // values evaluated, straight-line), limit all four components if marked (Alg. 11,
 // Eq. (35) in 2-D)
-template <int N, bool GLLP, bool ALL>
+// Characteristic limiting (Cockburn-Shu): eigenvectors of the Euler flux
+// Jacobian along axis DIR at the element average qb -- right columns
+// (1, u -/+ c n, H -/+ c u_n) acoustic, (1, u, |u|^2/2) entropy, (0, t, u_t) shear;
+// left rows in closed form (b1 = (gamma-1)/c^2, b2 = b1 |u|^2/2) -- the slope of
+// each field is minmod(L dp, L dm) and s = R (field slopes).
+template <int DIR>
+__device__ __forceinline__ void char_slopes(const double qb[4], const double dp[4], const double dm[4], double gam,
+                                            double s[4]) {
+  const double ri = 1.0 / qb[0], u = qb[1] * ri, v = qb[2] * ri;
+  const double q2 = 0.5 * (u * u + v * v), p = (gam - 1.0) * (qb[3] - qb[0] * q2);
+  const double H = (qb[3] + p) * ri, c = sqrt(gam * p * ri), rc = 1.0 / c;
+  const double nx = DIR == 0 ? 1.0 : 0.0, ny = 1.0 - nx;
+  const double un = DIR == 0 ? u : v, ut = DIR == 0 ? v : -u;
+  const double b1 = (gam - 1.0) * rc * rc, b2 = b1 * q2;
+  const double Lm[4][4] = {{0.5 * (b2 + un * rc), -0.5 * (b1 * u + nx * rc), -0.5 * (b1 * v + ny * rc), 0.5 * b1},
+                           {1.0 - b2, b1 * u, b1 * v, -b1},
+                           {-ut, -ny, nx, 0.0},
+                           {0.5 * (b2 - un * rc), -0.5 * (b1 * u - nx * rc), -0.5 * (b1 * v - ny * rc), 0.5 * b1}};
+  double w[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    double a = 0.0, b = 0.0;
+#pragma unroll
+    for (int c2 = 0; c2 < 4; ++c2) {
+      a += Lm[k][c2] * dp[c2];
+      b += Lm[k][c2] * dm[c2];
+    }
+    w[k] = minmod2(a, b, nullptr);
+  }
+  s[0] = w[0] + w[1] + w[3];
+  s[1] = (u - c * nx) * w[0] + u * w[1] - ny * w[2] + (u + c * nx) * w[3];
+  s[2] = (v - c * ny) * w[0] + v * w[1] + nx * w[2] + (v + c * ny) * w[3];
+  s[3] = (H - c * un) * w[0] + q2 * w[1] + ut * w[2] + (H + c * un) * w[3];
+}
+
+template <int N, bool GLLP, bool ALL, bool CHAR>
 __device__ __forceinline__ void limit_element(const AuxArgs& A, const Nodes& nd, double* q,
                                               const double* __restrict__ qbar, const double* qbar_lo,
                                               const double* qbar_hi, long long gcs, int bcx, double eps,
@@ -299,22 +334,42 @@ __device__ __forceinline__ void limit_element(const AuxArgs& A, const Nodes& nd,
   }
   if (!trip) return;
   if (dec) atomicAdd((unsigned long long*)&dec[0], 1ull);
+  // Eq. (35): minmod slopes of the neighbour-average differences, per component
+  // or (CHAR, f3 variant of Q12) per characteristic field of the average
+  double qv[4], dE[4], dW[4], dN[4], dS[4], sx[4], sy[4];
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
     const double qc = c == 0 ? qb : qbar[c * ne + m];
     double W, E, S, Nn;
     if (c == 0) { W = rW; E = rE; S = rS; Nn = rN; } else nbr(c, qc, W, E, S, Nn);
-    const double sx = minmod2((E - qc) / dx, (qc - W) / dx, nullptr);
-    const double sy = minmod2((Nn - qc) / dy, (qc - S) / dy, nullptr);
+    qv[c] = qc;
+    dE[c] = (E - qc) / dx;
+    dW[c] = (qc - W) / dx;
+    dN[c] = (Nn - qc) / dy;
+    dS[c] = (qc - S) / dy;
+  }
+  if (CHAR) {
+    char_slopes<0>(qv, dE, dW, A.gamma, sx);
+    char_slopes<1>(qv, dN, dS, A.gamma, sy);
+  } else {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      sx[c] = minmod2(dE[c], dW[c], nullptr);
+      sy[c] = minmod2(dN[c], dS[c], nullptr);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
     double* Qc = q + c * A.cs + m * NP;
 #pragma unroll
     for (int b = 0; b < N; ++b)
 #pragma unroll
-      for (int a = 0; a < N; ++a) Qc[b * N + a] = qc + (0.5 * dx) * nd.xi[a] * sx + (0.5 * dy) * nd.xi[b] * sy;
+      for (int a = 0; a < N; ++a)
+        Qc[b * N + a] = qv[c] + (0.5 * dx) * nd.xi[a] * sx[c] + (0.5 * dy) * nd.xi[b] * sy[c];
   }
 }
 
-template <int N, bool GLLP, bool ALL>
+template <int N, bool GLLP, bool ALL, bool CHAR>
 __global__ void __launch_bounds__(128) k_limit(const AuxArgs A, Nodes nd, double* q, const double* __restrict__ qbar,
                                                const double* qbar_lo, const double* qbar_hi, long long gcs, int bcx,
                                                double eps, long long* dec) {
@@ -322,7 +377,7 @@ __global__ void __launch_bounds__(128) k_limit(const AuxArgs A, Nodes nd, double
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= A.nx) return;
   for (int j = blockIdx.y; j < A.nrows; j += gridDim.y)
-    limit_element<N, GLLP, ALL>(A, nd, q, qbar, qbar_lo, qbar_hi, gcs, bcx, eps, dec, i, j);
+    limit_element<N, GLLP, ALL, CHAR>(A, nd, q, qbar, qbar_lo, qbar_hi, gcs, bcx, eps, dec, i, j);
 }
 }  // namespace
 
@@ -357,31 +412,41 @@ void launch_averages(const AuxArgs& a, const double* q, double* qbar, cudaStream
   k_avg<<<grid_for(ne, 128), 128, 0, s>>>(a, nodes_for(a.method, a.k), q, qbar);
 }
 
-template <int N, bool GLLP, bool ALL>
+template <int N, bool GLLP, bool ALL, bool CHAR>
 void launch_limit_t(const AuxArgs& a, double* q, const double* qbar, const double* qbar_lo, const double* qbar_hi,
                     long long qbar_gcs, int bcx, double eps, long long* dec, cudaStream_t s) {
   dim3 grid((a.nx + 127) / 128, a.nrows < 65535 ? a.nrows : 65535);
-  k_limit<N, GLLP, ALL><<<grid, 128, 0, s>>>(a, nodes_for(a.method, a.k), q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx,
-                                              eps, dec);
+  k_limit<N, GLLP, ALL, CHAR><<<grid, 128, 0, s>>>(a, nodes_for(a.method, a.k), q, qbar, qbar_lo, qbar_hi, qbar_gcs,
+                                                    bcx, eps, dec);
+}
+
+template <int N, bool GLLP>
+void launch_limit_g(const AuxArgs& a, double* q, const double* qbar, const double* qbar_lo, const double* qbar_hi,
+                    long long qbar_gcs, int bcx, double eps, int all_vars, int charact, long long* dec,
+                    cudaStream_t s) {
+  if (all_vars && charact) launch_limit_t<N, GLLP, true, true>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, dec, s);
+  else if (all_vars) launch_limit_t<N, GLLP, true, false>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, dec, s);
+  else if (charact) launch_limit_t<N, GLLP, false, true>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, dec, s);
+  else launch_limit_t<N, GLLP, false, false>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, dec, s);
 }
 
 template <int N>
 void launch_limit_n(const AuxArgs& a, double* q, const double* qbar, const double* qbar_lo, const double* qbar_hi,
-                    long long qbar_gcs, int bcx, double eps, int all_vars, long long* dec, cudaStream_t s) {
-  const bool gll = (a.method == 1 || a.method == 3);
-  if (gll && all_vars) launch_limit_t<N, true, true>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, dec, s);
-  else if (gll) launch_limit_t<N, true, false>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, dec, s);
-  else if (all_vars) launch_limit_t<N, false, true>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, dec, s);
-  else launch_limit_t<N, false, false>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, dec, s);
+                    long long qbar_gcs, int bcx, double eps, int all_vars, int charact, long long* dec,
+                    cudaStream_t s) {
+  if (a.method == 1 || a.method == 3)
+    launch_limit_g<N, true>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, all_vars, charact, dec, s);
+  else
+    launch_limit_g<N, false>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, all_vars, charact, dec, s);
 }
 
 void launch_limit(const AuxArgs& a, double* q, const double* qbar, const double* qbar_lo, const double* qbar_hi,
-                  long long qbar_gcs, int bcx, double eps, int all_vars, long long* dec, cudaStream_t s) {
+                  long long qbar_gcs, int bcx, double eps, int all_vars, int charact, long long* dec, cudaStream_t s) {
   switch (a.k) {
-    case 1: return launch_limit_n<2>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, all_vars, dec, s);
-    case 2: return launch_limit_n<3>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, all_vars, dec, s);
-    case 3: return launch_limit_n<4>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, all_vars, dec, s);
-    default: return launch_limit_n<5>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, all_vars, dec, s);
+    case 1: return launch_limit_n<2>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, all_vars, charact, dec, s);
+    case 2: return launch_limit_n<3>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, all_vars, charact, dec, s);
+    case 3: return launch_limit_n<4>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, all_vars, charact, dec, s);
+    default: return launch_limit_n<5>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, all_vars, charact, dec, s);
   }
 }
 

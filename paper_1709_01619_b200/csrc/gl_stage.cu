@@ -32,10 +32,11 @@ namespace {
 // smem, so narrower strips keep 2+ CTAs per SM (A/B on 4096^2: DG 16 > 32 by
 // 37 % at P3, 3-6 % at P2/P4; SD 32 > 16 by 10 % at P3, 16 > 32 by 13 % at P4)
 #ifndef H2D_DG_TX
-#define H2D_DG_TX (K == 3 ? 14 : 16)  // P3: 14-element strips = 16-slot TMA rows, 4 CTAs/SM (+7.5 % over 16)
+#define H2D_DG_TX (K == 3 ? 14 : 12)  // P3: 14-element strips = 16-slot TMA rows, 4 CTAs/SM (+7.5 % over 16);
+                                     // P4: 12 (60 threads, 4 CTAs/SM; +16 % over 16)
 #endif
 #ifndef H2D_SD_TX
-#define H2D_SD_TX (K == 3 ? 32 : 16)
+#define H2D_SD_TX (K == 3 ? 14 : 12)  // A/B: P3 14 +2.5 % over 32; P4 12 +4 % over 16
 #endif
 #ifndef H2D_LMINB
 #define H2D_LMINB 1

@@ -38,7 +38,7 @@ namespace {
 template <int K> struct GTile;
 // CTAs per SM (register cap 64K / (MINB x threads)) and strip widths, A/B-timed on
 // 4096^2 / 8192^2 (round 1): P1 MINB 4 (+9 % over 2), P2 MINB 4 (+41 % over 2),
-// P4 16-element strips at 2 CTAs/SM (+25 % over 32 at 1 CTA/SM)
+// P4 12-element strips (60 threads) at 4 CTAs/SM (+18-23 % over 16 at 2, +25 % over 32 at 1)
 #ifndef H2D_MINB1
 #define H2D_MINB1 4
 #endif
@@ -46,10 +46,10 @@ template <int K> struct GTile;
 #define H2D_MINB2 4
 #endif
 #ifndef H2D_TX4
-#define H2D_TX4 16
+#define H2D_TX4 12
 #endif
 #ifndef H2D_MINB4
-#define H2D_MINB4 2
+#define H2D_MINB4 4
 #endif
 template <> struct GTile<1> { static constexpr int TX = 64, RB = 64, MINB = H2D_MINB1; };  // 128 threads
 template <> struct GTile<2> { static constexpr int TX = 32, RB = 64, MINB = H2D_MINB2; };  //  96 threads

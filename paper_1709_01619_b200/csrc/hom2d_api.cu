@@ -103,7 +103,8 @@ hom2d_status check_cfg(const hom2d_config* c, int nranks) {
   const int G = c->method == HOM2D_FV ? 2 : 1;
   if (c->ny / nranks < G) return HOM2D_ERR_MESH;
   if (!(c->gamma > 1.0) || !(c->cfl > 0.0)) return HOM2D_ERR_ARG;
-  if ((unsigned)c->limiter_per_step > 1u || (unsigned)c->limiter_all_vars > 1u || (unsigned)c->fv_unlimited > 1u)
+  if ((unsigned)c->limiter_per_step > 1u || (unsigned)c->limiter_all_vars > 1u || (unsigned)c->fv_unlimited > 1u ||
+      (unsigned)c->limiter_characteristic > 1u)
     return HOM2D_ERR_ARG;
   return HOM2D_OK;
 }
@@ -308,7 +309,7 @@ hom2d_status run_limiter(hom2d* h, double* X, const double* dt = nullptr, bool a
   hom2d_status st = exchange(h, h->qbar, ne, h->cfg.nx, &lo, &hi, &gcs, h->qblo, h->qbhi, 1, h->stream);
   if (st) return st;
   launch_limit(A, X, h->qbar, lo, hi, gcs, h->cfg.bc, h->cfg.limiter_eps, h->cfg.limiter_all_vars,
-               h->cfg.record_decisions ? h->dec : nullptr, h->stream);
+               h->cfg.limiter_characteristic, h->cfg.record_decisions ? h->dec : nullptr, h->stream);
   h->launches++;
   CU(h, cudaPeekAtLastError());
   return HOM2D_OK;

@@ -78,6 +78,7 @@ void launch_error_final(const double* part, int nblocks, double* out3, cudaStrea
 // averages Qbar[4][nx*nrows] and the detect+limit pass (HO)
 void launch_averages(const AuxArgs& a, const double* q, double* qbar, cudaStream_t s);
 void launch_limit(const AuxArgs& a, double* q, const double* qbar, const double* qbar_lo, const double* qbar_hi,
-                  long long qbar_gcs, int bcx, double eps, int all_vars, long long* dec, cudaStream_t s);
+                  long long qbar_gcs, int bcx, double eps, int all_vars, int charact, long long* dec,
+                  cudaStream_t s);
 
 }  // namespace h2d

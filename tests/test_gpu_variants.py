@@ -56,7 +56,7 @@ SHOCK_CASES = [("cpr", 1, 0.2), ("cpr", 2, 0.1), ("ndg", 1, 0.2), ("dg", 1, 0.2)
 
 
 @pytest.mark.parametrize("method,k,cfl", SHOCK_CASES)
-@pytest.mark.parametrize("variant", ["limiter_per_step", "limiter_all_vars"])
+@pytest.mark.parametrize("variant", ["limiter_per_step", "limiter_all_vars", "limiter_characteristic"])
 def test_shock_limiter_variants(orc, P, method, k, cfl, variant):
     """Radial shock tube, transmissive, 40 steps: state parity and identical
     trouble-cell mark counts for each limiter variant."""

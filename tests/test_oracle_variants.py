@@ -115,3 +115,67 @@ def test_limit_per_step_is_unlimited_step_then_limit(orc, method, k):
     np.testing.assert_array_equal(q_step, q_ref)
     q_stage, _, _ = orc.run(c_stage, q0, 1)
     assert np.abs(q_stage - q_step).max() > 1e-8
+
+
+# --------------------------------------------------------------------------- #
+# Q12 alternative: Eq. (35) slopes limited in characteristic fields           #
+# --------------------------------------------------------------------------- #
+def _random_states(n, seed=0):
+    rng = np.random.default_rng(seed)
+    rho = rng.uniform(0.2, 2.0, n)
+    u, v = rng.uniform(-1.5, 1.5, n), rng.uniform(-1.5, 1.5, n)
+    p = rng.uniform(0.1, 3.0, n)
+    return [np.array([r, r * a, r * b, pp / 0.4 + 0.5 * r * (a * a + b * b)]) for r, a, b, pp in zip(rho, u, v, p)]
+
+
+@pytest.mark.parametrize("dir", [0, 1])
+def test_char_vectors_diagonalise_the_jacobian(orc, dir):
+    """L R = I and L A R = diag(u_n - c, u_n, u_n, u_n + c), with A the pinned
+    flux-Jacobian action."""
+    cfg = orc.config()
+    for q in _random_states(20, seed=dir):
+        R, Lm = orc.char_vectors(cfg, dir, q)
+        np.testing.assert_allclose(Lm @ R, np.eye(4), atol=1e-13)
+        A = np.column_stack([orc.jacobian_apply(cfg, dir, q, e) for e in np.eye(4)])
+        lam = Lm @ A @ R
+        un = q[1 + dir] / q[0]
+        c = np.sqrt(1.4 * orc.pressure(cfg, q) / q[0])
+        np.testing.assert_allclose(lam, np.diag([un - c, un, un, un + c]), atol=1e-12 * (abs(un) + c))
+
+
+@pytest.mark.parametrize("method,k", [("cpr", 1), ("dg", 2), ("sd", 1), ("ndg", 2)])
+def test_characteristic_limiting_flattens_opposite_waves(orc, method, k):
+    """Centre element average q0; its E neighbour differs by dx r_1 (the u-c
+    acoustic wave at q0), its W neighbour by -dx r_4 (the u+c wave): every
+    characteristic field has slopes of opposite sign or zero, so characteristic
+    limiting rebuilds the marked element as the constant q0, while the
+    componentwise limiter keeps a nonzero density slope."""
+    kw = dict(nx=3, ny=3, method=method, k=k, bc=1, box=(0.0, 3.0, 0.0, 3.0), limiter=1)
+    c_comp = orc.config(**kw)
+    c_char = orc.config(limiter_characteristic=1, **kw)
+    q0 = np.array([1.0, 0.3, -0.2, 2.6])
+    R, _ = orc.char_vectors(c_char, 0, q0)
+    X, Y = orc.point_coords(c_comp)
+    npe = (k + 1) ** 2
+    q = np.zeros((4, X.size))
+    for m in range(9):
+        i, j = m % 3, m // 3
+        sl = slice(m * npe, (m + 1) * npe)
+        st = q0.copy()
+        if (i, j) == (2, 1):
+            st = q0 + 1.0 * R[:, 0]
+        elif (i, j) == (0, 1):
+            st = q0 - 1.0 * R[:, 3]
+        q[:, sl] = st[:, None]
+        if (i, j) == (1, 1):  # zero-average density ramp inside the centre: it trips the detector
+            xi = X[sl] - 1.5
+            q[:, sl] = q0[:, None] + 0.4 * np.outer(np.array([1.0, 0.3, -0.2, 1.3]), xi)
+    q = q.reshape(-1)
+    qc, mc = orc.limit(c_char, q)
+    qm, mm = orc.limit(c_comp, q)
+    m = 4
+    assert mc[m] == 1 and mm[m] == 1
+    cen = qc.reshape(4, -1)[:, m * npe:(m + 1) * npe]
+    np.testing.assert_allclose(cen, np.repeat(q0[:, None], npe, axis=1), rtol=1e-13, atol=1e-14)
+    cen_comp = qm.reshape(4, -1)[:, m * npe:(m + 1) * npe]
+    assert np.ptp(cen_comp[0]) > 0.1
