@@ -24,13 +24,14 @@ __device__ __forceinline__ double frcp(double x) {
   return fma(r, e, r);
 }
 
-// fp64 square root: MUFU rsqrt seed + two Newton steps + one Markstein correction
+// fp64 square root: MUFU rsqrt seed (relative error e0 <= ~2^-21: the seed sees
+// the high word only), one Newton step (e1 ~ 1.5 e0^2 ~ 2^-41), then s = x y and
+// one Markstein correction s + y (x - s^2) / 2 (error ~ 1.5 e1^2 + final rounding),
+// i.e. as accurate as two Newton steps + correction, 4 fp64 operations fewer
 __device__ __forceinline__ double fsqrt(double x) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  double e = fma(-x * y, y, 1.0);
-  y = fma(0.5 * y, e, y);
-  e = fma(-x * y, y, 1.0);
+  const double e = fma(-x * y, y, 1.0);
   y = fma(0.5 * y, e, y);
   const double s = x * y;
   return fma(0.5 * y, fma(-s, s, x), s);
