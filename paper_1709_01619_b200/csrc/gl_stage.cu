@@ -448,10 +448,22 @@ __global__ void __launch_bounds__(L<M, K>::NT, LTile<M, K>::MINB) gl_stage_kerne
             }
             flux<0>(v, prims(v, gm1), phi[r]);
           }
+          // column b of the element, read once for its N-1 interior flux points
+          double colv[4][N];
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+#pragma unroll
+            for (int l = 0; l < N; ++l) colv[c][l] = own_at(vc, c, lx + 1, l * N + b);
 #pragma unroll
           for (int r = 1; r < N; ++r) {
             double v[4], g[4];
-            interp(vc, lx + 1, 1, b, tab.v + T::SI + r * N, v, false);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              double sv = 0.0;
+#pragma unroll
+              for (int l = 0; l < N; ++l) sv += tab.v[T::SI + r * N + l] * colv[c][l];
+              v[c] = sv;
+            }
             flux<1>(v, prims(v, gm1), g);
             st4(sPY + lx * H::PYS + (b * (N - 1) + (r - 1)) * 4, g);
           }
@@ -531,16 +543,23 @@ __global__ void __launch_bounds__(L<M, K>::NT, LTile<M, K>::MINB) gl_stage_kerne
             R[c] = a.rdx2 * fx + a.rdy2 * g2;
           }
         } else {  // SD
+          double gy[4];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) gy[c] = sT[T::SD + b * (N + 1) + 0] * FS[c] + sT[T::SD + b * (N + 1) + N] * FN[c];
+#pragma unroll
+          for (int r = 1; r < N; ++r) {  // interior y flux points of column x (16-B smem reads)
+            double pv[4];
+            ld4(sPY + lx * H::PYS + (x * (N - 1) + (r - 1)) * 4, pv);
+            const double dr = sT[T::SD + b * (N + 1) + r];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) gy[c] += dr * pv[c];
+          }
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
-            double fx = 0.0, gy = 0.0;
+            double fx = 0.0;
 #pragma unroll
             for (int r = 0; r <= N; ++r) fx += tab.v[T::SD + x * (N + 1) + r] * phi[r][c];
-            gy = sT[T::SD + b * (N + 1) + 0] * FS[c] + sT[T::SD + b * (N + 1) + N] * FN[c];
-#pragma unroll
-            for (int r = 1; r < N; ++r)
-              gy += sT[T::SD + b * (N + 1) + r] * sPY[lx * H::PYS + (x * (N - 1) + (r - 1)) * 4 + c];
-            R[c] = -a.rdx2 * fx - a.rdy2 * gy;
+            R[c] = -a.rdx2 * fx - a.rdy2 * gy[c];
           }
         }
 #pragma unroll
