@@ -406,7 +406,27 @@ __global__ void __launch_bounds__(L<M, K>::NT, LTile<M, K>::MINB) gl_stage_kerne
         double qw[4], qe[4], ql[4], sw, se, sl, fW[4], fE[4], flf[4], gd[4], sd, gu[4], su;
         {
           double v[4];
-          interp(vc, lx, 0, b, wr, v, true);  // E trace of the W neighbour's line
+          if constexpr (H::SWZ) {  // E trace of the W neighbour's line: its row b as two 16-B chunks
+            const bool fw = (lx == 0 && wrapW);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              double row[N];
+#pragma unroll
+              for (int h = 0; h < N / 2; ++h) {
+                const int iS = (c * H::RSW + lx) * 16 + (((2 * b + h) ^ (lx & 7)) << 1);
+                const int iF = H::FIXO + c * 16 + N * b + 2 * h;
+                const double2 u2 = *reinterpret_cast<const double2*>(vc.st + (fw ? iF : iS));
+                row[2 * h] = u2.x;
+                row[2 * h + 1] = u2.y;
+              }
+              double sv = 0.0;
+#pragma unroll
+              for (int l = 0; l < N; ++l) sv += wr[l] * row[l];
+              v[c] = sv;
+            }
+          } else {
+            interp(vc, lx, 0, b, wr, v, true);  // E trace of the W neighbour's line
+          }
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
             double s0 = 0.0, s1 = 0.0;
