@@ -304,8 +304,16 @@ __device__ __forceinline__ void limit_element(const AuxArgs& A, const Nodes& nd,
     }
     double r[NP];
     const double* Qc = q + c * A.cs + m * NP;
+    if constexpr (NP % 4 == 0) {  // P1, P3: the element's values as 32-B vectors (32-B aligned: cs, NP % 4 == 0)
 #pragma unroll
-    for (int p = 0; p < NP; ++p) r[p] = Qc[p];
+      for (int p = 0; p < NP; p += 4)
+        asm volatile("ld.global.v4.f64 {%0, %1, %2, %3}, [%4];"
+                     : "=d"(r[p]), "=d"(r[p + 1]), "=d"(r[p + 2]), "=d"(r[p + 3])
+                     : "l"(Qc + p));
+    } else {
+#pragma unroll
+      for (int p = 0; p < NP; ++p) r[p] = Qc[p];
+    }
 #pragma unroll
     for (int t = 0; t < N; ++t) {
       double qw, qe_, qs, qn;

@@ -335,11 +335,12 @@ __global__ void __launch_bounds__(L<M, K>::NT, LTile<M, K>::MINB) gl_stage_kerne
   auto interp = [&](const RowView& v, int e, int dir, int bb, const double* w, double out[4], bool anyslot) {
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
-      double s = 0.0;
+      double s;  // (sums start from their first product: no zero-initialised accumulators)
 #pragma unroll
       for (int l = 0; l < N; ++l) {
         const int p = dir == 0 ? bb * N + l : l * N + bb;
-        s += w[l] * (anyslot ? any_at(v, c, e, p) : own_at(v, c, e, p));
+        const double val = anyslot ? any_at(v, c, e, p) : own_at(v, c, e, p);
+        s = l == 0 ? w[l] * val : fma(w[l], val, s);
       }
       out[c] = s;
     }
@@ -351,6 +352,7 @@ __global__ void __launch_bounds__(L<M, K>::NT, LTile<M, K>::MINB) gl_stage_kerne
 
   double lam = 0.0;
   const double bdt = a.bcoef * dtv;
+  const double cx = bdt * a.rdx2, cy = bdt * a.rdy2;  // metric x dt folded (R below is bdt R)
   const double* EL = tab.v + T::EL;
   const double* ER = tab.v + T::ER;
   const double* SI0 = tab.v + T::SI;               // flux point 0 row of sd_I (== eL)
@@ -419,9 +421,9 @@ __global__ void __launch_bounds__(L<M, K>::NT, LTile<M, K>::MINB) gl_stage_kerne
                 row[2 * h] = u2.x;
                 row[2 * h + 1] = u2.y;
               }
-              double sv = 0.0;
+              double sv = wr[0] * row[0];
 #pragma unroll
-              for (int l = 0; l < N; ++l) sv += wr[l] * row[l];
+              for (int l = 1; l < N; ++l) sv = fma(wr[l], row[l], sv);
               v[c] = sv;
             }
           } else {
@@ -429,9 +431,9 @@ __global__ void __launch_bounds__(L<M, K>::NT, LTile<M, K>::MINB) gl_stage_kerne
           }
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
-            double s0 = 0.0, s1 = 0.0;
+            double s0 = wl[0] * q[c][0], s1 = wr[0] * q[c][0];
 #pragma unroll
-            for (int l = 0; l < N; ++l) { s0 += wl[l] * q[c][l]; s1 += wr[l] * q[c][l]; }
+            for (int l = 1; l < N; ++l) { s0 = fma(wl[l], q[c][l], s0); s1 = fma(wr[l], q[c][l], s1); }
             qw[c] = s0;
             qe[c] = s1;
           }
@@ -461,9 +463,9 @@ __global__ void __launch_bounds__(L<M, K>::NT, LTile<M, K>::MINB) gl_stage_kerne
             double v[4];
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
-              double s = 0.0;
+              double s = tab.v[T::SI + r * N] * q[c][0];
 #pragma unroll
-              for (int l = 0; l < N; ++l) s += tab.v[T::SI + r * N + l] * q[c][l];
+              for (int l = 1; l < N; ++l) s = fma(tab.v[T::SI + r * N + l], q[c][l], s);
               v[c] = s;
             }
             flux<0>(v, prims(v, gm1), phi[r]);
@@ -479,9 +481,9 @@ __global__ void __launch_bounds__(L<M, K>::NT, LTile<M, K>::MINB) gl_stage_kerne
             double v[4], g[4];
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
-              double sv = 0.0;
+              double sv = tab.v[T::SI + r * N] * colv[c][0];
 #pragma unroll
-              for (int l = 0; l < N; ++l) sv += tab.v[T::SI + r * N + l] * colv[c][l];
+              for (int l = 1; l < N; ++l) sv = fma(tab.v[T::SI + r * N + l], colv[c][l], sv);
               v[c] = sv;
             }
             flux<1>(v, prims(v, gm1), g);
@@ -542,25 +544,25 @@ __global__ void __launch_bounds__(L<M, K>::NT, LTile<M, K>::MINB) gl_stage_kerne
         if (M == LM_DG) {
           // weak form, Eq. (19) / SURVEY C6 divided by w_a:
           // (2/dx) [sum_l (w_l/w_a) l'_a(xi_l) f_l - (l_a(1) F^E - l_a(-1) F^W) / w_a] + (y likewise)
-          double gy[4] = {0.0, 0.0, 0.0, 0.0};
+          double gy[4];
 #pragma unroll
           for (int l = 0; l < N; ++l) {  // column x of the element: g of its points (16-B smem reads)
             double g[4];
             ld4(sG + lx * H::GS + (l * N + x) * 4, g);
             const double dv = sT[T::DV + b * N + l];
 #pragma unroll
-            for (int c = 0; c < 4; ++c) gy[c] += dv * g[c];
+            for (int c = 0; c < 4; ++c) gy[c] = l == 0 ? dv * g[c] : fma(dv, g[c], gy[c]);
           }
           const double sRa = tab.v[T::SR + x], sLa = tab.v[T::SL + x];
           const double sRb = sT[T::SR + b], sLb = sT[T::SL + b];
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
-            double fx = 0.0;
+            double fx = tab.v[T::DV + x * N] * fl[c][0];
 #pragma unroll
-            for (int l = 0; l < N; ++l) fx += tab.v[T::DV + x * N + l] * fl[c][l];
+            for (int l = 1; l < N; ++l) fx = fma(tab.v[T::DV + x * N + l], fl[c][l], fx);
             fx += sLa * FW[c] - sRa * FE[c];
             const double g2 = gy[c] + sLb * FS[c] - sRb * FN[c];
-            R[c] = a.rdx2 * fx + a.rdy2 * g2;
+            R[c] = fma(cx, fx, cy * g2);  // bdt R, R = (2/dx) fx + (2/dy) g2 (weak form signs)
           }
         } else {  // SD
           double gy[4];
@@ -576,14 +578,14 @@ __global__ void __launch_bounds__(L<M, K>::NT, LTile<M, K>::MINB) gl_stage_kerne
           }
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
-            double fx = 0.0;
+            double fx = tab.v[T::SD + x * (N + 1)] * phi[0][c];
 #pragma unroll
-            for (int r = 0; r <= N; ++r) fx += tab.v[T::SD + x * (N + 1) + r] * phi[r][c];
-            R[c] = -a.rdx2 * fx - a.rdy2 * gy[c];
+            for (int r = 1; r <= N; ++r) fx = fma(tab.v[T::SD + x * (N + 1) + r], phi[r][c], fx);
+            R[c] = fma(-cx, fx, -cy * gy[c]);  // bdt R, R = -(2/dx) fx - (2/dy) gy
           }
         }
 #pragma unroll
-        for (int c = 0; c < 4; ++c) ov[c][x] = fma(a.a0, q0v[c][x], fma(a.a1, v[c], bdt * R[c]));
+        for (int c = 0; c < 4; ++c) ov[c][x] = fma(a.a0, q0v[c][x], fma(a.a1, v[c], R[c]));
       }
       if (a.lam || a.bad) {  // dt wave speed and non-physical check (straight-line)
         unsigned long long bidx = ~0ull;

@@ -345,6 +345,7 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
   const double gLb = sT[N * N + b], gRb = sT[N * N + N + b];
   double lam = 0.0;
   const double bdt = a.bcoef * dtv;
+  const double cx = -bdt * a.rdx2, cy = -bdt * a.rdy2;
 
   for (int L = 0; L <= RBv; ++L) {
     mbar_wait(&bar[L % NSTG], (L / NSTG) & 1);
@@ -468,10 +469,7 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
       // 16-B swizzled chunk (half the shared-memory loads of a per-point loop)
       double dyall[N][4];
       if constexpr (M == GM_CPR && H::SWZ) {
-#pragma unroll
-        for (int x = 0; x < N; ++x)
-#pragma unroll
-          for (int c = 0; c < 4; ++c) dyall[x][c] = 0.0;
+        // (sums start from their first product: no zero-initialised accumulators)
 #pragma unroll
         for (int l = 0; l < N; ++l) {
           const double db = D[b * N + l];
@@ -481,8 +479,13 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
             for (int h = 0; h < N / 2; ++h) {
               const double2 u = *reinterpret_cast<const double2*>(
                   vc.st + (c * H::RSW + lx + 1) * 16 + (((2 * l + h) ^ ((lx + 1) & 7)) << 1));
-              dyall[2 * h][c] += db * u.x;
-              dyall[2 * h + 1][c] += db * u.y;
+              if (l == 0) {
+                dyall[2 * h][c] = db * u.x;
+                dyall[2 * h + 1][c] = db * u.y;
+              } else {
+                dyall[2 * h][c] = fma(db, u.x, dyall[2 * h][c]);
+                dyall[2 * h + 1][c] = fma(db, u.y, dyall[2 * h + 1][c]);
+              }
             }
         }
       }
@@ -494,7 +497,7 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
 #pragma unroll
       for (int x = 0; x < N; ++x) {
         double v[4] = {q[0][x], q[1][x], q[2][x], q[3][x]};
-        double Fx[4], Gy[4], dy[4] = {0, 0, 0, 0};
+        double Fx[4], Gy[4], dy[4];
 #pragma unroll
         for (int l = 0; l < N; ++l) {  // column x of the element (broadcast over its lines)
           const double db = D[b * N + l];
@@ -505,30 +508,33 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
             }
           } else if (M == GM_CPR) {
 #pragma unroll
-            for (int c = 0; c < 4; ++c) dy[c] += db * own_at(vc, c, lx + 1, l * N + x);
+            for (int c = 0; c < 4; ++c) {
+              const double u = own_at(vc, c, lx + 1, l * N + x);
+              dy[c] = l == 0 ? db * u : fma(db, u, dy[c]);
+            }
           } else {
             double u[4];
             ld4(sG + lx * H::GS + (l * N + x) * 4, u);
 #pragma unroll
-            for (int c = 0; c < 4; ++c) dy[c] += db * u[c];
+            for (int c = 0; c < 4; ++c) dy[c] = l == 0 ? db * u[c] : fma(db, u[c], dy[c]);
           }
         }
         if (M == GM_CPR) {  // chain rule: A(q) dq/dxi + B(q) dq/deta
-          double dx[4] = {0, 0, 0, 0};
+          double dx[4];
 #pragma unroll
           for (int l = 0; l < N; ++l) {
             const double da = tab.v[x * N + l];  // compile-time index: constant-bank operand
 #pragma unroll
-            for (int c = 0; c < 4; ++c) dx[c] += da * q[c][l];
+            for (int c = 0; c < 4; ++c) dx[c] = l == 0 ? da * q[c][l] : fma(da, q[c][l], dx[c]);
           }
           const Prim w = (x == 0) ? pW : (x == N - 1) ? pE : prims(v, gm1);
           jac_pair(v, w, gm1, dx, dy, Fx, Gy);
         } else {            // NDG: D[F]
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
-            double s = 0.0;
+            double s = tab.v[x * N] * fxl[c][0];
 #pragma unroll
-            for (int l = 0; l < N; ++l) s += tab.v[x * N + l] * fxl[c][l];
+            for (int l = 1; l < N; ++l) s = fma(tab.v[x * N + l], fxl[c][l], s);
             Fx[c] = s;
             Gy[c] = dy[c];
           }
@@ -541,8 +547,8 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
         for (int c = 0; c < 4; ++c) {
           const double fx = Fx[c] + gLa * jW[c] + gRa * jE[c];
           const double gy = Gy[c] + gLb * jS[c] + gRb * jN[c];
-          const double R = -a.rdx2 * fx - a.rdy2 * gy;
-          ov[c][x] = fma(a.a0, q0v[c][x], fma(a.a1, v[c], bdt * R));
+          // out = a0 q^n + a1 q + bdt R,  R = -(2/dx) fx - (2/dy) gy  (metric folded into cx, cy)
+          ov[c][x] = fma(a.a0, q0v[c][x], fma(a.a1, v[c], fma(cx, fx, cy * gy)));
         }
       }
       if (a.lam || a.bad) {  // dt wave speed and non-physical check share one reciprocal (straight-line)
