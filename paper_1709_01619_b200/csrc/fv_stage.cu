@@ -20,7 +20,10 @@
 namespace h2d {
 
 namespace {
-constexpr int FTX = 128, FRB = 64, FNS = 5;   // cells per strip, rows per march, ring rows
+#ifndef H2D_FTX
+#define H2D_FTX 128  // A/B: 64 at 8 CTAs/SM -5 %; 256 exceeds the static smem limit
+#endif
+constexpr int FTX = H2D_FTX, FRB = 64, FNS = 5;   // cells per strip, rows per march, ring rows
 constexpr int FW = FTX + 4;                    // ring row width: 2 halo cells each side
 
 // the two reconstructed face values of cell i (stencil i-1, i, i+1): lo at its
