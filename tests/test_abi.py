@@ -51,8 +51,9 @@ def test_config_struct_layout_matches_header():
 #include <stddef.h>
 #include "hom2d.h"
 int main(void) {
-  printf("%zu %zu %zu %zu %zu %zu\n", sizeof(hom2d_config), offsetof(hom2d_config, gamma),
+  printf("%zu %zu %zu %zu %zu %zu %zu %zu\n", sizeof(hom2d_config), offsetof(hom2d_config, gamma),
          offsetof(hom2d_config, limiter_eps), offsetof(hom2d_config, record_decisions),
+         offsetof(hom2d_config, limiter_per_step), offsetof(hom2d_config, limiter_characteristic),
          sizeof(hom2d_dist), offsetof(hom2d_dist, cuda_stream));
   return 0;
 }
@@ -67,7 +68,7 @@ int main(void) {
     C = P.Config
     D = P.Dist
     assert vals == [ctypes.sizeof(C), C.gamma.offset, C.limiter_eps.offset, C.record_decisions.offset,
-                    ctypes.sizeof(D), D.cuda_stream.offset]
+                    C.limiter_per_step.offset, C.limiter_characteristic.offset, ctypes.sizeof(D), D.cuda_stream.offset]
 
 
 def test_product_does_not_import_oracle():
