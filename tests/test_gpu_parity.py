@@ -207,7 +207,9 @@ def test_determinism_bitwise(orc, P):
     np.testing.assert_array_equal(out[0], out[1])
 
 
-@pytest.mark.parametrize("method,k,n", [("cpr", 3, 2048), ("cpr", 2, 1024), ("fv", 1, 2048)])
+@pytest.mark.parametrize("method,k,n", [("cpr", 3, 2048), ("cpr", 2, 1024), ("fv", 1, 2048), ("ndg", 3, 2048),
+                                          ("dg", 3, 2048), ("sd", 3, 2048), ("cpr", 1, 2048), ("cpr", 4, 1024),
+                                          ("dg", 4, 1024), ("sd", 2, 1024), ("fv", 2, 2048)])
 def test_full_size_tiled_patch(orc, P, method, k, n):
     """At BASELINE sizes, in the bench's launch configuration: a state that repeats
     a seeded 16x16-element patch must give the oracle's residual of that patch on
@@ -250,4 +252,36 @@ def test_full_size_free_stream_and_mass(orc, P):
     out = torch.empty_like(q)
     s.get_state(out)
     assert float((out - q).abs().max()) < 1e-12
+    s.close()
+
+
+@pytest.mark.parametrize("method,k,n,cfl", [("cpr", 1, 1024, 0.2), ("cpr", 2, 1024, 0.1), ("dg", 1, 1024, 0.2),
+                                            ("sd", 1, 1024, 0.27), ("ndg", 3, 512, 0.06)])
+def test_full_size_tiled_patch_limited_step(orc, P, method, k, n, cfl):
+    """Limiter path at bench sizes (fused element averages in the stage kernels,
+    k_limit, the lambda pass): one limited SSP-RK3 step of a periodic state that
+    repeats a seeded 16x16 patch equals the oracle's step of the patch on its own
+    periodic grid, tiled (dt agrees: same element size, same max wave speed)."""
+    import torch
+    pn = 16
+    box_small = (-5.0, -5.0 + 10.0 * pn / n, -5.0, -5.0 + 10.0 * pn / n)
+    oc = orc.config(nx=pn, ny=pn, method=method, k=k, box=box_small, cfl=cfl, limiter=1)
+    from paper_1709_01619_b200.inputs import perturb
+    X, Y = orc.point_coords(oc)
+    inner = (X - box_small[0]) ** 2 + (Y - box_small[2]) ** 2 < (0.3 * (box_small[1] - box_small[0])) ** 2
+    rho = np.where(inner, 1.0, 0.125)  # a shock-tube disc in the patch (and jumps at its tiled edges)
+    qp = perturb(np.concatenate([rho, 0 * rho, 0 * rho, np.where(inner, 2.5, 0.25)]), seed=23, amp=1e-2)
+    cnt = np.zeros(8, dtype=np.int64)
+    q1, _, _ = orc.run(oc, qp, 1, counts=cnt)
+    assert cnt[0] > 0
+    npe = (k + 1) ** 2
+    big = np.tile(qp.reshape(4, pn, pn, npe), (1, n // pn, n // pn, 1)).reshape(-1)
+    s = P.Solver(P.make_config(n, n, method=method, k=k, cfl=cfl, limiter=1, record_decisions=1))
+    s.set_state(torch.from_numpy(big).cuda())
+    s.step(1)
+    out = s.get_state().reshape(4, n // pn, pn, n // pn, pn, npe)
+    ref = q1.reshape(4, 1, pn, 1, pn, npe)
+    err = np.abs(out - ref).max(axis=(1, 2, 3, 4, 5)) / np.maximum(np.abs(ref).reshape(4, -1).max(1), 1e-300)
+    assert err.max() < 1e-10
+    assert s.decisions()[0] == cnt[0] * (n // pn) ** 2
     s.close()
