@@ -192,6 +192,58 @@ def reference_arm(args, wl):
     print(json.dumps(line), flush=True)
 
 
+# CFL of the smooth problem: Table 1 for P1/P2, the max-CFL protocol for P3/P4
+# (profiles/round1_cfl_protocol.md); FV Table 1's smallest value
+TTE_CFL = {("cpr", 1): 0.24, ("ndg", 1): 0.24, ("dg", 1): 0.24, ("sd", 1): 0.3,
+           ("cpr", 2): 0.13, ("ndg", 2): 0.13, ("dg", 2): 0.13, ("sd", 2): 0.2,
+           ("cpr", 3): 0.09, ("ndg", 3): 0.09, ("dg", 3): 0.09, ("sd", 3): 0.09,
+           ("cpr", 4): 0.05, ("ndg", 4): 0.06, ("dg", 4): 0.04, ("sd", 4): 0.03,
+           ("fv", 1): 0.37, ("fv", 2): 0.37}
+TTE_TARGETS = (1e-4, 2e-5)
+
+
+def time_to_error(P, torch, method, k, stream, max_seconds=20.0):
+    """The second half of the BASELINE metric (configs[1]): isentropic vortex to
+    t = 1 on a grid ladder (FV NDoF-matched), L2(rho) error (reading
+    R8) and device seconds of hom2d_step per grid; T(E*) by log-log interpolation
+    between the bracketing grids (E* = 1e-4, 2e-5).  One GPU."""
+    ladder = [20, 28, 40, 57, 80, 113, 160, 226, 320, 453, 640, 905, 1280, 1810, 2560]
+    rows, spent = [], 0.0
+    for n in ladder:
+        nn = n * (k + 1) if method == "fv" else n
+        s = P.Solver(P.make_config(nn, nn, method=method, k=k, cfl=TTE_CFL[(method, k)]), stream=stream)
+        s.init_case(P.VORTEX)
+        if not rows:  # load the kernels once, untimed (lazy module loading)
+            s.step(1)
+            s.init_case(P.VORTEX)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        t, steps = s.step(10 ** 7, 1.0)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        sec = e0.elapsed_time(e1) / 1e3
+        err = s.error(P.VORTEX, 0)[1]
+        s.close()
+        rows.append({"n": nn, "l2_rho": err, "seconds": sec, "steps": steps})
+        spent += sec
+        if err <= min(TTE_TARGETS) or spent > max_seconds:
+            break
+    out = {"case": "isentropic vortex to t = 1 (BASELINE configs[1])", "cfl": TTE_CFL[(method, k)], "grids": rows}
+    for tgt in TTE_TARGETS:
+        val = None
+        for a_, b_ in zip(rows, rows[1:]):
+            if a_["l2_rho"] >= tgt >= b_["l2_rho"]:
+                la, lb = math.log(a_["l2_rho"]), math.log(b_["l2_rho"])
+                w = (math.log(tgt) - la) / (lb - la) if lb != la else 0.0
+                val = math.exp(math.log(a_["seconds"]) + w * (math.log(b_["seconds"]) - math.log(a_["seconds"])))
+                break
+        if val is None and rows and rows[0]["l2_rho"] <= tgt:
+            val = rows[0]["seconds"]
+        out[f"seconds_to_{tgt:g}"] = val
+    return out
+
+
 def traffic_from_profiles(wl):
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
@@ -210,6 +262,7 @@ def main():
     ap.add_argument("--workload", default="cpr_p3_4096", choices=sorted(WORKLOADS))
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-tte", action="store_true", help="skip the time-to-error ladder")
     args = ap.parse_args()
     assert args.warmup >= 3, "timing rules: W >= 3"
     wl = args.workload
@@ -316,6 +369,10 @@ def main():
                 "stage_avg_ms": stage_avg_ms, "bytes_per_launch": ndof_local * BYTES_PER_DOF_STEP / 3.0,
                 "stage_share_of_step": 3 * stage_avg_ms / (ms / args.steps)}
 
+    tte = None
+    if world == 1 and case == "vortex" and not args.no_tte:
+        tte = time_to_error(P, torch, method, k, stream)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         sn = 768 if method != "fv" else 3072   # ~15 s of single-core oracle work
@@ -335,6 +392,7 @@ def main():
                            "cfl": cfl, "parallelism": f"ystrip{world}",
                            "l2_flush": f"none needed: {4 * ndof_global * 8 / 1e9:.2f} GB/state array >> 126 MB L2"},
                 "e2e": e2e, "gpu_launches": gpu_launches, "roofline": roofline, "cpu_baseline": cpu,
+                "time_to_error": tte,
                 "clocks": clocks,
                 "hbm_frac_end_to_end": value * BYTES_PER_DOF_STEP / 3.0 / 1e9 / world / peak}
         print(json.dumps(line), flush=True)
