@@ -3,6 +3,8 @@
 // radial shock tube P:1043-1047), error reductions, and the
 // high-order limiter (Average Alg. 9; Limit Algs. 10-11 P:802-864;
 // Eq. (35)).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "ops_tables.h"
 
@@ -47,6 +49,18 @@ GL8v gl8() {
   return g;
 }
 
+}  // namespace
+
+bool pdl_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* v = getenv("HOM2D_NO_PDL");
+    on = (v && v[0] == '1') ? 0 : 1;
+  }
+  return on == 1;
+}
+
+namespace {
 int grid_for(long long n, int bs) {
   long long b = (n + bs - 1) / bs;
   if (b > 148 * 16) b = 148 * 16;
@@ -92,6 +106,8 @@ __device__ void case_state(const AuxArgs& A, int cid, double x, double y, double
 __global__ void k_lambda(const AuxArgs A, const double* __restrict__ q, long long npts, unsigned long long* lam,
                          unsigned long long* bad) {
   __shared__ double sred[32];
+  pdl_wait();
+  pdl_launch();
   const double gm1 = A.gamma - 1.0;
   double m = 0.0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < npts; i += (long long)gridDim.x * blockDim.x) {
@@ -107,6 +123,8 @@ __global__ void k_lambda(const AuxArgs A, const double* __restrict__ q, long lon
 // clk = {t, dt, steps, stepped, t_end}: t_end comes from device memory so that a
 // captured CUDA graph of steps does not depend on it
 __global__ void k_dt(double* clk, unsigned long long* lam, double cfl, double hmin) {
+  pdl_wait();
+  pdl_launch();
   if (clk[3] != 0.0) lam[1] = lam[0];
   lam[0] = 0ull;
   const double l = __longlong_as_double((long long)lam[1]);
@@ -218,6 +236,8 @@ __global__ void k_err_final(const double* part, int nb, double* out3) {
 }
 
 __global__ void k_avg(const AuxArgs A, Nodes nd, const double* __restrict__ q, double* qbar) {
+  pdl_wait();
+  pdl_launch();
   if (A.dt && *A.dt == 0.0) return;
   const int n = nd.n, np = n * n;
   const long long ne = (long long)A.nx * A.nrows;
@@ -381,6 +401,8 @@ template <int N, bool GLLP, bool ALL, bool CHAR>
 __global__ void __launch_bounds__(128) k_limit(const AuxArgs A, Nodes nd, double* q, const double* __restrict__ qbar,
                                                const double* qbar_lo, const double* qbar_hi, long long gcs, int bcx,
                                                double eps, long long* dec) {
+  pdl_wait();
+  pdl_launch();
   if (A.dt && *A.dt == 0.0) return;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= A.nx) return;
@@ -392,11 +414,11 @@ __global__ void __launch_bounds__(128) k_limit(const AuxArgs A, Nodes nd, double
 void launch_lambda(const AuxArgs& a, const double* q, unsigned long long* lam, unsigned long long* bad,
                    cudaStream_t s) {
   const long long npts = a.cs;
-  k_lambda<<<grid_for(npts, 256), 256, 0, s>>>(a, q, npts, lam, bad);
+  launch_pdl(k_lambda, dim3(grid_for(npts, 256)), dim3(256), 0, s, a, q, npts, lam, bad);
 }
 
 void launch_dt(double* clock, unsigned long long* lam, double cfl, double hmin, cudaStream_t s) {
-  k_dt<<<1, 1, 0, s>>>(clock, lam, cfl, hmin);
+  launch_pdl(k_dt, dim3(1), dim3(1), 0, s, clock, lam, cfl, hmin);
 }
 
 void launch_init_case(const AuxArgs& a, int case_id, double* q, cudaStream_t s) {
@@ -417,15 +439,15 @@ void launch_error_final(const double* part, int nb, double* out3, cudaStream_t s
 
 void launch_averages(const AuxArgs& a, const double* q, double* qbar, cudaStream_t s) {
   const long long ne = (long long)a.nx * a.nrows;
-  k_avg<<<grid_for(ne, 128), 128, 0, s>>>(a, nodes_for(a.method, a.k), q, qbar);
+  launch_pdl(k_avg, dim3(grid_for(ne, 128)), dim3(128), 0, s, a, nodes_for(a.method, a.k), q, qbar);
 }
 
 template <int N, bool GLLP, bool ALL, bool CHAR>
 void launch_limit_t(const AuxArgs& a, double* q, const double* qbar, const double* qbar_lo, const double* qbar_hi,
                     long long qbar_gcs, int bcx, double eps, long long* dec, cudaStream_t s) {
   dim3 grid((a.nx + 127) / 128, a.nrows < 65535 ? a.nrows : 65535);
-  k_limit<N, GLLP, ALL, CHAR><<<grid, 128, 0, s>>>(a, nodes_for(a.method, a.k), q, qbar, qbar_lo, qbar_hi, qbar_gcs,
-                                                    bcx, eps, dec);
+  launch_pdl(k_limit<N, GLLP, ALL, CHAR>, grid, dim3(128), 0, s, a, nodes_for(a.method, a.k), q, qbar, qbar_lo,
+             qbar_hi, qbar_gcs, bcx, eps, dec);
 }
 
 template <int N, bool GLLP>

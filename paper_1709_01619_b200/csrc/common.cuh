@@ -9,6 +9,15 @@
 
 namespace h2d {
 
+// Programmatic dependent launch (sm_90+): a kernel launched with the
+// programmatic-serialization attribute may become resident while its
+// predecessor in the stream drains; it must not touch global memory before
+// pdl_wait() (full completion and visibility of the predecessor).  pdl_launch()
+// lets the successor start launching once every CTA of this grid has run it.
+// Both are no-ops for an ordinary launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 struct Prim {
   double ri, u, v, p;  // 1/rho, velocities, pressure
 };

@@ -85,6 +85,8 @@ __global__ void __launch_bounds__(FTX, H2D_FV_MINB) fv_stage_kernel(const StageA
   __shared__ double sF[FTX + 1][4];   // W-face fluxes of the row (+ the strip's last E face)
   __shared__ double sXL[2][4][FTX + 2], sXH[2][4][FTX + 2];  // x face states lo/hi per cell, 2 rows
   __shared__ double sred[32];
+  pdl_wait();
+  pdl_launch();
   double dtv = 1.0;
   if (a.dt) {
     dtv = *a.dt;
@@ -287,17 +289,17 @@ int launch_fv_stage(int k, const StageArgs& a0, cudaStream_t s) {
   const int rec = k + (a.fv_unlimited ? 2 : 0);
   if (a.dec) {
     switch (rec) {
-      case 1: fv_stage_kernel<1, true><<<grid, FTX, 0, s>>>(a); break;
-      case 2: fv_stage_kernel<2, true><<<grid, FTX, 0, s>>>(a); break;
-      case 3: fv_stage_kernel<3, true><<<grid, FTX, 0, s>>>(a); break;
-      default: fv_stage_kernel<4, true><<<grid, FTX, 0, s>>>(a); break;
+      case 1: launch_pdl(fv_stage_kernel<1, true>, grid, dim3(FTX), 0, s, a); break;
+      case 2: launch_pdl(fv_stage_kernel<2, true>, grid, dim3(FTX), 0, s, a); break;
+      case 3: launch_pdl(fv_stage_kernel<3, true>, grid, dim3(FTX), 0, s, a); break;
+      default: launch_pdl(fv_stage_kernel<4, true>, grid, dim3(FTX), 0, s, a); break;
     }
   } else {
     switch (rec) {
-      case 1: fv_stage_kernel<1, false><<<grid, FTX, 0, s>>>(a); break;
-      case 2: fv_stage_kernel<2, false><<<grid, FTX, 0, s>>>(a); break;
-      case 3: fv_stage_kernel<3, false><<<grid, FTX, 0, s>>>(a); break;
-      default: fv_stage_kernel<4, false><<<grid, FTX, 0, s>>>(a); break;
+      case 1: launch_pdl(fv_stage_kernel<1, false>, grid, dim3(FTX), 0, s, a); break;
+      case 2: launch_pdl(fv_stage_kernel<2, false>, grid, dim3(FTX), 0, s, a); break;
+      case 3: launch_pdl(fv_stage_kernel<3, false>, grid, dim3(FTX), 0, s, a); break;
+      default: launch_pdl(fv_stage_kernel<4, false>, grid, dim3(FTX), 0, s, a); break;
     }
   }
   return (int)cudaPeekAtLastError();

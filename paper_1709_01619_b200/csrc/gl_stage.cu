@@ -214,11 +214,6 @@ __global__ void __launch_bounds__(L<M, K>::NT, LTile<M, K>::MINB) gl_stage_kerne
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + H::OB);
   double* sQ0 = sm + H::OQ0;
 
-  double dtv = 1.0;
-  if (a.dt) {
-    dtv = *a.dt;
-    if (dtv == 0.0) return;
-  }
   const int tid = threadIdx.x;
   const int i0 = blockIdx.x * TX, jb = a.row_lo + blockIdx.y * a.rows;
   const int TXv = min(TX, a.nx - i0), RBv = min(a.rows, a.row_hi - jb);
@@ -241,6 +236,13 @@ __global__ void __launch_bounds__(L<M, K>::NT, LTile<M, K>::MINB) gl_stage_kerne
     mbar_fence_init();
   }
   __syncthreads();
+  pdl_wait();  // everything above touched only shared memory and kernel parameters
+  pdl_launch();
+  double dtv = 1.0;  // (read after pdl_wait)
+  if (a.dt) {
+    dtv = *a.dt;
+    if (dtv == 0.0) return;
+  }
 
   auto issue_row = [&](int Lr) {
     if (tid != 0) return;
@@ -685,7 +687,7 @@ static int launch_l(const StageArgs& a, cudaStream_t s) {
   if (nr <= 0) return 0;
   b.rows = march_rows(nr, strips, H::RB);
   dim3 grid(strips, (nr + b.rows - 1) / b.rows);
-  gl_stage_kernel<M, K><<<grid, H::NT, H::SMEM, s>>>(b, tab, maps);
+  launch_pdl(gl_stage_kernel<M, K>, grid, dim3(H::NT), H::SMEM, s, b, tab, maps);
   return (int)cudaPeekAtLastError();
 }
 

@@ -215,11 +215,6 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + H::OB);
   double* sQ0 = sm + H::OQ0;
 
-  double dtv = 1.0;
-  if (a.dt) {
-    dtv = *a.dt;
-    if (dtv == 0.0) return;  // clipped-out step (t == t_end): uniform across the grid
-  }
   const int tid = threadIdx.x;
   const int i0 = blockIdx.x * TX, jb = a.row_lo + blockIdx.y * a.rows;
   const int TXv = min(TX, a.nx - i0), RBv = min(a.rows, a.row_hi - jb);
@@ -242,6 +237,13 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
     mbar_fence_init();
   }
   __syncthreads();
+  pdl_wait();  // everything above touched only shared memory and kernel parameters
+  pdl_launch();
+  double dtv = 1.0;  // (read after pdl_wait)
+  if (a.dt) {
+    dtv = *a.dt;
+    if (dtv == 0.0) return;  // clipped-out step (t == t_end): uniform across the grid
+  }
 
   // ---- streaming: thread 0 moves row L (L = 0 -> row jb-1) into stage L % NSTG ----
   auto issue_row = [&](int L) {
@@ -678,7 +680,7 @@ static int launch_g(const StageArgs& a, cudaStream_t s) {
   if (nr <= 0) return 0;
   b.rows = march_rows(nr, strips, H::RB);
   dim3 grid(strips, (nr + b.rows - 1) / b.rows);
-  gll_stage_kernel<M, K><<<grid, H::NT, H::SMEM, s>>>(b, tab, maps);
+  launch_pdl(gll_stage_kernel<M, K>, grid, dim3(H::NT), H::SMEM, s, b, tab, maps);
   return (int)cudaPeekAtLastError();
 }
 

@@ -6,6 +6,26 @@
 
 namespace h2d {
 
+// launch with programmatic stream serialization (PDL): the kernel may be
+// scheduled while its predecessor's last CTAs run; kernels call pdl_wait()
+// before any global access.  HOM2D_NO_PDL=1: ordinary launches (A/B).
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 // One RK stage (or a bare residual):  out = a0*q0 + a1*q + bcoef*dt*R(q)
 // (SSP-RK3 of P:868 in Shu-Osher form; residual mode: a0 = a1 = 0, bcoef = 1,
 // dt == nullptr).  Arrays are the local strip in the canonical SoA layout.
