@@ -198,11 +198,15 @@ __device__ __forceinline__ const void* piece_src(const double* src) {
 
 }  // namespace
 
-template <int M, int K>
+// V (stage variant, compile time): bit 0 q^n read (RK stages 2, 3), bit 1 the
+// dt wave speed / non-physical epilogue (stage 3), bit 2 fused element
+// averages (limiter runs): each launch runs only the code its stage needs
+template <int M, int K, int V>
 __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
     gll_stage_kernel(const StageArgs a, const GTab tab, const __grid_constant__ GMaps maps) {
+  constexpr bool HQ0 = V & 1, HLAM = V & 2, HAVG = V & 4;
   using H = G<M, K>;
-  constexpr int N = H::N, NP = H::NP, TX = H::TX, RB = H::RB, NT = H::NT, NSL = H::NSL;
+  constexpr int N = H::N, NP = H::NP, TX = H::TX, NT = H::NT, NSL = H::NSL;
   constexpr int CW = H::CW, CM = H::CM, CREG = H::CREG, STGA = H::STGA;
   extern __shared__ __align__(1024) double4 smem4[];  // no static smem: the window base is 1024-B aligned
   double* sm = reinterpret_cast<double*>(smem4);
@@ -340,7 +344,7 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
   };
 
   for (int L = 0; L < NSTG && L < nload; ++L) issue_row(L);
-  if (a.q0 && own)  // q^n of the first own row (step L = 1)
+  if (HQ0 && own)  // q^n of the first own row (step L = 1)
     q0_prefetch<N, NT, H::LP>(sQ0, a.q0, a.cs, ((long long)jb * a.nx + i0 + lx) * NP + b * N, tid, vec);
 
   const double* D = sT;
@@ -460,7 +464,7 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
     if (L > 0 && own) {
       const long long base = (jr * a.nx + i0 + lx) * NP + b * N;
       // q^n of the line: prefetched by cp.async one row ahead into thread-private smem
-      if (a.q0) asm volatile("cp.async.wait_group 0;" ::: "memory");
+      if (HQ0) asm volatile("cp.async.wait_group 0;" ::: "memory");
 #define Q0V(c, x) (N % 2 == 0 && vec ? sQ0[((c) * N + ((x) & ~1)) * NT + 2 * tid + ((x) & 1)] \
                                      : sQ0[((c) * N + (x)) * NT + tid])
       double F[4], jE[4];
@@ -495,7 +499,7 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
 #pragma unroll
       for (int c = 0; c < 4; ++c)
 #pragma unroll
-        for (int x = 0; x < N; ++x) q0v[c][x] = a.q0 ? Q0V(c, x) : 0.0;
+        for (int x = 0; x < N; ++x) q0v[c][x] = HQ0 ? Q0V(c, x) : 0.0;
 #pragma unroll
       for (int x = 0; x < N; ++x) {
         double v[4] = {q[0][x], q[1][x], q[2][x], q[3][x]};
@@ -550,10 +554,11 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
           const double fx = Fx[c] + gLa * jW[c] + gRa * jE[c];
           const double gy = Gy[c] + gLb * jS[c] + gRb * jN[c];
           // out = a0 q^n + a1 q + bdt R,  R = -(2/dx) fx - (2/dy) gy  (metric folded into cx, cy)
-          ov[c][x] = fma(a.a0, q0v[c][x], fma(a.a1, v[c], fma(cx, fx, cy * gy)));
+          const double rk = fma(a.a1, v[c], fma(cx, fx, cy * gy));
+          ov[c][x] = HQ0 ? fma(a.a0, q0v[c][x], rk) : rk;
         }
       }
-      if (a.lam || a.bad) {  // dt wave speed and non-physical check share one reciprocal (straight-line)
+      if (HLAM) {  // dt wave speed and non-physical check share one reciprocal (straight-line)
         unsigned long long bidx = ~0ull;
 #pragma unroll
         for (int x = 0; x < N; ++x) {
@@ -580,9 +585,9 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
           for (int x = 0; x < N; ++x) o[x] = ov[c][x];
         }
       }
-      if (a.q0 && L < RBv)  // q^n of the next row into the (now consumed) private slots
+      if (HQ0 && L < RBv)  // q^n of the next row into the (now consumed) private slots
         q0_prefetch<N, NT, H::LP>(sQ0, a.q0, a.cs, base + (long long)a.nx * NP, tid, vec);
-      if (a.qbar) {  // this line's share of the element average: w_b sum_x w_x q
+      if (HAVG) {  // this line's share of the element average: w_b sum_x w_x q
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           double sx = 0.0;
@@ -592,7 +597,7 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
         }
       }
     }
-    if (a.qbar && (N == 2 || N == 4)) {  // element averages: the element's N lines are N aligned lanes
+    if (HAVG && (N == 2 || N == 4)) {  // element averages: the element's N lines are N aligned lanes
       // lanes of this warp that exist (NT need not be a multiple of 32; element lane groups are whole)
       const unsigned wmask = (NT % 32 == 0 || (tid >> 5) < NT / 32) ? 0xffffffffu : ((1u << (NT % 32)) - 1u);
 #pragma unroll
@@ -604,7 +609,7 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
 #pragma unroll
         for (int c = 0; c < 4; ++c) a.qbar[c * ne + m] = 0.25 * lpart[c];
       }
-    } else if (a.qbar) {  // element averages (N = 3, 5: through the W-face buffer)
+    } else if (HAVG) {  // element averages (N = 3, 5: through the W-face buffer)
       __syncthreads();
       if (L > 0 && own) st4(sFW + (lx * N + b) * 4, lpart);
       __syncthreads();
@@ -624,7 +629,7 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
       issue_row(L + NSTG);
     }
   }
-  if (a.lam) block_max_to(lam, a.lam, sm + H::ORD);
+  if (HLAM && a.lam) block_max_to(lam, a.lam, sm + H::ORD);
 }
 
 // ---- host: tensor maps (P3 path) ------------------------------------------------------
@@ -657,14 +662,20 @@ bool make_map(CUtensorMap* m, const double* base, long long nelem, long long cs,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int M, int K>
-static int launch_g(const StageArgs& a, cudaStream_t s) {
+template <int M, int K, int V>
+static void launch_v(dim3 grid, const StageArgs& b, const GTab& tab, const GMaps& maps, cudaStream_t s) {
   using H = G<M, K>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(gll_stage_kernel<M, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)H::SMEM);
+    cudaFuncSetAttribute(gll_stage_kernel<M, K, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)H::SMEM);
     attr = true;
   }
+  launch_pdl(gll_stage_kernel<M, K, V>, grid, dim3(H::NT), H::SMEM, s, b, tab, maps);
+}
+
+template <int M, int K>
+static int launch_g(const StageArgs& a, cudaStream_t s) {
+  using H = G<M, K>;
   static const GTab tab = make_gtab<K>();
   GMaps maps;
   memset(&maps, 0, sizeof(maps));
@@ -680,7 +691,15 @@ static int launch_g(const StageArgs& a, cudaStream_t s) {
   if (nr <= 0) return 0;
   b.rows = march_rows(nr, strips, H::RB);
   dim3 grid(strips, (nr + b.rows - 1) / b.rows);
-  launch_pdl(gll_stage_kernel<M, K>, grid, dim3(H::NT), H::SMEM, s, b, tab, maps);
+  const int v = (a.q0 ? 1 : 0) | ((a.lam || a.bad) ? 2 : 0) | (a.qbar ? 4 : 0);
+  switch (v) {
+    case 0: launch_v<M, K, 0>(grid, b, tab, maps, s); break;
+    case 1: launch_v<M, K, 1>(grid, b, tab, maps, s); break;
+    case 3: launch_v<M, K, 3>(grid, b, tab, maps, s); break;
+    case 4: launch_v<M, K, 4>(grid, b, tab, maps, s); break;
+    case 5: launch_v<M, K, 5>(grid, b, tab, maps, s); break;
+    default: launch_v<M, K, 7>(grid, b, tab, maps, s); break;
+  }
   return (int)cudaPeekAtLastError();
 }
 
