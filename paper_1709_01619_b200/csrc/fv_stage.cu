@@ -79,8 +79,11 @@ __device__ __forceinline__ void rusanov2(const double qL[4], const double qR[4],
 #ifndef H2D_FV_MINB
 #define H2D_FV_MINB 4  // 124 registers, no spills (A/B: +12 % over 3)
 #endif
-template <int ORDER, bool REC>
+// V (stage variant, compile time): bit 0 q^n read, bit 1 dt / non-physical epilogue
+template <int ORDER, bool REC, int V>
 __global__ void __launch_bounds__(FTX, H2D_FV_MINB) fv_stage_kernel(const StageArgs a) {
+  // V == 8: any other combination, decided at run time from the pointers
+  const bool HQ0 = V == 8 ? a.q0 != nullptr : (V & 1), HLAM = V == 8 ? (a.lam || a.bad) : (V & 2) != 0;
   __shared__ double ring[FNS][4][FW];
   __shared__ double sF[FTX + 1][4];   // W-face fluxes of the row (+ the strip's last E face)
   __shared__ double sXL[2][4][FTX + 2], sXH[2][4][FTX + 2];  // x face states lo/hi per cell, 2 rows
@@ -201,7 +204,7 @@ __global__ void __launch_bounds__(FTX, H2D_FV_MINB) fv_stage_kernel(const StageA
     const int sc = slot_of(r);
     const long long gidx = (long long)(jb + r) * a.nx + (i0 + tid);
     double q0v[4] = {0, 0, 0, 0};
-    if (own && a.q0) {
+    if (HQ0 && own) {
 #pragma unroll
       for (int c = 0; c < 4; ++c) q0v[c] = a.q0[c * a.cs + gidx];
     }
@@ -253,14 +256,14 @@ __global__ void __launch_bounds__(FTX, H2D_FV_MINB) fv_stage_kernel(const StageA
         a.out[c * a.cs + gidx] = v;
         GS[c] = GN[c];
       }
-      if (a.lam || a.bad) {
+      if (HLAM) {
         const Prim w = prims(o, gm1);
         lam = fmax(lam, fmax(fabs(w.u), fabs(w.v)) + fsqrt(gam * w.p * w.ri));
         if (a.bad && !admissible(o[0], w.p)) atomicMin(a.bad, (unsigned long long)gidx);
       }
     }
   }
-  if (a.lam) block_max_to(lam, a.lam, sred);
+  if (HLAM && a.lam) block_max_to(lam, a.lam, sred);
 }
 
 int march_rows(int nrows, int strips, int rb_max) {
@@ -277,6 +280,26 @@ int march_rows(int nrows, int strips, int rb_max) {
   return (int)rows;
 }
 
+template <int ORDER, bool REC>
+static void fv_launch_v(int v, dim3 grid, const StageArgs& a, cudaStream_t s) {
+  switch (v) {
+    case 0: launch_pdl(fv_stage_kernel<ORDER, REC, 0>, grid, dim3(FTX), 0, s, a); break;
+    case 1: launch_pdl(fv_stage_kernel<ORDER, REC, 1>, grid, dim3(FTX), 0, s, a); break;
+    case 3: launch_pdl(fv_stage_kernel<ORDER, REC, 3>, grid, dim3(FTX), 0, s, a); break;
+    default: launch_pdl(fv_stage_kernel<ORDER, REC, 8>, grid, dim3(FTX), 0, s, a); break;
+  }
+}
+
+template <bool REC>
+static void fv_launch_r(int rec, int v, dim3 grid, const StageArgs& a, cudaStream_t s) {
+  switch (rec) {
+    case 1: fv_launch_v<1, REC>(v, grid, a, s); break;
+    case 2: fv_launch_v<2, REC>(v, grid, a, s); break;
+    case 3: fv_launch_v<3, REC>(v, grid, a, s); break;
+    default: fv_launch_v<4, REC>(v, grid, a, s); break;
+  }
+}
+
 int launch_fv_stage(int k, const StageArgs& a0, cudaStream_t s) {
   StageArgs a = a0;
   const int strips = (a.nx + FTX - 1) / FTX;
@@ -287,21 +310,9 @@ int launch_fv_stage(int k, const StageArgs& a0, cudaStream_t s) {
   // reconstruction: 1 MUSCL-2, 2 MUSCL-3 (minmod-limited); 3 / 4 the same
   // kappa-schemes unlimited (hom2d_config.fv_unlimited, f3)
   const int rec = k + (a.fv_unlimited ? 2 : 0);
-  if (a.dec) {
-    switch (rec) {
-      case 1: launch_pdl(fv_stage_kernel<1, true>, grid, dim3(FTX), 0, s, a); break;
-      case 2: launch_pdl(fv_stage_kernel<2, true>, grid, dim3(FTX), 0, s, a); break;
-      case 3: launch_pdl(fv_stage_kernel<3, true>, grid, dim3(FTX), 0, s, a); break;
-      default: launch_pdl(fv_stage_kernel<4, true>, grid, dim3(FTX), 0, s, a); break;
-    }
-  } else {
-    switch (rec) {
-      case 1: launch_pdl(fv_stage_kernel<1, false>, grid, dim3(FTX), 0, s, a); break;
-      case 2: launch_pdl(fv_stage_kernel<2, false>, grid, dim3(FTX), 0, s, a); break;
-      case 3: launch_pdl(fv_stage_kernel<3, false>, grid, dim3(FTX), 0, s, a); break;
-      default: launch_pdl(fv_stage_kernel<4, false>, grid, dim3(FTX), 0, s, a); break;
-    }
-  }
+  const int v = (a.q0 ? 1 : 0) | ((a.lam || a.bad) ? 2 : 0);
+  if (a.dec) fv_launch_r<true>(rec, v, grid, a, s);
+  else fv_launch_r<false>(rec, v, grid, a, s);
   return (int)cudaPeekAtLastError();
 }
 

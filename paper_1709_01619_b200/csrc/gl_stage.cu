@@ -196,9 +196,14 @@ __device__ __forceinline__ const void* piece_src(const double* src) {
 
 }  // namespace
 
-template <int M, int K>
+// V (stage variant, compile time): bit 0 q^n read, bit 1 dt / non-physical
+// epilogue, bit 2 fused element averages (as gll_stage_kernel)
+template <int M, int K, int V>
 __global__ void __launch_bounds__(L<M, K>::NT, LTile<M, K>::MINB) gl_stage_kernel(const StageArgs a, const LTab tab,
                                                                const __grid_constant__ LMaps maps) {
+  // V == 8: any other combination, decided at run time from the pointers
+  const bool HQ0 = V == 8 ? a.q0 != nullptr : (V & 1), HLAM = V == 8 ? (a.lam || a.bad) : (V & 2) != 0,
+             HAVG = V == 8 ? a.qbar != nullptr : (V & 4) != 0;
   using H = L<M, K>;
   using T = LOps<K>;
   constexpr int N = H::N, NP = H::NP, TX = H::TX, NT = H::NT, NSL = H::NSL;
@@ -349,7 +354,7 @@ __global__ void __launch_bounds__(L<M, K>::NT, LTile<M, K>::MINB) gl_stage_kerne
   };
 
   for (int Lr = 0; Lr < NSTG && Lr < nload; ++Lr) issue_row(Lr);
-  if (a.q0 && own)  // q^n of the first own row
+  if (HQ0 && own)  // q^n of the first own row
     q0_prefetch<N, NT>(sQ0, a.q0, a.cs, ((long long)jb * a.nx + i0 + lx) * NP + b * N, tid, vec);
 
   double lam = 0.0;
@@ -522,7 +527,7 @@ __global__ void __launch_bounds__(L<M, K>::NT, LTile<M, K>::MINB) gl_stage_kerne
 
     if (Lr > 0 && own) {
       const long long base = (jr * a.nx + i0 + lx) * NP + b * N;
-      if (a.q0) asm volatile("cp.async.wait_group 0;" ::: "memory");
+      if (HQ0) asm volatile("cp.async.wait_group 0;" ::: "memory");
 #define Q0V(c, x) (N % 2 == 0 && vec ? sQ0[((c) * N + ((x) & ~1)) * NT + 2 * tid + ((x) & 1)] \
                                      : sQ0[((c) * N + (x)) * NT + tid])
       double FW[4], FE[4];
@@ -536,7 +541,7 @@ __global__ void __launch_bounds__(L<M, K>::NT, LTile<M, K>::MINB) gl_stage_kerne
 #pragma unroll
       for (int c = 0; c < 4; ++c)
 #pragma unroll
-        for (int x = 0; x < N; ++x) q0v[c][x] = a.q0 ? Q0V(c, x) : 0.0;
+        for (int x = 0; x < N; ++x) q0v[c][x] = HQ0 ? Q0V(c, x) : 0.0;
 #pragma unroll
       for (int x = 0; x < N; ++x) {
         double v[4] = {q[0][x], q[1][x], q[2][x], q[3][x]};
@@ -587,9 +592,9 @@ __global__ void __launch_bounds__(L<M, K>::NT, LTile<M, K>::MINB) gl_stage_kerne
           }
         }
 #pragma unroll
-        for (int c = 0; c < 4; ++c) ov[c][x] = fma(a.a0, q0v[c][x], fma(a.a1, v[c], R[c]));
+        for (int c = 0; c < 4; ++c) ov[c][x] = HQ0 ? fma(a.a0, q0v[c][x], fma(a.a1, v[c], R[c])) : fma(a.a1, v[c], R[c]);
       }
-      if (a.lam || a.bad) {  // dt wave speed and non-physical check (straight-line)
+      if (HLAM) {  // dt wave speed and non-physical check (straight-line)
         unsigned long long bidx = ~0ull;
 #pragma unroll
         for (int x = 0; x < N; ++x) {
@@ -617,9 +622,9 @@ __global__ void __launch_bounds__(L<M, K>::NT, LTile<M, K>::MINB) gl_stage_kerne
           for (int x = 0; x < N; ++x) o[x] = ov[c][x];
         }
       }
-      if (a.q0 && Lr < RBv)  // q^n of the next row into the consumed private slots
+      if (HQ0 && Lr < RBv)  // q^n of the next row into the consumed private slots
         q0_prefetch<N, NT>(sQ0, a.q0, a.cs, base + (long long)a.nx * NP, tid, vec);
-      if (a.qbar) {  // this line's share of the element average: w_b sum_x w_x q
+      if (HAVG) {  // this line's share of the element average: w_b sum_x w_x q
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           double sx = 0.0;
@@ -629,7 +634,7 @@ __global__ void __launch_bounds__(L<M, K>::NT, LTile<M, K>::MINB) gl_stage_kerne
         }
       }
     }
-    if (a.qbar && (N == 2 || N == 4)) {  // element averages: the element's N lines are N aligned lanes
+    if (HAVG && (N == 2 || N == 4)) {  // element averages: the element's N lines are N aligned lanes
       // lanes of this warp that exist (NT need not be a multiple of 32; element lane groups are whole)
       const unsigned wmask = (NT % 32 == 0 || (tid >> 5) < NT / 32) ? 0xffffffffu : ((1u << (NT % 32)) - 1u);
 #pragma unroll
@@ -641,7 +646,7 @@ __global__ void __launch_bounds__(L<M, K>::NT, LTile<M, K>::MINB) gl_stage_kerne
 #pragma unroll
         for (int c = 0; c < 4; ++c) a.qbar[c * ne + m] = 0.25 * lpart[c];
       }
-    } else if (a.qbar) {  // element averages (N = 3, 5: through the W-face buffer)
+    } else if (HAVG) {  // element averages (N = 3, 5: through the W-face buffer)
       __syncthreads();
       if (Lr > 0 && own) st4(sFW + (lx * N + b) * 4, lpart);
       __syncthreads();
@@ -661,17 +666,23 @@ __global__ void __launch_bounds__(L<M, K>::NT, LTile<M, K>::MINB) gl_stage_kerne
       issue_row(Lr + NSTG);
     }
   }
-  if (a.lam) block_max_to(lam, a.lam, sm + H::ORD);
+  if (HLAM && a.lam) block_max_to(lam, a.lam, sm + H::ORD);
+}
+
+template <int M, int K, int V>
+static void launch_lv(dim3 grid, const StageArgs& b, const LTab& tab, const LMaps& maps, cudaStream_t s) {
+  using H = L<M, K>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(gl_stage_kernel<M, K, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)H::SMEM);
+    attr = true;
+  }
+  launch_pdl(gl_stage_kernel<M, K, V>, grid, dim3(H::NT), H::SMEM, s, b, tab, maps);
 }
 
 template <int M, int K>
 static int launch_l(const StageArgs& a, cudaStream_t s) {
   using H = L<M, K>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(gl_stage_kernel<M, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)H::SMEM);
-    attr = true;
-  }
   static const LTab tab = make_ltab<K>();
   LMaps maps;
   memset(&maps, 0, sizeof(maps));
@@ -687,7 +698,15 @@ static int launch_l(const StageArgs& a, cudaStream_t s) {
   if (nr <= 0) return 0;
   b.rows = march_rows(nr, strips, H::RB);
   dim3 grid(strips, (nr + b.rows - 1) / b.rows);
-  launch_pdl(gl_stage_kernel<M, K>, grid, dim3(H::NT), H::SMEM, s, b, tab, maps);
+  const int v = (a.q0 ? 1 : 0) | ((a.lam || a.bad) ? 2 : 0) | (a.qbar ? 4 : 0);
+  switch (v) {
+    case 0: launch_lv<M, K, 0>(grid, b, tab, maps, s); break;
+    case 1: launch_lv<M, K, 1>(grid, b, tab, maps, s); break;
+    case 3: launch_lv<M, K, 3>(grid, b, tab, maps, s); break;
+    case 4: launch_lv<M, K, 4>(grid, b, tab, maps, s); break;
+    case 5: launch_lv<M, K, 5>(grid, b, tab, maps, s); break;
+    default: launch_lv<M, K, 8>(grid, b, tab, maps, s); break;
+  }
   return (int)cudaPeekAtLastError();
 }
 

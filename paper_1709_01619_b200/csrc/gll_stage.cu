@@ -204,7 +204,9 @@ __device__ __forceinline__ const void* piece_src(const double* src) {
 template <int M, int K, int V>
 __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
     gll_stage_kernel(const StageArgs a, const GTab tab, const __grid_constant__ GMaps maps) {
-  constexpr bool HQ0 = V & 1, HLAM = V & 2, HAVG = V & 4;
+  // V == 8: any other combination, decided at run time from the pointers
+  const bool HQ0 = V == 8 ? a.q0 != nullptr : (V & 1), HLAM = V == 8 ? (a.lam || a.bad) : (V & 2) != 0,
+             HAVG = V == 8 ? a.qbar != nullptr : (V & 4) != 0;
   using H = G<M, K>;
   constexpr int N = H::N, NP = H::NP, TX = H::TX, NT = H::NT, NSL = H::NSL;
   constexpr int CW = H::CW, CM = H::CM, CREG = H::CREG, STGA = H::STGA;
@@ -698,7 +700,7 @@ static int launch_g(const StageArgs& a, cudaStream_t s) {
     case 3: launch_v<M, K, 3>(grid, b, tab, maps, s); break;
     case 4: launch_v<M, K, 4>(grid, b, tab, maps, s); break;
     case 5: launch_v<M, K, 5>(grid, b, tab, maps, s); break;
-    default: launch_v<M, K, 7>(grid, b, tab, maps, s); break;
+    default: launch_v<M, K, 8>(grid, b, tab, maps, s); break;
   }
   return (int)cudaPeekAtLastError();
 }
