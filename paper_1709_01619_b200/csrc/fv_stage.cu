@@ -283,10 +283,10 @@ int march_rows(int nrows, int strips, int rb_max) {
 template <int ORDER, bool REC>
 static void fv_launch_v(int v, dim3 grid, const StageArgs& a, cudaStream_t s) {
   switch (v) {
-    case 0: launch_pdl(fv_stage_kernel<ORDER, REC, 0>, grid, dim3(FTX), 0, s, a); break;
-    case 1: launch_pdl(fv_stage_kernel<ORDER, REC, 1>, grid, dim3(FTX), 0, s, a); break;
-    case 3: launch_pdl(fv_stage_kernel<ORDER, REC, 3>, grid, dim3(FTX), 0, s, a); break;
-    default: launch_pdl(fv_stage_kernel<ORDER, REC, 8>, grid, dim3(FTX), 0, s, a); break;
+    case 0: launch_pdl_if(!a.no_pdl, fv_stage_kernel<ORDER, REC, 0>, grid, dim3(FTX), 0, s, a); break;
+    case 1: launch_pdl_if(!a.no_pdl, fv_stage_kernel<ORDER, REC, 1>, grid, dim3(FTX), 0, s, a); break;
+    case 3: launch_pdl_if(!a.no_pdl, fv_stage_kernel<ORDER, REC, 3>, grid, dim3(FTX), 0, s, a); break;
+    default: launch_pdl_if(!a.no_pdl, fv_stage_kernel<ORDER, REC, 8>, grid, dim3(FTX), 0, s, a); break;
   }
 }
 

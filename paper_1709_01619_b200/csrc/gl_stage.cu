@@ -677,7 +677,7 @@ static void launch_lv(dim3 grid, const StageArgs& b, const LTab& tab, const LMap
     cudaFuncSetAttribute(gl_stage_kernel<M, K, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)H::SMEM);
     attr = true;
   }
-  launch_pdl(gl_stage_kernel<M, K, V>, grid, dim3(H::NT), H::SMEM, s, b, tab, maps);
+  launch_pdl_if(!b.no_pdl, gl_stage_kernel<M, K, V>, grid, dim3(H::NT), H::SMEM, s, b, tab, maps);
 }
 
 template <int M, int K>

@@ -672,7 +672,7 @@ static void launch_v(dim3 grid, const StageArgs& b, const GTab& tab, const GMaps
     cudaFuncSetAttribute(gll_stage_kernel<M, K, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)H::SMEM);
     attr = true;
   }
-  launch_pdl(gll_stage_kernel<M, K, V>, grid, dim3(H::NT), H::SMEM, s, b, tab, maps);
+  launch_pdl_if(!b.no_pdl, gll_stage_kernel<M, K, V>, grid, dim3(H::NT), H::SMEM, s, b, tab, maps);
 }
 
 template <int M, int K>

@@ -284,6 +284,7 @@ hom2d_status run_stage(hom2d* h, const double* q, const double* q0, double* out,
     StageArgs lo = s, hi = s;
     lo.row_lo = 0; lo.row_hi = G;
     hi.row_lo = h->nrows - G; hi.row_hi = h->nrows;
+    lo.no_pdl = hi.no_pdl = async ? 1 : 0;  // they follow the wait on the exchange stream's event
     if (!e) e = launch_stage(h, lo);
     if (!e) e = launch_stage(h, hi);
     h->launches += 3;

@@ -11,8 +11,8 @@ namespace h2d {
 // before any global access.  HOM2D_NO_PDL=1: ordinary launches (A/B).
 bool pdl_enabled();
 template <typename... KArgs, typename... Args>
-cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
-                       Args... args) {
+cudaError_t launch_pdl_if(bool pdl, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                          Args... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
@@ -22,8 +22,13 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cfg.numAttrs = (pdl && pdl_enabled()) ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args... args) {
+  return launch_pdl_if(true, kernel, grid, block, smem, s, args...);
 }
 
 // One RK stage (or a bare residual):  out = a0*q0 + a1*q + bcoef*dt*R(q)
@@ -52,6 +57,8 @@ struct StageArgs {
   double* qbar;            // optional (HO limiter runs): element averages of `out`, [4][nx*nrows]
                            // (Alg. 9: 1/4 sum_ab w_a w_b q_ab), fused into the stage epilogue
   int fv_unlimited;        // FV: unlimited kappa-scheme (hom2d_config.fv_unlimited)
+  int no_pdl;              // launch without programmatic serialization (after a cross-stream
+                           // event wait: griddepcontrol.wait only covers the previous kernel)
   int row_lo, row_hi;      // this launch updates strip rows [row_lo, row_hi) (row_hi == 0: all rows);
                           // it may read rows row_lo-G .. row_hi+G-1 (ghost rows outside the strip)
   int rows;                // marching kernels: element rows per CTA (set by the launcher)
