@@ -51,14 +51,13 @@ GL8v gl8() {
 
 }  // namespace
 
-bool pdl_enabled() {
-  static int on = -1;
-  if (on < 0) {
-    const char* v = getenv("HOM2D_NO_PDL");
-    on = (v && v[0] == '1') ? 0 : 1;
-  }
-  return on == 1;
+static int g_pdl_on = 1;
+// (re)read HOM2D_NO_PDL; called at every hom2d_create
+void pdl_refresh() {
+  const char* v = getenv("HOM2D_NO_PDL");
+  g_pdl_on = (v && v[0] == '1') ? 0 : 1;
 }
+bool pdl_enabled() { return g_pdl_on == 1; }
 
 namespace {
 int grid_for(long long n, int bs) {

@@ -398,6 +398,7 @@ hom2d_status hom2d_create(const hom2d_config* cfg, const hom2d_dist* dist, void*
   {
     const char* ng = getenv("HOM2D_NO_GRAPH");  // A/B: eager launches instead of CUDA graphs
     h->graph_off = ng && ng[0] == '1';
+    pdl_refresh();
   }
   cudaError_t ce = cudaSetDevice(h->device);
   if (ce != cudaSuccess) { delete h; return HOM2D_ERR_CUDA; }

@@ -10,6 +10,7 @@ namespace h2d {
 // scheduled while its predecessor's last CTAs run; kernels call pdl_wait()
 // before any global access.  HOM2D_NO_PDL=1: ordinary launches (A/B).
 bool pdl_enabled();
+void pdl_refresh();
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl_if(bool pdl, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                           Args... args) {

@@ -96,3 +96,22 @@ def test_graph_replay_bitwise_equals_eager(orc, P, monkeypatch, method, k, limit
     (qa, *ra), (qb, *rb) = out
     np.testing.assert_array_equal(qa, qb)
     assert ra == rb
+
+
+@pytest.mark.parametrize("method,k,limiter", [("cpr", 3, 0), ("sd", 2, 0), ("fv", 2, 0), ("dg", 1, 1)])
+def test_programmatic_launch_bitwise_equals_plain(orc, P, monkeypatch, method, k, limiter):
+    """Programmatic dependent launches (each kernel waits on griddepcontrol.wait)
+    give bitwise the state of ordinary stream-ordered launches."""
+    box, bc, case, cfl = ((-1.0, 1.0, -1.0, 1.0), 1, P.SHOCK, 0.2) if limiter else ((-5.0, 5.0, -5.0, 5.0), 0,
+                                                                                   P.VORTEX, 0.08)
+    out = []
+    for no_pdl in ("0", "1"):
+        monkeypatch.setenv("HOM2D_NO_PDL", no_pdl)  # read at hom2d_create
+        s = P.Solver(P.make_config(40, 32, method=method, k=k, bc=bc, box=box, cfl=cfl, limiter=limiter))
+        s.init_case(case)
+        s.step(60)
+        out.append(s.get_state())
+        s.close()
+    monkeypatch.setenv("HOM2D_NO_PDL", "0")
+    P.Solver(P.make_config(8, 8)).close()  # leave PDL on for the tests that follow
+    np.testing.assert_array_equal(out[0], out[1])
