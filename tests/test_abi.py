@@ -89,3 +89,30 @@ def test_missing_extension_fails_loudly(tmp_path):
             P.load(str(tmp_path / "nope.so"))
     finally:
         P._lib = saved
+
+
+@pytest.mark.parametrize("kw,status", [
+    (dict(method="cpr", k=5), 3),                 # HOM2D_ERR_ORDER: k outside 1..4
+    (dict(method="cpr", k=0), 3),
+    (dict(method="fv", k=3), 3),                  # FV: 1 = MUSCL-2, 2 = MUSCL-3
+    (dict(method=7, k=1), 1),                     # HOM2D_ERR_ARG: unknown method
+    (dict(nx=1), 2),                              # HOM2D_ERR_MESH: nx < 2
+    (dict(box=(1.0, 1.0, 0.0, 1.0)), 2),          # degenerate box
+    (dict(gamma=1.0), 1),                         # gamma must exceed 1
+    (dict(cfl=0.0), 1),
+    (dict(bc=2), 1),
+    (dict(limiter_per_step=2), 1),                # variant switches are 0/1
+    (dict(fv_unlimited=5), 1),
+    (dict(limiter_characteristic=-1), 1),
+])
+def test_config_validation_status(kw, status):
+    """hom2d_strip_plan validates the config on the host exactly as hom2d_create
+    does: each bad field maps to its documented status (include/hom2d.h)."""
+    import paper_1709_01619_b200 as P
+    args = dict(nx=8, ny=8, method="cpr", k=1)
+    args.update(kw)
+    nx, ny = args.pop("nx"), args.pop("ny")
+    cfg = P.make_config(nx, ny, **args)
+    with pytest.raises(P.Hom2dError) as e:
+        P.strip_plan(cfg, 0, 1)
+    assert e.value.status == status
