@@ -53,7 +53,17 @@ __device__ __forceinline__ void cell_faces(double qm, double q0, double qp, doub
   } else {  // kappa = 1/3, beta = (3 - kappa)/(1 - kappa) = 4
     constexpr double kap = 1.0 / 3.0, beta = (3.0 - kap) / (1.0 - kap);
     const double dm = q0 - qm, dp = qp - q0;
-    const double A = minmod2(dm, beta * dp, dec, w), B = minmod2(dp, beta * dm, dec, w);
+    double A, B;
+    if (dec) {
+      A = minmod2(dm, beta * dp, dec, w);
+      B = minmod2(dp, beta * dm, dec, w);
+    } else {  // both minmods share the sign test (beta > 0): one sign-bit comparison
+      const double bdp = beta * dp, bdm = beta * dm;
+      const bool same = (__double2hiint(dm) ^ __double2hiint(dp)) >= 0;
+      const double ma = fabs(dm) <= fabs(bdp) ? dm : bdp, mb = fabs(dp) <= fabs(bdm) ? dp : bdm;
+      A = same ? ma : 0.0;
+      B = same ? mb : 0.0;
+    }
     hi = __fma_rn(0.25, __fma_rn(1.0 - kap, A, __dmul_rn(1.0 + kap, B)), q0);
     lo = __fma_rn(-0.25, __fma_rn(1.0 - kap, B, __dmul_rn(1.0 + kap, A)), q0);
   }
