@@ -44,8 +44,9 @@ __device__ __forceinline__ void cell_faces(double qm, double q0, double qp, doub
   } else if (ORDER == 4) {  // unlimited kappa = 1/3 (f3 variant of MUSCL-3)
     constexpr double kap = 1.0 / 3.0;
     const double dm = q0 - qm, dp = qp - q0;
-    hi = __fma_rn(0.25, __fma_rn(1.0 - kap, dm, __dmul_rn(1.0 + kap, dp)), q0);
-    lo = __fma_rn(-0.25, __fma_rn(1.0 - kap, dp, __dmul_rn(1.0 + kap, dm)), q0);
+    constexpr double c1 = 0.25 * (1.0 - kap), c2 = 0.25 * (1.0 + kap);
+    hi = __fma_rn(c1, dm, __fma_rn(c2, dp, q0));
+    lo = __fma_rn(-c1, dp, __fma_rn(-c2, dm, q0));
   } else if (ORDER == 1) {
     const double s = minmod2(q0 - qm, qp - q0, dec, w);
     hi = __fma_rn(0.5, s, q0);
@@ -64,8 +65,10 @@ __device__ __forceinline__ void cell_faces(double qm, double q0, double qp, doub
       A = same ? ma : 0.0;
       B = same ? mb : 0.0;
     }
-    hi = __fma_rn(0.25, __fma_rn(1.0 - kap, A, __dmul_rn(1.0 + kap, B)), q0);
-    lo = __fma_rn(-0.25, __fma_rn(1.0 - kap, B, __dmul_rn(1.0 + kap, A)), q0);
+    // q0 +- ((1 - kappa) X + (1 + kappa) Y) / 4 with the quarter folded into the weights
+    constexpr double c1 = 0.25 * (1.0 - kap), c2 = 0.25 * (1.0 + kap);
+    hi = __fma_rn(c1, A, __fma_rn(c2, B, q0));
+    lo = __fma_rn(-c1, B, __fma_rn(-c2, A, q0));
   }
 }
 
