@@ -8,6 +8,13 @@
 #include "common.cuh"
 #include "ops_tables.h"
 
+// k_limit: 8 CTAs/SM (<= 64 registers) for P1/P2 -- the per-element limit branch
+// is rare, its spills are cheap, detection wants the occupancy (+11 % on the
+// shock-tube steps); P3/P4 at 4 (their limit branch spills heavily at 8)
+#ifndef H2D_LIMIT_MINB
+#define H2D_LIMIT_MINB (N <= 3 ? 8 : 4)
+#endif
+
 namespace h2d {
 
 namespace {
@@ -397,7 +404,7 @@ __device__ __forceinline__ void limit_element(const AuxArgs& A, const Nodes& nd,
 }
 
 template <int N, bool GLLP, bool ALL, bool CHAR>
-__global__ void __launch_bounds__(128) k_limit(const AuxArgs A, Nodes nd, double* q, const double* __restrict__ qbar,
+__global__ void __launch_bounds__(128, H2D_LIMIT_MINB) k_limit(const AuxArgs A, Nodes nd, double* q, const double* __restrict__ qbar,
                                                const double* qbar_lo, const double* qbar_hi, long long gcs, int bcx,
                                                double eps, long long* dec) {
   pdl_wait();
