@@ -296,27 +296,39 @@ __device__ __forceinline__ void char_slopes(const double qb[4], const double dp[
   s[3] = (H - c * un) * w[0] + q2 * w[1] + ut * w[2] + (H + c * un) * w[3];
 }
 
-template <int N, bool GLLP, bool ALL, bool CHAR>
-__device__ __forceinline__ void limit_element(const AuxArgs& A, const Nodes& nd, double* q,
-                                              const double* __restrict__ qbar, const double* qbar_lo,
-                                              const double* qbar_hi, long long gcs, int bcx, double eps,
-                                              long long* dec, int i, int j) {
-  constexpr int NP = N * N;
-  const long long ne = (long long)A.nx * A.nrows, m = (long long)j * A.nx + i;
-  const double dx = (A.xmax - A.xmin) / A.nx, dy = (A.ymax - A.ymin) / A.ny_global;
-  int iw = i - 1, ie = i + 1;
-  bool hw = true, he = true;
-  if (iw < 0) { if (bcx) hw = false; else iw += A.nx; }
-  if (ie >= A.nx) { if (bcx) he = false; else ie -= A.nx; }
-  // neighbour averages of component c (own average at a transmissive boundary)
-  auto nbr = [&](int c, double own, double& W, double& E, double& S, double& Nn) {
+// neighbour averages of component c of element (i, j) (own average at a transmissive boundary)
+struct Nbr {
+  const AuxArgs& A;
+  const double* __restrict__ qbar;
+  const double *qbar_lo, *qbar_hi;
+  long long gcs, ne, m;
+  int i, j, iw, ie;
+  bool hw, he;
+  __device__ Nbr(const AuxArgs& A_, const double* __restrict__ qb, const double* lo, const double* hi, long long g,
+                 int bcx, int i_, int j_)
+      : A(A_), qbar(qb), qbar_lo(lo), qbar_hi(hi), gcs(g), ne((long long)A_.nx * A_.nrows),
+        m((long long)j_ * A_.nx + i_), i(i_), j(j_), iw(i_ - 1), ie(i_ + 1), hw(true), he(true) {
+    if (iw < 0) { if (bcx) hw = false; else iw += A.nx; }
+    if (ie >= A.nx) { if (bcx) he = false; else ie -= A.nx; }
+  }
+  __device__ void operator()(int c, double own, double& W, double& E, double& S, double& Nn) const {
     W = hw ? qbar[c * ne + (long long)j * A.nx + iw] : own;
     E = he ? qbar[c * ne + (long long)j * A.nx + ie] : own;
     if (j > 0) S = qbar[c * ne + m - A.nx];
     else S = qbar_lo ? qbar_lo[c * gcs + i] : own;
     if (j < A.nrows - 1) Nn = qbar[c * ne + m + A.nx];
     else Nn = qbar_hi ? qbar_hi[c * gcs + i] : own;
-  };
+  }
+};
+
+// Alg. 10: does element (i, j) trip the detector?  (loads only: the detections of
+// several elements of one thread overlap their memory latency)
+template <int N, bool GLLP, bool ALL>
+__device__ __forceinline__ bool detect_element(const AuxArgs& A, const Nodes& nd, const double* __restrict__ q,
+                                               const Nbr& nbr, double eps) {
+  constexpr int NP = N * N;
+  const long long ne = nbr.ne, m = nbr.m;
+  const double* __restrict__ qbar = nbr.qbar;
   const double qb = qbar[m];
   double rW, rE, rS, rN;
   nbr(0, qb, rW, rE, rS, rN);
@@ -366,16 +378,26 @@ __device__ __forceinline__ void limit_element(const AuxArgs& A, const Nodes& nd,
       trip |= (fabs(qw - ew) > eps) | (fabs(qe_ - ee) > eps) | (fabs(qs - es) > eps) | (fabs(qn - en) > eps);
     }
   }
-  if (!trip) return;
+  return trip;
+}
+
+// Alg. 11 / Eq. (35) on a marked element: minmod slopes of the neighbour-average
+// differences, per component or (CHAR, f3 variant of Q12) per characteristic
+// field of the average; all four components rebuilt
+template <int N, bool CHAR>
+__device__ __forceinline__ void rebuild_element(const AuxArgs& A, const Nodes& nd, double* __restrict__ q,
+                                             const Nbr& nbr, long long* dec) {
+  constexpr int NP = N * N;
+  const long long ne = nbr.ne, m = nbr.m;
+  const double* __restrict__ qbar = nbr.qbar;
+  const double dx = (A.xmax - A.xmin) / A.nx, dy = (A.ymax - A.ymin) / A.ny_global;
   if (dec) atomicAdd((unsigned long long*)&dec[0], 1ull);
-  // Eq. (35): minmod slopes of the neighbour-average differences, per component
-  // or (CHAR, f3 variant of Q12) per characteristic field of the average
   double qv[4], dE[4], dW[4], dN[4], dS[4], sx[4], sy[4];
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
-    const double qc = c == 0 ? qb : qbar[c * ne + m];
+    const double qc = qbar[c * ne + m];
     double W, E, S, Nn;
-    if (c == 0) { W = rW; E = rE; S = rS; Nn = rN; } else nbr(c, qc, W, E, S, Nn);
+    nbr(c, qc, W, E, S, Nn);
     qv[c] = qc;
     dE[c] = (E - qc) / dx;
     dW[c] = (qc - W) / dx;
@@ -403,17 +425,34 @@ __device__ __forceinline__ void limit_element(const AuxArgs& A, const Nodes& nd,
   }
 }
 
+// rows of elements per thread: the detections of a thread's LROWS elements issue
+// their loads back to back (and with the dt flag's), one memory round trip for all
+#ifndef H2D_LROWS
+#define H2D_LROWS(N) ((N) <= 3 ? 2 : 1)
+#endif
+
 template <int N, bool GLLP, bool ALL, bool CHAR>
-__global__ void __launch_bounds__(128, H2D_LIMIT_MINB) k_limit(const AuxArgs A, Nodes nd, double* q, const double* __restrict__ qbar,
-                                               const double* qbar_lo, const double* qbar_hi, long long gcs, int bcx,
-                                               double eps, long long* dec) {
+__global__ void __launch_bounds__(128, H2D_LIMIT_MINB) k_limit(const AuxArgs A, Nodes nd, double* __restrict__ q,
+                                                               const double* __restrict__ qbar,
+                                                               const double* qbar_lo, const double* qbar_hi,
+                                                               long long gcs, int bcx, double eps, long long* dec) {
+  constexpr int R = H2D_LROWS(N);
   pdl_wait();
   pdl_launch();
-  if (A.dt && *A.dt == 0.0) return;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= A.nx) return;
-  for (int j = blockIdx.y; j < A.nrows; j += gridDim.y)
-    limit_element<N, GLLP, ALL, CHAR>(A, nd, q, qbar, qbar_lo, qbar_hi, gcs, bcx, eps, dec, i, j);
+  const bool done = A.dt && *A.dt == 0.0;  // past t_end (graph replay): no writes
+  for (int j0 = blockIdx.y * R; j0 < A.nrows; j0 += gridDim.y * R) {
+    bool trip[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      trip[r] = j0 + r < A.nrows &&
+                detect_element<N, GLLP, ALL>(A, nd, q, Nbr(A, qbar, qbar_lo, qbar_hi, gcs, bcx, i, j0 + r), eps);
+    if (done) return;
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (trip[r]) rebuild_element<N, CHAR>(A, nd, q, Nbr(A, qbar, qbar_lo, qbar_hi, gcs, bcx, i, j0 + r), dec);
+  }
 }
 }  // namespace
 
@@ -451,7 +490,8 @@ void launch_averages(const AuxArgs& a, const double* q, double* qbar, cudaStream
 template <int N, bool GLLP, bool ALL, bool CHAR>
 void launch_limit_t(const AuxArgs& a, double* q, const double* qbar, const double* qbar_lo, const double* qbar_hi,
                     long long qbar_gcs, int bcx, double eps, long long* dec, cudaStream_t s) {
-  dim3 grid((a.nx + 127) / 128, a.nrows < 65535 ? a.nrows : 65535);
+  const int ry = (a.nrows + H2D_LROWS(N) - 1) / H2D_LROWS(N);
+  dim3 grid((a.nx + 127) / 128, ry < 65535 ? ry : 65535);
   launch_pdl(k_limit<N, GLLP, ALL, CHAR>, grid, dim3(128), 0, s, a, nodes_for(a.method, a.k), q, qbar, qbar_lo,
              qbar_hi, qbar_gcs, bcx, eps, dec);
 }
