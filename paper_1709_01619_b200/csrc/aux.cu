@@ -321,6 +321,26 @@ struct Nbr {
   }
 };
 
+// minmod3(a, b, c) with (b, c) fixed: the value of minmod3 for any
+// a, its pair (b, c) reduced once.  Same value as the three-way form whenever
+// every argument is nonzero (the smallest magnitude of the three when all signs
+// agree, else 0); with a zero argument both give a signed zero (and qbar -+ 0 is
+// qbar), so the detector's decisions are identical.  Sign tests on the high
+// words (integer pipe), one fp64 magnitude compare per edge point.
+struct MM3 {
+  double B;  // the smaller-magnitude of b, c (its sign is the pair's common sign)
+  bool same;
+  __device__ __forceinline__ MM3(double b, double c) {
+    const int hb = __double2hiint(b), hc = __double2hiint(c);
+    same = (hb ^ hc) >= 0;
+    B = fabs(b) <= fabs(c) ? b : c;
+  }
+  __device__ __forceinline__ double operator()(double a) const {
+    const bool ok = same && (__double2hiint(a) ^ __double2hiint(B)) >= 0;
+    return ok ? (fabs(a) <= fabs(B) ? a : B) : 0.0;
+  }
+};
+
 // Alg. 10: does element (i, j) trip the detector?  (loads only: the detections of
 // several elements of one thread overlap their memory latency)
 template <int N, bool GLLP, bool ALL>
@@ -340,6 +360,9 @@ __device__ __forceinline__ bool detect_element(const AuxArgs& A, const Nodes& nd
       cb = qbar[c * ne + m];
       nbr(c, cb, cW, cE, cS, cN);
     }
+    // the neighbour-difference arguments of minmod3 are the element's, shared by
+    // its 2N edge points along each axis: reduce them once
+    const MM3 mx(cE - cb, cb - cW), my(cN - cb, cb - cS);
     double r[NP];
     const double* Qc = q + c * A.cs + m * NP;
     if constexpr (NP % 4 == 0) {  // P1, P3: the element's values as 32-B vectors (32-B aligned: cs, NP % 4 == 0)
@@ -371,10 +394,10 @@ __device__ __forceinline__ bool detect_element(const AuxArgs& A, const Nodes& nd
         }
       }
       // right/top side: q_e = qbar + mm(q_l - qbar, ...); left/bottom: qbar - mm(qbar - q_l, ...)
-      const double ew = cb - minmod3(cb - qw, cE - cb, cb - cW);
-      const double ee = cb + minmod3(qe_ - cb, cE - cb, cb - cW);
-      const double es = cb - minmod3(cb - qs, cN - cb, cb - cS);
-      const double en = cb + minmod3(qn - cb, cN - cb, cb - cS);
+      const double ew = cb - mx(cb - qw);
+      const double ee = cb + mx(qe_ - cb);
+      const double es = cb - my(cb - qs);
+      const double en = cb + my(qn - cb);
       trip |= (fabs(qw - ew) > eps) | (fabs(qe_ - ee) > eps) | (fabs(qs - es) > eps) | (fabs(qn - en) > eps);
     }
   }
