@@ -337,7 +337,9 @@ struct MM3 {
   }
   __device__ __forceinline__ double operator()(double a) const {
     const bool ok = same && (__double2hiint(a) ^ __double2hiint(B)) >= 0;
-    return ok ? (fabs(a) <= fabs(B) ? a : B) : 0.0;
+    const double m = fabs(a) <= fabs(B) ? a : B;
+    // 0 by masking the bits (the compiler would branch on a select here)
+    return __longlong_as_double(__double_as_longlong(m) & -(long long)ok);
   }
 };
 
@@ -409,11 +411,10 @@ __device__ __forceinline__ bool detect_element(const AuxArgs& A, const Nodes& nd
 // field of the average; all four components rebuilt
 template <int N, bool CHAR>
 __device__ __forceinline__ void rebuild_element(const AuxArgs& A, const Nodes& nd, double* __restrict__ q,
-                                             const Nbr& nbr, long long* dec) {
+                                             const Nbr& nbr, double dx, double dy, long long* dec) {
   constexpr int NP = N * N;
   const long long ne = nbr.ne, m = nbr.m;
   const double* __restrict__ qbar = nbr.qbar;
-  const double dx = (A.xmax - A.xmin) / A.nx, dy = (A.ymax - A.ymin) / A.ny_global;
   if (dec) atomicAdd((unsigned long long*)&dec[0], 1ull);
   double qv[4], dE[4], dW[4], dN[4], dS[4], sx[4], sy[4];
 #pragma unroll
@@ -458,7 +459,8 @@ template <int N, bool GLLP, bool ALL, bool CHAR>
 __global__ void __launch_bounds__(128, H2D_LIMIT_MINB) k_limit(const AuxArgs A, Nodes nd, double* __restrict__ q,
                                                                const double* __restrict__ qbar,
                                                                const double* qbar_lo, const double* qbar_hi,
-                                                               long long gcs, int bcx, double eps, long long* dec) {
+                                                               long long gcs, int bcx, double eps, double dx,
+                                                               double dy, long long* dec) {
   constexpr int R = H2D_LROWS(N);
   pdl_wait();
   pdl_launch();
@@ -474,7 +476,8 @@ __global__ void __launch_bounds__(128, H2D_LIMIT_MINB) k_limit(const AuxArgs A, 
     if (done) return;
 #pragma unroll
     for (int r = 0; r < R; ++r)
-      if (trip[r]) rebuild_element<N, CHAR>(A, nd, q, Nbr(A, qbar, qbar_lo, qbar_hi, gcs, bcx, i, j0 + r), dec);
+      if (trip[r])
+        rebuild_element<N, CHAR>(A, nd, q, Nbr(A, qbar, qbar_lo, qbar_hi, gcs, bcx, i, j0 + r), dx, dy, dec);
   }
 }
 }  // namespace
@@ -515,8 +518,10 @@ void launch_limit_t(const AuxArgs& a, double* q, const double* qbar, const doubl
                     long long qbar_gcs, int bcx, double eps, long long* dec, cudaStream_t s) {
   const int ry = (a.nrows + H2D_LROWS(N) - 1) / H2D_LROWS(N);
   dim3 grid((a.nx + 127) / 128, ry < 65535 ? ry : 65535);
+  // element widths (Eq. (35)) in host IEEE double: bitwise the device's quotient
+  const double dx = (a.xmax - a.xmin) / a.nx, dy = (a.ymax - a.ymin) / a.ny_global;
   launch_pdl(k_limit<N, GLLP, ALL, CHAR>, grid, dim3(128), 0, s, a, nodes_for(a.method, a.k), q, qbar, qbar_lo,
-             qbar_hi, qbar_gcs, bcx, eps, dec);
+             qbar_hi, qbar_gcs, bcx, eps, dx, dy, dec);
 }
 
 template <int N, bool GLLP>
