@@ -16,6 +16,7 @@
 //  * flux differences, the SSP-RK combination, the dt wave speed and the
 //    non-physical check are fused; one coalesced store per component.
 #include "common.cuh"
+#include "tma.cuh"
 
 namespace h2d {
 
@@ -89,6 +90,12 @@ __device__ __forceinline__ void rusanov2(const double qL[4], const double qR[4],
 }
 }  // namespace
 
+#ifndef H2D_FV_ASYNC
+#define H2D_FV_ASYNC 1  // ring rows by cp.async, two rows in flight (0: register-staged, one row)
+#endif
+#ifndef H2D_FV_Q0PF
+#define H2D_FV_Q0PF 0  // q^n loaded one row ahead into registers (A/B)
+#endif
 #ifndef H2D_FV_MINB
 #define H2D_FV_MINB 4  // 124 registers, no spills (A/B: +12 % over 3)
 #endif
@@ -132,6 +139,37 @@ __global__ void __launch_bounds__(FTX, H2D_FV_MINB) fv_stage_kernel(const StageA
     }
     return a.q + (long long)jr * a.nx;
   };
+  auto slot_of = [&](int r) { return ((r % FNS) + FNS) % FNS; };  // r = row - jb
+#if H2D_FV_ASYNC
+  // this thread's ring column(s) of row jr (own cell: slot tid + 2; threads 0..3
+  // also a halo slot) copied by cp.async straight into ring slot `slot`: no
+  // register staging, so two rows stay in flight (the ring's FNS = 5 slots hold
+  // rows r .. r+4; rows r-2, r-1 are dead once row r starts)
+  auto issue_row = [&](int jr, int slot) {
+    long long cs;
+    const double* rb = row_ptr(jr, cs);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      if (own)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(&ring[slot][c][tid + 2])),
+                     "l"(rb + c * cs + i0 + tid)
+                     : "memory");
+      if (tid < 4)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(&ring[slot][c][tid < 2 ? tid : TXv + tid])),
+                     "l"(rb + c * cs + hx)
+                     : "memory");
+    }
+  };
+  auto commit = [] { asm volatile("cp.async.commit_group;" ::: "memory"); };
+  // prologue: rows jb-2 .. jb+1 (group 0), jb+2 (group 1); rows jb+3, jb+4 go
+  // into the slots of rows jb-2, jb-1 once the prologue below has read them
+  for (int r = -2; r <= 1; ++r) issue_row(jb + r, slot_of(r));
+  commit();
+  issue_row(jb + 2, slot_of(2));
+  commit();
+  asm volatile("cp.async.wait_group 1;" ::: "memory");
+  __syncthreads();
+#else
   // this thread's ring column(s): own cell (slot tid + 2), threads 0..3 also a halo slot
   auto load_row = [&](int jr, double v[4], double h[4]) {
     long long cs;
@@ -158,7 +196,7 @@ __global__ void __launch_bounds__(FTX, H2D_FV_MINB) fv_stage_kernel(const StageA
   }
   load_row(jb + 2, pv, ph);
   __syncthreads();
-  auto slot_of = [&](int r) { return ((r % FNS) + FNS) % FNS; };  // r = row - jb
+#endif
 
   // y reconstruction once per cell: the hi (N-side) state of the row below the
   // current one is carried in registers.  Decision weights: an own row stands
@@ -209,18 +247,49 @@ __global__ void __launch_bounds__(FTX, H2D_FV_MINB) fv_stage_kernel(const StageA
   double lam = 0.0;
   const double bdt = a.bcoef * dtv;
   const double hrdx = 0.5 * a.rdx2, hrdy = 0.5 * a.rdy2;
+#if H2D_FV_Q0PF
+  double q0n[4] = {0, 0, 0, 0};
+  if (HQ0 && own) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) q0n[c] = __ldg(a.q0 + c * a.cs + (long long)jb * a.nx + i0 + tid);
+  }
+#endif
   for (int r = 0; r < RBv; ++r) {
+#if H2D_FV_ASYNC
+    // row r+2 has landed (this thread's copies; the barrier publishes everyone's);
+    // after the barrier row r-1's slot is dead: row r+4 goes there (at r = 0
+    // also row 3, into row -2's slot)
+    if (r == 0) asm volatile("cp.async.wait_group 0;" ::: "memory");
+    else asm volatile("cp.async.wait_group 1;" ::: "memory");
+    __syncthreads();
+    if (r == 0) {
+      if (3 <= RBv + 1) issue_row(jb + 3, slot_of(3));
+      commit();
+    }
+    if (r + 4 <= RBv + 1) issue_row(jb + r + 4, slot_of(r + 4));
+    commit();
+#else
     // the prefetched row r+2 enters the ring; prefetch row r+3
     store_row(slot_of(r + 2), pv, ph);
     if (r + 3 <= RBv + 1) load_row(jb + r + 3, pv, ph);
     __syncthreads();
+#endif
     const int sc = slot_of(r);
     const long long gidx = (long long)(jb + r) * a.nx + (i0 + tid);
+#if H2D_FV_Q0PF
+    // q^n of row r was loaded one row ahead; load row r+1's now
+    double q0v[4] = {q0n[0], q0n[1], q0n[2], q0n[3]};
+    if (HQ0 && own && r + 1 < RBv) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) q0n[c] = __ldg(a.q0 + c * a.cs + gidx + a.nx);
+    }
+#else
     double q0v[4] = {0, 0, 0, 0};
     if (HQ0 && own) {
 #pragma unroll
       for (int c = 0; c < 4; ++c) q0v[c] = a.q0[c * a.cs + gidx];
     }
+#endif
     // x faces (the W face of each own cell, from the face states reconstructed one
     // row earlier) and the N face of the column (carried hi state of row r, lo
     // state of row r+1 reconstructed now from rows r..r+2; its hi state is
