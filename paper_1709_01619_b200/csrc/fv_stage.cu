@@ -24,7 +24,10 @@ namespace {
 #ifndef H2D_FTX
 #define H2D_FTX 128  // A/B: 64 at 8 CTAs/SM -5 %; 256 exceeds the static smem limit
 #endif
-constexpr int FTX = H2D_FTX, FRB = 64, FNS = 5;   // cells per strip, rows per march, ring rows
+#ifndef H2D_FV_DEPTH
+#define H2D_FV_DEPTH 3  // ring rows in flight (cp.async; A/B: 3 vs 2 +1 % at MUSCL-3, 46 KB static smem)
+#endif
+constexpr int FTX = H2D_FTX, FRB = 64, FD = H2D_FV_DEPTH, FNS = 3 + FD;  // cells/strip, rows/march, in flight, ring rows
 constexpr int FW = FTX + 4;                    // ring row width: 2 halo cells each side
 
 // the two reconstructed face values of cell i (stencil i-1, i, i+1): lo at its
@@ -93,9 +96,6 @@ __device__ __forceinline__ void rusanov2(const double qL[4], const double qR[4],
 #ifndef H2D_FV_ASYNC
 #define H2D_FV_ASYNC 1  // ring rows by cp.async, two rows in flight (0: register-staged, one row)
 #endif
-#ifndef H2D_FV_Q0PF
-#define H2D_FV_Q0PF 0  // q^n loaded one row ahead into registers (A/B)
-#endif
 #ifndef H2D_FV_MINB
 #define H2D_FV_MINB 4  // 124 registers, no spills (A/B: +12 % over 3)
 #endif
@@ -143,8 +143,8 @@ __global__ void __launch_bounds__(FTX, H2D_FV_MINB) fv_stage_kernel(const StageA
 #if H2D_FV_ASYNC
   // this thread's ring column(s) of row jr (own cell: slot tid + 2; threads 0..3
   // also a halo slot) copied by cp.async straight into ring slot `slot`: no
-  // register staging, so two rows stay in flight (the ring's FNS = 5 slots hold
-  // rows r .. r+4; rows r-2, r-1 are dead once row r starts)
+  // register staging, so FD rows stay in flight (the ring's FNS = 3 + FD slots
+  // hold rows r .. r+2+FD; rows r-2, r-1 are dead once row r starts)
   auto issue_row = [&](int jr, int slot) {
     long long cs;
     const double* rb = row_ptr(jr, cs);
@@ -247,26 +247,22 @@ __global__ void __launch_bounds__(FTX, H2D_FV_MINB) fv_stage_kernel(const StageA
   double lam = 0.0;
   const double bdt = a.bcoef * dtv;
   const double hrdx = 0.5 * a.rdx2, hrdy = 0.5 * a.rdy2;
-#if H2D_FV_Q0PF
-  double q0n[4] = {0, 0, 0, 0};
-  if (HQ0 && own) {
-#pragma unroll
-    for (int c = 0; c < 4; ++c) q0n[c] = __ldg(a.q0 + c * a.cs + (long long)jb * a.nx + i0 + tid);
-  }
-#endif
   for (int r = 0; r < RBv; ++r) {
 #if H2D_FV_ASYNC
     // row r+2 has landed (this thread's copies; the barrier publishes everyone's);
     // after the barrier row r-1's slot is dead: row r+4 goes there (at r = 0
     // also row 3, into row -2's slot)
     if (r == 0) asm volatile("cp.async.wait_group 0;" ::: "memory");
-    else asm volatile("cp.async.wait_group 1;" ::: "memory");
+    else asm volatile("cp.async.wait_group %0;" ::"n"(FD - 1) : "memory");
     __syncthreads();
     if (r == 0) {
-      if (3 <= RBv + 1) issue_row(jb + 3, slot_of(3));
-      commit();
+#pragma unroll
+      for (int k = 3; k < 2 + FD; ++k) {
+        if (k <= RBv + 1) issue_row(jb + k, slot_of(k));
+        commit();
+      }
     }
-    if (r + 4 <= RBv + 1) issue_row(jb + r + 4, slot_of(r + 4));
+    if (r + 2 + FD <= RBv + 1) issue_row(jb + r + 2 + FD, slot_of(r + 2 + FD));
     commit();
 #else
     // the prefetched row r+2 enters the ring; prefetch row r+3
@@ -276,20 +272,11 @@ __global__ void __launch_bounds__(FTX, H2D_FV_MINB) fv_stage_kernel(const StageA
 #endif
     const int sc = slot_of(r);
     const long long gidx = (long long)(jb + r) * a.nx + (i0 + tid);
-#if H2D_FV_Q0PF
-    // q^n of row r was loaded one row ahead; load row r+1's now
-    double q0v[4] = {q0n[0], q0n[1], q0n[2], q0n[3]};
-    if (HQ0 && own && r + 1 < RBv) {
-#pragma unroll
-      for (int c = 0; c < 4; ++c) q0n[c] = __ldg(a.q0 + c * a.cs + gidx + a.nx);
-    }
-#else
     double q0v[4] = {0, 0, 0, 0};
     if (HQ0 && own) {
 #pragma unroll
       for (int c = 0; c < 4; ++c) q0v[c] = a.q0[c * a.cs + gidx];
     }
-#endif
     // x faces (the W face of each own cell, from the face states reconstructed one
     // row earlier) and the N face of the column (carried hi state of row r, lo
     // state of row r+1 reconstructed now from rows r..r+2; its hi state is
