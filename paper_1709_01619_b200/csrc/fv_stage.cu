@@ -25,7 +25,7 @@ namespace {
 #define H2D_FTX 128  // A/B: 64 at 8 CTAs/SM -5 %; 256 exceeds the static smem limit
 #endif
 #ifndef H2D_FV_DEPTH
-#define H2D_FV_DEPTH 3  // ring rows in flight (cp.async; A/B: 3 vs 2 +1 % at MUSCL-3, 46 KB static smem)
+#define H2D_FV_DEPTH 2  // ring rows in flight (cp.async); 3 is +1 % at 4 CTAs/SM but its 46 KB keep 5 out
 #endif
 constexpr int FTX = H2D_FTX, FRB = 64, FD = H2D_FV_DEPTH, FNS = 3 + FD;  // cells/strip, rows/march, in flight, ring rows
 constexpr int FW = FTX + 4;                    // ring row width: 2 halo cells each side
@@ -97,7 +97,7 @@ __device__ __forceinline__ void rusanov2(const double qL[4], const double qR[4],
 #define H2D_FV_ASYNC 1  // ring rows by cp.async, two rows in flight (0: register-staged, one row)
 #endif
 #ifndef H2D_FV_MINB
-#define H2D_FV_MINB 4  // 124 registers, no spills (A/B: +12 % over 3)
+#define H2D_FV_MINB 5  // 96 registers, no spills, 5 x 42 KB smem (A/B: +1.5 % over 4 at depth 3; 4 was +12 % over 3)
 #endif
 // V (stage variant, compile time): bit 0 q^n read, bit 1 dt / non-physical epilogue
 template <int ORDER, bool REC, int V>
