@@ -321,11 +321,12 @@ struct Nbr {
   }
 };
 
-// minmod3(a, b, c) with (b, c) fixed: the value of minmod3 for any
-// a, its pair (b, c) reduced once.  Same value as the three-way form whenever
-// every argument is nonzero (the smallest magnitude of the three when all signs
-// agree, else 0); with a zero argument both give a signed zero (and qbar -+ 0 is
-// qbar), so the detector's decisions are identical.  Sign tests on the high
+// minmod3(a, b, c) with (b, c) fixed: minmod3 = min(a, b, c) if all
+// three are > 0, max(a, b, c) if all are < 0, else 0 (the oracle's form); here
+// the pair (b, c) is reduced once per element and direction.  Same value as the
+// three-way form whenever every argument is nonzero (the smallest magnitude of
+// the three when all signs agree, else 0); with a zero argument both give a
+// signed zero (and qbar -+ 0 is qbar), so the detector's decisions are identical.  Sign tests on the high
 // words (integer pipe), one fp64 magnitude compare per edge point.
 struct MM3 {
   double B;  // the smaller-magnitude of b, c (its sign is the pair's common sign)

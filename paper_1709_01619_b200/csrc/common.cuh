@@ -204,10 +204,4 @@ __device__ __forceinline__ double minmod2(double a, double b, long long* dec, in
   return r;
 }
 
-__device__ __forceinline__ double minmod3(double a, double b, double c) {
-  if (a > 0.0 && b > 0.0 && c > 0.0) return fmin(a, fmin(b, c));
-  if (a < 0.0 && b < 0.0 && c < 0.0) return fmax(a, fmax(b, c));
-  return 0.0;
-}
-
 }  // namespace h2d
