@@ -39,6 +39,9 @@ template <int K> struct GTile;
 // CTAs per SM (register cap 64K / (MINB x threads)) and strip widths, A/B-timed on
 // 4096^2 / 8192^2 (round 1): P1 MINB 4 (+9 % over 2), P2 MINB 4 (+41 % over 2),
 // P4 12-element strips (60 threads) at 4 CTAs/SM (+18-23 % over 16 at 2, +25 % over 32 at 1)
+#ifndef H2D_P1V2
+#define H2D_P1V2 1  // CPR P1 1-D path: 16-B pair loads of lines and element rows (+2 %, shock +4.7 %)
+#endif
 #ifndef H2D_MINB1
 #define H2D_MINB1 4
 #endif
@@ -305,6 +308,7 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
     int dW, dM, dE;  // 1-D path offsets of component 0 (odd component strides flip them)
     int csodd;
     bool have;
+    bool v2;  // 1-D path: every component's own piece 16-B aligned (P1 pairs load as double2)
   };
   auto view = [&](int L) {
     RowView v;
@@ -319,7 +323,12 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
       v.dW = piece_off(rb + (long long)iw * NP);
       v.dE = piece_off(rb + (long long)ie * NP);
     }
+    v.v2 = H2D_P1V2 && M == GM_CPR && N == 2 && !H::SWZ && (((v.dM | v.csodd) & 1) == 0);  // NDG: -0.8 %
     return v;
+  };
+  // address of (c, p) of own element slot e on the 1-D path (N == 2 pair loads)
+  auto own_ptr = [&](const RowView& v, int c, int e, int p) -> const double* {
+    return v.st + c * CREG + CW + (v.dM ^ (c & v.csodd)) + (e - 1) * NP + p;
   };
   // value (c, p) of own element slot e = lx + 1 (hot path: no branches)
   auto own_at = [&](const RowView& v, int c, int e, int p) -> double {
@@ -391,6 +400,12 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
                     vc.st + (c * H::RSW + lx + 1) * 16 + (((2 * b + (x >> 1)) ^ ((lx + 1) & 7)) << 1));
                 q[c][x] = u.x;
                 q[c][x + 1] = u.y;
+              }
+            } else if (N == 2 && vc.v2) {  // P1: the line's two points as one 16-B load
+              if (x == 0) {
+                const double2 u = *reinterpret_cast<const double2*>(own_ptr(vc, c, lx + 1, b * N));
+                q[c][0] = u.x;
+                q[c][1 % N] = u.y;
               }
             } else {
               q[c][x] = own_at(vc, c, lx + 1, b * N + x);
@@ -497,6 +512,23 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
             }
         }
       }
+      // CPR P1 (1-D path, aligned): eta-derivatives of both points of the line
+      // from the element's rows as 16-B pairs (same operation order as below)
+      double dy2[N][4];
+      if constexpr (M == GM_CPR && N == 2 && !H::SWZ) {
+        if (vc.v2) {
+#pragma unroll
+          for (int l = 0; l < N; ++l) {
+            const double db = D[b * N + l];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              const double2 u = *reinterpret_cast<const double2*>(own_ptr(vc, c, lx + 1, l * N));
+              dy2[0][c] = l == 0 ? db * u.x : fma(db, u.x, dy2[0][c]);
+              dy2[1 % N][c] = l == 0 ? db * u.y : fma(db, u.y, dy2[1 % N][c]);
+            }
+          }
+        }
+      }
       double ov[4][N], q0v[4][N];  // q^n of the line (0 in stage 1: a0 = 0)
 #pragma unroll
       for (int c = 0; c < 4; ++c)
@@ -513,6 +545,11 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
             if (l == 0) {
 #pragma unroll
               for (int c = 0; c < 4; ++c) dy[c] = dyall[x][c];
+            }
+          } else if (M == GM_CPR && N == 2 && vc.v2) {
+            if (l == 0) {
+#pragma unroll
+              for (int c = 0; c < 4; ++c) dy[c] = dy2[x][c];
             }
           } else if (M == GM_CPR) {
 #pragma unroll
