@@ -335,14 +335,14 @@ __global__ void __launch_bounds__(FTX, H2D_FV_MINB) fv_stage_kernel(const StageA
   if (HLAM && a.lam) block_max_to(lam, a.lam, sred);
 }
 
-int march_rows(int nrows, int strips, int rb_max) {
+int march_rows(int nrows, int strips, int rb_max, int ctas_per_sm) {
   static int nsm = 0;
   if (!nsm) {
     int dev = 0;
     cudaGetDevice(&dev);
     if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || nsm <= 0) nsm = 148;
   }
-  const long long target = 4LL * nsm;
+  const long long target = (long long)ctas_per_sm * nsm;
   long long rows = ((long long)nrows * strips + target - 1) / target;
   if (rows > rb_max) rows = rb_max;
   if (rows < 1) rows = 1;  // small grids: short marches, more CTAs (latency-bound sizes)
@@ -374,7 +374,7 @@ int launch_fv_stage(int k, const StageArgs& a0, cudaStream_t s) {
   const int strips = (a.nx + FTX - 1) / FTX;
   const int nr = row_range(a);
   if (nr <= 0) return 0;
-  a.rows = march_rows(nr, strips, FRB);
+  a.rows = march_rows(nr, strips, FRB, H2D_FV_MINB);
   dim3 grid(strips, (nr + a.rows - 1) / a.rows);
   // reconstruction: 1 MUSCL-2, 2 MUSCL-3 (minmod-limited); 3 / 4 the same
   // kappa-schemes unlimited (hom2d_config.fv_unlimited, f3)

@@ -71,10 +71,11 @@ inline int row_range(StageArgs& a) {
   return a.row_hi - a.row_lo;
 }
 
-// rows per CTA for a marching kernel: enough CTAs to fill the GPU (>= 4 per SM),
-// at most rb_max (each march re-reads 1-2 prologue rows: long marches on big
-// grids, short ones -- down to 1 row -- on the latency-bound small grids)
-int march_rows(int nrows, int strips, int rb_max);
+// rows per CTA for a marching kernel: enough CTAs to fill the GPU (ctas_per_sm
+// resident per SM), at most rb_max (each march re-reads 1-2 prologue rows: long
+// marches on big grids, short ones -- down to 1 row -- on the latency-bound
+// small grids)
+int march_rows(int nrows, int strips, int rb_max, int ctas_per_sm = 4);
 
 // host: 3-D TMA tensor map {16 points, nelem elements, 4 components} (fp64,
 // box {16, box_e, 1}, 128-B swizzle) over an element-row array; base == nullptr
