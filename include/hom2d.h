@@ -173,6 +173,20 @@ hom2d_status hom2d_time(const hom2d* h, double* t);
  * difference within 1e-12 of the switch point; not counted in 1-3), [5-7] 0. */
 hom2d_status hom2d_decisions(hom2d* h, int64_t* counts8);
 
+/* Per-element decision map accumulated since create/set_state/init_case
+ * (record_decisions = 1, nranks == 1; SURVEY C12 "per-element dumps"): host
+ * array out[n], n = nx * ny, element m = j*nx + i.
+ *   HO limiter runs: out[m] = number of limiter passes (Alg. 10-11)
+ *     that marked element m.
+ *   FV (MUSCL + minmod): the outcomes of the minmods that limit cell
+ *     m's own slopes (both directions, all components, each face side once, as
+ *     in counts8[1..4]), packed as  sum over outcomes of 1 << (16 * slot),
+ *     slot 0 -> 0, 1 -> first argument, 2 -> second argument, 3 -> tie.  A
+ *     reconstruction of a ghost cell counts for the cell it copies (periodic
+ *     wrap / transmissive clamp).
+ * HOM2D_ERR_STATE without record_decisions or with nranks > 1. */
+hom2d_status hom2d_decision_map(hom2d* h, int64_t* out, int64_t n);
+
 /* Kernel launches issued by this handle since create (bench accounting). */
 int64_t hom2d_launch_count(const hom2d* h);
 

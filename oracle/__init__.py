@@ -81,6 +81,7 @@ def lib():
         L.orc_muscl_face_unlimited.argtypes = [C.c_int, vp, vp, vp, vp, vp, vp]
         L.orc_char_vectors.argtypes = [cfgp, C.c_int, vp, vp, vp]
         L.orc_residual.argtypes = [cfgp, vp, vp, vp]
+        L.orc_residual_map.argtypes = [cfgp, vp, vp, vp, vp]
         L.orc_averages.argtypes = [cfgp, vp, vp]
         L.orc_limit.argtypes = [cfgp, vp, vp, vp]
         L.orc_max_wave_speed.argtypes = [cfgp, vp]
@@ -89,6 +90,7 @@ def lib():
         L.orc_dt.restype = d
         L.orc_ssprk3.argtypes = [vp, i64, d, vp, vp, vp]
         L.orc_run.argtypes = [cfgp, vp, i32, d, P(d), P(i64), vp]
+        L.orc_run_map.argtypes = [cfgp, vp, i32, d, P(d), P(i64), vp, vp]
         L.orc_vortex_state.argtypes = [cfgp, d, d, d, vp]
         L.orc_shock_state.argtypes = [cfgp, d, d, vp]
         L.orc_init_case.argtypes = [cfgp, C.c_int, vp]
@@ -202,9 +204,12 @@ def muscl_face(order, qm1, q0, q1, q2, unlimited=False):
     return qW, qE
 
 
-def residual(cfg, q, counts=None):
+def residual(cfg, q, counts=None, emap=None):
+    """R(q).  emap (int64 per cell, FV): per-cell minmod outcomes accumulated
+    (1 << 16*slot; slot 0 -> 0, 1 -> first argument, 2 -> second, 3 tie)."""
     q = _v4(q); r = np.zeros_like(q)
-    _chk(lib().orc_residual(C.byref(cfg), _p(q), _p(r), _p(counts) if counts is not None else None))
+    _chk(lib().orc_residual_map(C.byref(cfg), _p(q), _p(r), _p(counts) if counts is not None else None,
+                                _p(emap) if emap is not None else None))
     return r
 
 
@@ -248,12 +253,16 @@ def ssprk3(q, dt, rhs):
     return q
 
 
-def run(cfg, q, max_steps, t_end=float("inf"), t0=0.0, counts=None):
-    """March; returns (q, t, steps).  Raises on non-physical state."""
+def run(cfg, q, max_steps, t_end=float("inf"), t0=0.0, counts=None, emap=None):
+    """March; returns (q, t, steps).  Raises on non-physical state.  emap (int64
+    per element, accumulated): HO limiter runs -- the number of limiter passes
+    that marked the element; FV -- per-cell minmod outcomes (see residual)."""
     q = np.array(q, dtype=np.float64, copy=True)
     t = C.c_double(t0); s = C.c_int64(0)
-    st = lib().orc_run(C.byref(cfg), _p(q), int(max_steps), float(t_end), C.byref(t), C.byref(s),
-                       _p(counts) if counts is not None else None)
+    if emap is not None:
+        assert emap.dtype == np.int64 and emap.size == cfg.nx * cfg.ny
+    st = lib().orc_run_map(C.byref(cfg), _p(q), int(max_steps), float(t_end), C.byref(t), C.byref(s),
+                           _p(counts) if counts is not None else None, _p(emap) if emap is not None else None)
     if st == 4:
         raise FloatingPointError("oracle: non-physical state")
     _chk(st)

@@ -349,16 +349,20 @@ void orc_char_vectors(const orc_config *cf, int dir, const double *q, double *R1
 /* ------------------------------------------------------------------------- */
 /* minmod (Q17)                                                         */
 /* ------------------------------------------------------------------------- */
-static double mm2(double a, double b, int64_t *cnt) {
+/* cell: optional per-cell decision map entry (SURVEY C12 dumps): the outcome is
+ * added as 1 << (16 * slot), slot 0 -> 0, 1 -> first argument, 2 -> second, 3 tie */
+static double mm2c(double a, double b, int64_t *cnt, int64_t *cell) {
   double r = 0.0; int which = 0;
   if (a > 0.0 && b > 0.0) { if (a <= b) { r = a; which = 1; } else { r = b; which = 2; } }
   else if (a < 0.0 && b < 0.0) { if (a >= b) { r = a; which = 1; } else { r = b; which = 2; } }
-  if (cnt) {
-    if (fabs(a) <= DEC_TIE || fabs(b) <= DEC_TIE || fabs(a - b) <= DEC_TIE) cnt[DEC_MM_TIE]++;
-    else cnt[which == 0 ? DEC_MM_ZERO : (which == 1 ? DEC_MM_FIRST : DEC_MM_SECOND)]++;
+  if (cnt || cell) {
+    int slot = (fabs(a) <= DEC_TIE || fabs(b) <= DEC_TIE || fabs(a - b) <= DEC_TIE) ? 3 : which;
+    if (cnt) cnt[slot == 3 ? DEC_MM_TIE : (slot == 0 ? DEC_MM_ZERO : (slot == 1 ? DEC_MM_FIRST : DEC_MM_SECOND))]++;
+    if (cell) *cell += (int64_t)1 << (16 * slot);
   }
   return r;
 }
+static double mm2(double a, double b, int64_t *cnt) { return mm2c(a, b, cnt, NULL); }
 static double mm3(double a, double b, double c) {
   if (a > 0.0 && b > 0.0 && c > 0.0) return fmin(a, fmin(b, c));
   if (a < 0.0 && b < 0.0 && c < 0.0) return fmax(a, fmax(b, c));
@@ -616,8 +620,10 @@ static int fv_idx(int i, int n, int bc) {
  * unlim = 1: the same kappa-schemes without the limiter (Q10 alternative, f3):
  * MUSCL-2 kappa = 0, q_W = q_i + (dm + dp)/4; MUSCL-3 kappa = 1/3 with the raw
  * differences in place of the two minmods (van Leer's kappa-scheme). */
+/* emW / emE: optional decision-map entries of cells i and i+1 (the cell whose
+ * slope each minmod limits) */
 static void muscl_face(int order, const double *qm1, const double *q0, const double *q1, const double *q2,
-                       double *qW, double *qE, int64_t *cnt, int unlim) {
+                       double *qW, double *qE, int64_t *cnt, int unlim, int64_t *emW, int64_t *emE) {
   for (int c = 0; c < 4; ++c) {
     if (unlim) {
       const double kap = order == 1 ? 0.0 : 1.0 / 3.0;
@@ -626,31 +632,33 @@ static void muscl_face(int order, const double *qm1, const double *q0, const dou
       qW[c] = q0[c] + 0.25 * ((1.0 - kap) * dm0 + (1.0 + kap) * dp0);
       qE[c] = q1[c] - 0.25 * ((1.0 - kap) * dp1 + (1.0 + kap) * dm1);
     } else if (order == 1) {
-      double s0 = mm2(q0[c] - qm1[c], q1[c] - q0[c], cnt);
-      double s1 = mm2(q1[c] - q0[c], q2[c] - q1[c], cnt);
+      double s0 = mm2c(q0[c] - qm1[c], q1[c] - q0[c], cnt, emW);
+      double s1 = mm2c(q1[c] - q0[c], q2[c] - q1[c], cnt, emE);
       qW[c] = q0[c] + 0.5 * s0;
       qE[c] = q1[c] - 0.5 * s1;
     } else {
       const double kap = 1.0 / 3.0, beta = (3.0 - kap) / (1.0 - kap);
       double dm0 = q0[c] - qm1[c], dp0 = q1[c] - q0[c];   /* cell i   */
       double dm1 = q1[c] - q0[c], dp1 = q2[c] - q1[c];    /* cell i+1 */
-      qW[c] = q0[c] + 0.25 * ((1.0 - kap) * mm2(dm0, beta * dp0, cnt) + (1.0 + kap) * mm2(dp0, beta * dm0, cnt));
-      qE[c] = q1[c] - 0.25 * ((1.0 - kap) * mm2(dp1, beta * dm1, cnt) + (1.0 + kap) * mm2(dm1, beta * dp1, cnt));
+      qW[c] = q0[c] + 0.25 * ((1.0 - kap) * mm2c(dm0, beta * dp0, cnt, emW) + (1.0 + kap) * mm2c(dp0, beta * dm0, cnt, emW));
+      qE[c] = q1[c] - 0.25 * ((1.0 - kap) * mm2c(dp1, beta * dm1, cnt, emE) + (1.0 + kap) * mm2c(dm1, beta * dp1, cnt, emE));
     }
   }
 }
 
 void orc_muscl_face(int order, const double *qm1, const double *q0, const double *q1, const double *q2,
                     double *qW, double *qE) {
-  muscl_face(order, qm1, q0, q1, q2, qW, qE, NULL, 0);
+  muscl_face(order, qm1, q0, q1, q2, qW, qE, NULL, 0, NULL, NULL);
 }
 
 void orc_muscl_face_unlimited(int order, const double *qm1, const double *q0, const double *q1, const double *q2,
                               double *qW, double *qE) {
-  muscl_face(order, qm1, q0, q1, q2, qW, qE, NULL, 1);
+  muscl_face(order, qm1, q0, q1, q2, qW, qE, NULL, 1, NULL, NULL);
 }
 
-static void residual_fv(const orc_config *cf, const double *Q, double *R, int64_t *cnt) {
+/* emap (nullable): per-cell decision map, the cell index after the periodic wrap
+ * / transmissive clamp of fv_idx */
+static void residual_fv(const orc_config *cf, const double *Q, double *R, int64_t *cnt, int64_t *emap) {
   phys_t P = mkphys(cf);
   int nx = cf->nx, ny = cf->ny;
   int64_t N = (int64_t)nx * ny;
@@ -662,7 +670,9 @@ static void residual_fv(const orc_config *cf, const double *Q, double *R, int64_
     for (int f = 0; f <= nx; ++f) {   /* face f between cells f-1 and f */
       double s[4][4], qW[4], qE[4], F[4];
       for (int t = 0; t < 4; ++t) getq(Q, N, (int64_t)j * nx + fv_idx(f - 2 + t, nx, cf->bc), 1, 0, s[t]);
-      muscl_face(cf->k, s[0], s[1], s[2], s[3], qW, qE, cnt, cf->fv_unlimited);
+      muscl_face(cf->k, s[0], s[1], s[2], s[3], qW, qE, cnt, cf->fv_unlimited,
+                 emap ? emap + (int64_t)j * nx + fv_idx(f - 1, nx, cf->bc) : NULL,
+                 emap ? emap + (int64_t)j * nx + fv_idx(f, nx, cf->bc) : NULL);
       rusanov(&P, 0, qW, qE, F);
       for (int c = 0; c < 4; ++c) Fx[((size_t)j * (nx + 1) + f) * 4 + c] = F[c];
     }
@@ -670,7 +680,9 @@ static void residual_fv(const orc_config *cf, const double *Q, double *R, int64_
     for (int i = 0; i < nx; ++i) {
       double s[4][4], qW[4], qE[4], F[4];
       for (int t = 0; t < 4; ++t) getq(Q, N, (int64_t)fv_idx(f - 2 + t, ny, cf->bc) * nx + i, 1, 0, s[t]);
-      muscl_face(cf->k, s[0], s[1], s[2], s[3], qW, qE, cnt, cf->fv_unlimited);
+      muscl_face(cf->k, s[0], s[1], s[2], s[3], qW, qE, cnt, cf->fv_unlimited,
+                 emap ? emap + (int64_t)fv_idx(f - 1, ny, cf->bc) * nx + i : NULL,
+                 emap ? emap + (int64_t)fv_idx(f, ny, cf->bc) * nx + i : NULL);
       rusanov(&P, 1, qW, qE, F);
       for (int c = 0; c < 4; ++c) Gy[((size_t)f * nx + i) * 4 + c] = F[c];
     }
@@ -687,16 +699,21 @@ static void residual_fv(const orc_config *cf, const double *Q, double *R, int64_
 /* ------------------------------------------------------------------------- */
 /* public: residual                                                            */
 /* ------------------------------------------------------------------------- */
-int orc_residual(const orc_config *cf, const double *Q, double *R, int64_t *cnt) {
+/* emap (nullable, FV only): per-cell minmod outcomes, see mm2c */
+int orc_residual_map(const orc_config *cf, const double *Q, double *R, int64_t *cnt, int64_t *emap) {
   int st = check_cfg(cf);
   if (st) return st;
-  if (cf->method == ORC_FV) { residual_fv(cf, Q, R, cnt); return ORC_OK; }
+  if (cf->method == ORC_FV) { residual_fv(cf, Q, R, cnt, emap); return ORC_OK; }
   ops_t o;
   build_ops(cf->method, cf->k, &o);
   if (cf->method == ORC_CPR || cf->method == ORC_NDG) residual_cpr_ndg(cf, &o, Q, R);
   else if (cf->method == ORC_DG) residual_dg(cf, &o, Q, R);
   else residual_sd(cf, &o, Q, R);
   return ORC_OK;
+}
+
+int orc_residual(const orc_config *cf, const double *Q, double *R, int64_t *cnt) {
+  return orc_residual_map(cf, Q, R, cnt, NULL);
 }
 
 /* ------------------------------------------------------------------------- */
@@ -871,14 +888,18 @@ static void ssprk3_post(double *q, int64_t n, double dt, orc_rhs_fn rhs, orc_pos
   free(r);
 }
 
-typedef struct { const orc_config *cf; int64_t *cnt; } run_ctx;
+/* emap: per-element decision map (HO: stages in which the element was marked;
+ * FV: per-cell minmod outcomes, mm2c), accumulated over the run */
+typedef struct { const orc_config *cf; int64_t *cnt; int64_t *emap; int32_t *marks; } run_ctx;
 static void run_rhs(const double *q, double *r, void *ctx) {
   run_ctx *c = (run_ctx *)ctx;
-  orc_residual(c->cf, q, r, c->cnt);
+  orc_residual_map(c->cf, q, r, c->cnt, c->cf->method == ORC_FV ? c->emap : NULL);
 }
 static void run_post(double *q, void *ctx) {
   run_ctx *c = (run_ctx *)ctx;
-  orc_limit(c->cf, q, NULL, c->cnt);
+  orc_limit(c->cf, q, c->emap ? c->marks : NULL, c->cnt);
+  if (c->emap)
+    for (int64_t m = 0; m < (int64_t)c->cf->nx * c->cf->ny; ++m) c->emap[m] += c->marks[m];
 }
 
 /* first non-physical point (rho <= 0, p <= 0 or non-finite), or -1 */
@@ -896,12 +917,13 @@ static int64_t first_nonphysical(const orc_config *cf, const double *Q) {
 
 /* March until steps == max_steps or t == t_end; dt recomputed from q^n each step
  * and clipped to t_end - t.  *t is the start time on entry, the end time on exit. */
-int orc_run(const orc_config *cf, double *Q, int32_t max_steps, double t_end, double *t,
-            int64_t *steps, int64_t *cnt) {
+int orc_run_map(const orc_config *cf, double *Q, int32_t max_steps, double t_end, double *t,
+                int64_t *steps, int64_t *cnt, int64_t *emap) {
   int st = check_cfg(cf);
   if (st) return st;
   int64_t n = (int64_t)4 * cf->nx * cf->ny * points_per_elem(cf);
-  run_ctx ctx = { cf, cnt };
+  int32_t *marks = emap ? (int32_t *)calloc((size_t)cf->nx * cf->ny, sizeof(int32_t)) : NULL;
+  run_ctx ctx = { cf, cnt, emap, marks };
   int use_lim = cf->limiter && cf->method != ORC_FV;
   int64_t s = 0;
   while (s < max_steps && *t < t_end) {
@@ -911,10 +933,16 @@ int orc_run(const orc_config *cf, double *Q, int32_t max_steps, double t_end, do
                 &ctx);
     *t += dt;
     ++s;
-    if (first_nonphysical(cf, Q) >= 0) { if (steps) *steps = s; return ORC_ERR_NONPHYSICAL; }
+    if (first_nonphysical(cf, Q) >= 0) { if (steps) *steps = s; free(marks); return ORC_ERR_NONPHYSICAL; }
   }
   if (steps) *steps = s;
+  free(marks);
   return ORC_OK;
+}
+
+int orc_run(const orc_config *cf, double *Q, int32_t max_steps, double t_end, double *t,
+            int64_t *steps, int64_t *cnt) {
+  return orc_run_map(cf, Q, max_steps, t_end, t, steps, cnt, NULL);
 }
 
 /* ------------------------------------------------------------------------- */

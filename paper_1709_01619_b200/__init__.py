@@ -28,7 +28,7 @@ STATUS = {0: "OK", 1: "ERR_ARG", 2: "ERR_MESH", 3: "ERR_ORDER", 4: "ERR_NONPHYSI
 # every symbol include/hom2d.h declares
 EXPORTS = ["hom2d_strip_plan", "hom2d_workspace_bytes", "hom2d_nccl_unique_id", "hom2d_create", "hom2d_local_extent",
            "hom2d_set_state", "hom2d_get_state", "hom2d_init_case", "hom2d_residual", "hom2d_residual_strip", "hom2d_limit",
-           "hom2d_compute_dt", "hom2d_step", "hom2d_error", "hom2d_time", "hom2d_decisions",
+           "hom2d_compute_dt", "hom2d_step", "hom2d_error", "hom2d_time", "hom2d_decisions", "hom2d_decision_map",
            "hom2d_launch_count", "hom2d_stage_timing", "hom2d_stage_time", "hom2d_last_error", "hom2d_destroy"]
 
 
@@ -95,6 +95,7 @@ def load(path: str = LIB_PATH):
     L.hom2d_error.argtypes = [vp, i32, i32, P(d), P(d), P(d)]
     L.hom2d_time.argtypes = [vp, P(d)]
     L.hom2d_decisions.argtypes = [vp, vp]
+    L.hom2d_decision_map.argtypes = [vp, vp, i64]
     L.hom2d_launch_count.argtypes = [vp]
     L.hom2d_launch_count.restype = i64
     L.hom2d_stage_timing.argtypes = [vp, i32]
@@ -244,6 +245,13 @@ class Solver:
     def decisions(self):
         out = np.zeros(8, dtype=np.int64)
         self._check(self._L.hom2d_decisions(self.h, C.c_void_p(out.ctypes.data)))
+        return out
+
+    def decision_map(self):
+        """Per-element decision map (int64 [nx * nrows]); see hom2d_decision_map."""
+        n = self.cfg.nx * self.nrows
+        out = np.zeros(n, dtype=np.int64)
+        self._check(self._L.hom2d_decision_map(self.h, C.c_void_p(out.ctypes.data), n))
         return out
 
     def launch_count(self) -> int:

@@ -412,11 +412,12 @@ __device__ __forceinline__ bool detect_element(const AuxArgs& A, const Nodes& nd
 // field of the average; all four components rebuilt
 template <int N, bool CHAR>
 __device__ __forceinline__ void rebuild_element(const AuxArgs& A, const Nodes& nd, double* __restrict__ q,
-                                             const Nbr& nbr, double dx, double dy, long long* dec) {
+                                             const Nbr& nbr, double dx, double dy, long long* dec, long long* emap) {
   constexpr int NP = N * N;
   const long long ne = nbr.ne, m = nbr.m;
   const double* __restrict__ qbar = nbr.qbar;
   if (dec) atomicAdd((unsigned long long*)&dec[0], 1ull);
+  if (emap) emap[m] += 1;  // one thread per element
   double qv[4], dE[4], dW[4], dN[4], dS[4], sx[4], sy[4];
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
@@ -461,7 +462,7 @@ __global__ void __launch_bounds__(128, H2D_LIMIT_MINB) k_limit(const AuxArgs A, 
                                                                const double* __restrict__ qbar,
                                                                const double* qbar_lo, const double* qbar_hi,
                                                                long long gcs, int bcx, double eps, double dx,
-                                                               double dy, long long* dec) {
+                                                               double dy, long long* dec, long long* emap) {
   constexpr int R = H2D_LROWS(N);
   pdl_wait();
   pdl_launch();
@@ -478,7 +479,7 @@ __global__ void __launch_bounds__(128, H2D_LIMIT_MINB) k_limit(const AuxArgs A, 
 #pragma unroll
     for (int r = 0; r < R; ++r)
       if (trip[r])
-        rebuild_element<N, CHAR>(A, nd, q, Nbr(A, qbar, qbar_lo, qbar_hi, gcs, bcx, i, j0 + r), dx, dy, dec);
+        rebuild_element<N, CHAR>(A, nd, q, Nbr(A, qbar, qbar_lo, qbar_hi, gcs, bcx, i, j0 + r), dx, dy, dec, emap);
   }
 }
 }  // namespace
@@ -516,42 +517,43 @@ void launch_averages(const AuxArgs& a, const double* q, double* qbar, cudaStream
 
 template <int N, bool GLLP, bool ALL, bool CHAR>
 void launch_limit_t(const AuxArgs& a, double* q, const double* qbar, const double* qbar_lo, const double* qbar_hi,
-                    long long qbar_gcs, int bcx, double eps, long long* dec, cudaStream_t s) {
+                    long long qbar_gcs, int bcx, double eps, long long* dec, long long* emap, cudaStream_t s) {
   const int ry = (a.nrows + H2D_LROWS(N) - 1) / H2D_LROWS(N);
   dim3 grid((a.nx + 127) / 128, ry < 65535 ? ry : 65535);
   // element widths (Eq. (35)) in host IEEE double: bitwise the device's quotient
   const double dx = (a.xmax - a.xmin) / a.nx, dy = (a.ymax - a.ymin) / a.ny_global;
   launch_pdl(k_limit<N, GLLP, ALL, CHAR>, grid, dim3(128), 0, s, a, nodes_for(a.method, a.k), q, qbar, qbar_lo,
-             qbar_hi, qbar_gcs, bcx, eps, dx, dy, dec);
+             qbar_hi, qbar_gcs, bcx, eps, dx, dy, dec, emap);
 }
 
 template <int N, bool GLLP>
 void launch_limit_g(const AuxArgs& a, double* q, const double* qbar, const double* qbar_lo, const double* qbar_hi,
                     long long qbar_gcs, int bcx, double eps, int all_vars, int charact, long long* dec,
-                    cudaStream_t s) {
-  if (all_vars && charact) launch_limit_t<N, GLLP, true, true>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, dec, s);
-  else if (all_vars) launch_limit_t<N, GLLP, true, false>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, dec, s);
-  else if (charact) launch_limit_t<N, GLLP, false, true>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, dec, s);
-  else launch_limit_t<N, GLLP, false, false>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, dec, s);
+                    long long* emap, cudaStream_t s) {
+  if (all_vars && charact) launch_limit_t<N, GLLP, true, true>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, dec, emap, s);
+  else if (all_vars) launch_limit_t<N, GLLP, true, false>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, dec, emap, s);
+  else if (charact) launch_limit_t<N, GLLP, false, true>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, dec, emap, s);
+  else launch_limit_t<N, GLLP, false, false>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, dec, emap, s);
 }
 
 template <int N>
 void launch_limit_n(const AuxArgs& a, double* q, const double* qbar, const double* qbar_lo, const double* qbar_hi,
                     long long qbar_gcs, int bcx, double eps, int all_vars, int charact, long long* dec,
-                    cudaStream_t s) {
+                    long long* emap, cudaStream_t s) {
   if (a.method == 1 || a.method == 3)
-    launch_limit_g<N, true>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, all_vars, charact, dec, s);
+    launch_limit_g<N, true>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, all_vars, charact, dec, emap, s);
   else
-    launch_limit_g<N, false>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, all_vars, charact, dec, s);
+    launch_limit_g<N, false>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, all_vars, charact, dec, emap, s);
 }
 
 void launch_limit(const AuxArgs& a, double* q, const double* qbar, const double* qbar_lo, const double* qbar_hi,
-                  long long qbar_gcs, int bcx, double eps, int all_vars, int charact, long long* dec, cudaStream_t s) {
+                  long long qbar_gcs, int bcx, double eps, int all_vars, int charact, long long* dec,
+                  long long* emap, cudaStream_t s) {
   switch (a.k) {
-    case 1: return launch_limit_n<2>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, all_vars, charact, dec, s);
-    case 2: return launch_limit_n<3>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, all_vars, charact, dec, s);
-    case 3: return launch_limit_n<4>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, all_vars, charact, dec, s);
-    default: return launch_limit_n<5>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, all_vars, charact, dec, s);
+    case 1: return launch_limit_n<2>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, all_vars, charact, dec, emap, s);
+    case 2: return launch_limit_n<3>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, all_vars, charact, dec, emap, s);
+    case 3: return launch_limit_n<4>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, all_vars, charact, dec, emap, s);
+    default: return launch_limit_n<5>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, all_vars, charact, dec, emap, s);
   }
 }
 

@@ -157,9 +157,13 @@ __device__ __forceinline__ bool nonphysical(const double q[4], double gm1) {
   return !admissible(q[0], w.p);
 }
 
+// NaN-propagating max (fmax would drop a NaN): a non-finite wave speed must
+// reach the dt of Eq. (36) rather than vanish in the reduction
+__device__ __forceinline__ double nanmax(double v, double o) { return (o > v || o != o) ? o : v; }
+
 __device__ __forceinline__ double warp_max(double v) {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  for (int o = 16; o > 0; o >>= 1) v = nanmax(v, __shfl_xor_sync(0xffffffffu, v, o));
   return v;
 }
 
@@ -188,8 +192,10 @@ __device__ __forceinline__ void count_dec(long long* dec, int which, int w = 1) 
 // as a tie (slot 4), not by outcome: its branch may legitimately differ between
 // two fp64 evaluation orders.
 #define DEC_TIE 1e-12
-// (w: how many of the paper's face evaluations this one call stands for)
-__device__ __forceinline__ double minmod2(double a, double b, long long* dec, int w = 1) {
+// (w: how many of the paper's face evaluations this one call stands for; mp:
+// optional per-cell decision-map entry, the outcome added as w << 16*(slot),
+// slot 0 -> 0, 1 -> first argument, 2 -> second, 3 tie -- hom2d_decision_map)
+__device__ __forceinline__ double minmod2(double a, double b, long long* dec, int w = 1, long long* mp = nullptr) {
   // value without branches: the argument of smaller magnitude when both have the
   // same strict sign (equal magnitudes: equal values), else 0.  Equal sign BITS
   // suffice: a zero argument has the smaller magnitude, so m is then +-0 anyway.
@@ -200,6 +206,7 @@ __device__ __forceinline__ double minmod2(double a, double b, long long* dec, in
     if ((a > 0.0 && b > 0.0) || (a < 0.0 && b < 0.0)) which = (fabs(a) <= fabs(b)) ? 2 : 3;
     if (fabs(a) <= DEC_TIE || fabs(b) <= DEC_TIE || fabs(a - b) <= DEC_TIE) which = 4;
     count_dec(dec, which, w);
+    if (mp && w) atomicAdd((unsigned long long*)mp, (unsigned long long)w << (16 * (which - 1)));
   }
   return r;
 }

@@ -37,7 +37,7 @@ constexpr int FW = FTX + 4;                    // ring row width: 2 halo cells e
 // form this one reconstruction stands for (decision counting only).
 template <int ORDER>
 __device__ __forceinline__ void cell_faces(double qm, double q0, double qp, double& lo, double& hi, long long* dec,
-                                           int w) {
+                                           int w, long long* mp = nullptr) {
   // explicit rounding (no contraction freedom): a face state is bitwise the same
   // wherever it is evaluated (prologue or carried), so results do not depend on
   // how the rows are split over CTAs / launches / ranks
@@ -52,7 +52,7 @@ __device__ __forceinline__ void cell_faces(double qm, double q0, double qp, doub
     hi = __fma_rn(c1, dm, __fma_rn(c2, dp, q0));
     lo = __fma_rn(-c1, dp, __fma_rn(-c2, dm, q0));
   } else if (ORDER == 1) {
-    const double s = minmod2(q0 - qm, qp - q0, dec, w);
+    const double s = minmod2(q0 - qm, qp - q0, dec, w, mp);
     hi = __fma_rn(0.5, s, q0);
     lo = __fma_rn(-0.5, s, q0);
   } else {  // kappa = 1/3, beta = (3 - kappa)/(1 - kappa) = 4
@@ -60,8 +60,8 @@ __device__ __forceinline__ void cell_faces(double qm, double q0, double qp, doub
     const double dm = q0 - qm, dp = qp - q0;
     double A, B;
     if (dec) {
-      A = minmod2(dm, beta * dp, dec, w);
-      B = minmod2(dp, beta * dm, dec, w);
+      A = minmod2(dm, beta * dp, dec, w, mp);
+      B = minmod2(dp, beta * dm, dec, w, mp);
     } else {  // both minmods share the sign test (beta > 0): one sign-bit comparison
       const double bdp = beta * dp, bdm = beta * dm;
       const bool same = (__double2hiint(dm) ^ __double2hiint(dp)) >= 0;
@@ -140,6 +140,17 @@ __global__ void __launch_bounds__(FTX, H2D_FV_MINB) fv_stage_kernel(const StageA
     return a.q + (long long)jr * a.nx;
   };
   auto slot_of = [&](int r) { return ((r % FNS) + FNS) % FNS; };  // r = row - jb
+  // decision-map entry of cell (jr, ir) (REC runs, one rank): a ghost cell's
+  // reconstruction is attributed to the cell it copies (periodic wrap /
+  // transmissive clamp), as the oracle's fv_idx does
+  auto dmap_at = [&](int jr, int ir) -> long long* {
+    if (!REC || !a.dmap) return nullptr;
+    if (ir < 0) ir = a.bcx == 0 ? ir + a.nx : 0;
+    if (ir >= a.nx) ir = a.bcx == 0 ? ir - a.nx : a.nx - 1;
+    if (jr < 0) jr = a.ghost_lo ? jr + a.nrows : 0;
+    if (jr >= a.nrows) jr = a.ghost_hi ? jr - a.nrows : a.nrows - 1;
+    return a.dmap + (long long)jr * a.nx + ir;
+  };
 #if H2D_FV_ASYNC
   // this thread's ring column(s) of row jr (own cell: slot tid + 2; threads 0..3
   // also a halo slot) copied by cp.async straight into ring slot `slot`: no
@@ -212,8 +223,8 @@ __global__ void __launch_bounds__(FTX, H2D_FV_MINB) fv_stage_kernel(const StageA
     for (int c = 0; c < 4; ++c) {
       const double r0 = own ? ring[slot_of(-2)][c][tid + 2] : 1.0, r1 = own ? ring[slot_of(-1)][c][tid + 2] : 1.0;
       const double r2 = own ? ring[slot_of(0)][c][tid + 2] : 1.0, r3 = own ? ring[slot_of(1)][c][tid + 2] : 1.0;
-      cell_faces<ORDER>(r0, r1, r2, dm, hi[c], own ? dec : nullptr, wb);
-      cell_faces<ORDER>(r1, r2, r3, lo[c], yHi[c], own ? dec : nullptr, 2);
+      cell_faces<ORDER>(r0, r1, r2, dm, hi[c], own ? dec : nullptr, wb, own ? dmap_at(jb - 1, i0 + tid) : nullptr);
+      cell_faces<ORDER>(r1, r2, r3, lo[c], yHi[c], own ? dec : nullptr, 2, own ? dmap_at(jb, i0 + tid) : nullptr);
     }
     if (own) rusanov2<1>(hi, lo, gm1, gam, GS);
   }
@@ -222,27 +233,28 @@ __global__ void __launch_bounds__(FTX, H2D_FV_MINB) fv_stage_kernel(const StageA
   // cell i0-1+s (own cells 1..TXv; slot 0 / TXv+1 the strip's halo cells, whose
   // hi / lo state the strip's end faces need).  Decision weights as for y: own
   // cells 2, the domain's end cells' ghosts 1, a neighbouring strip's cells 0.
-  auto recon_x = [&](int rs, int buf) {
+  auto recon_x = [&](int rs, int buf, int jr) {
     double dm;
     if (own) {
 #pragma unroll
       for (int c = 0; c < 4; ++c)
         cell_faces<ORDER>(ring[rs][c][tid + 1], ring[rs][c][tid + 2], ring[rs][c][tid + 3], sXL[buf][c][tid + 1],
-                          sXH[buf][c][tid + 1], dec, 2);
+                          sXH[buf][c][tid + 1], dec, 2, dmap_at(jr, i0 + tid));
     }
     if (tid == 0) {
 #pragma unroll
       for (int c = 0; c < 4; ++c)
-        cell_faces<ORDER>(ring[rs][c][0], ring[rs][c][1], ring[rs][c][2], dm, sXH[buf][c][0], dec, i0 == 0 ? 1 : 0);
+        cell_faces<ORDER>(ring[rs][c][0], ring[rs][c][1], ring[rs][c][2], dm, sXH[buf][c][0], dec, i0 == 0 ? 1 : 0,
+                          dmap_at(jr, i0 - 1));
     }
     if (tid == TXv - 1) {
 #pragma unroll
       for (int c = 0; c < 4; ++c)
         cell_faces<ORDER>(ring[rs][c][TXv + 1], ring[rs][c][TXv + 2], ring[rs][c][TXv + 3], sXL[buf][c][TXv + 1], dm,
-                          dec, (i0 + TXv == a.nx) ? 1 : 0);
+                          dec, (i0 + TXv == a.nx) ? 1 : 0, dmap_at(jr, i0 + TXv));
     }
   };
-  recon_x(slot_of(0), 0);  // read after the first loop barrier
+  recon_x(slot_of(0), 0, jb);  // read after the first loop barrier
 
   double lam = 0.0;
   const double bdt = a.bcoef * dtv;
@@ -291,7 +303,7 @@ __global__ void __launch_bounds__(FTX, H2D_FV_MINB) fv_stage_kernel(const StageA
         qL[c] = sXH[b][c][tid];
         qR[c] = sXL[b][c][tid + 1];
         cell_faces<ORDER>(ring[sc][c][tid + 2], ring[slot_of(r + 1)][c][tid + 2], ring[slot_of(r + 2)][c][tid + 2],
-                          lo[c], hi[c], dec, wn);
+                          lo[c], hi[c], dec, wn, dmap_at(jb + r + 1, i0 + tid));
       }
       rusanov2<0>(qL, qR, gm1, gam, F);
       rusanov2<1>(yHi, lo, gm1, gam, GN);
@@ -313,7 +325,7 @@ __global__ void __launch_bounds__(FTX, H2D_FV_MINB) fv_stage_kernel(const StageA
 #pragma unroll
       for (int c = 0; c < 4; ++c) sF[tid + 1][c] = F[c];
     }
-    if (r + 1 < RBv) recon_x(slot_of(r + 1), (r + 1) & 1);
+    if (r + 1 < RBv) recon_x(slot_of(r + 1), (r + 1) & 1, jb + r + 1);
     __syncthreads();
     if (own) {
       double o[4];

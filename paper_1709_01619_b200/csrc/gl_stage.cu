@@ -670,14 +670,12 @@ __global__ void __launch_bounds__(L<M, K>::NT, LTile<M, K>::MINB) gl_stage_kerne
 }
 
 template <int M, int K, int V>
-static void launch_lv(dim3 grid, const StageArgs& b, const LTab& tab, const LMaps& maps, cudaStream_t s) {
+static cudaError_t launch_lv(dim3 grid, const StageArgs& b, const LTab& tab, const LMaps& maps, cudaStream_t s) {
   using H = L<M, K>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(gl_stage_kernel<M, K, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)H::SMEM);
-    attr = true;
-  }
-  launch_pdl_if(!b.no_pdl, gl_stage_kernel<M, K, V>, grid, dim3(H::NT), H::SMEM, s, b, tab, maps);
+  static std::atomic<unsigned long long> attr{0};
+  const cudaError_t e = smem_optin(gl_stage_kernel<M, K, V>, (int)H::SMEM, attr);
+  if (e != cudaSuccess) return e;
+  return launch_pdl_if(!b.no_pdl, gl_stage_kernel<M, K, V>, grid, dim3(H::NT), H::SMEM, s, b, tab, maps);
 }
 
 template <int M, int K>
@@ -699,15 +697,16 @@ static int launch_l(const StageArgs& a, cudaStream_t s) {
   b.rows = march_rows(nr, strips, H::RB);
   dim3 grid(strips, (nr + b.rows - 1) / b.rows);
   const int v = (a.q0 ? 1 : 0) | ((a.lam || a.bad) ? 2 : 0) | (a.qbar ? 4 : 0);
+  cudaError_t e = cudaSuccess;
   switch (v) {
-    case 0: launch_lv<M, K, 0>(grid, b, tab, maps, s); break;
-    case 1: launch_lv<M, K, 1>(grid, b, tab, maps, s); break;
-    case 3: launch_lv<M, K, 3>(grid, b, tab, maps, s); break;
-    case 4: launch_lv<M, K, 4>(grid, b, tab, maps, s); break;
-    case 5: launch_lv<M, K, 5>(grid, b, tab, maps, s); break;
-    default: launch_lv<M, K, 8>(grid, b, tab, maps, s); break;
+    case 0: e = launch_lv<M, K, 0>(grid, b, tab, maps, s); break;
+    case 1: e = launch_lv<M, K, 1>(grid, b, tab, maps, s); break;
+    case 3: e = launch_lv<M, K, 3>(grid, b, tab, maps, s); break;
+    case 4: e = launch_lv<M, K, 4>(grid, b, tab, maps, s); break;
+    case 5: e = launch_lv<M, K, 5>(grid, b, tab, maps, s); break;
+    default: e = launch_lv<M, K, 8>(grid, b, tab, maps, s); break;
   }
-  return (int)cudaPeekAtLastError();
+  return e != cudaSuccess ? (int)e : (int)cudaPeekAtLastError();
 }
 
 int launch_gl_stage(int method, int k, const StageArgs& a, cudaStream_t s) {

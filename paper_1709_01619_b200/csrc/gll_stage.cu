@@ -702,14 +702,12 @@ bool make_map(CUtensorMap* m, const double* base, long long nelem, long long cs,
 }
 
 template <int M, int K, int V>
-static void launch_v(dim3 grid, const StageArgs& b, const GTab& tab, const GMaps& maps, cudaStream_t s) {
+static cudaError_t launch_v(dim3 grid, const StageArgs& b, const GTab& tab, const GMaps& maps, cudaStream_t s) {
   using H = G<M, K>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(gll_stage_kernel<M, K, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)H::SMEM);
-    attr = true;
-  }
-  launch_pdl_if(!b.no_pdl, gll_stage_kernel<M, K, V>, grid, dim3(H::NT), H::SMEM, s, b, tab, maps);
+  static std::atomic<unsigned long long> attr{0};
+  const cudaError_t e = smem_optin(gll_stage_kernel<M, K, V>, (int)H::SMEM, attr);
+  if (e != cudaSuccess) return e;
+  return launch_pdl_if(!b.no_pdl, gll_stage_kernel<M, K, V>, grid, dim3(H::NT), H::SMEM, s, b, tab, maps);
 }
 
 template <int M, int K>
@@ -731,15 +729,16 @@ static int launch_g(const StageArgs& a, cudaStream_t s) {
   b.rows = march_rows(nr, strips, H::RB);
   dim3 grid(strips, (nr + b.rows - 1) / b.rows);
   const int v = (a.q0 ? 1 : 0) | ((a.lam || a.bad) ? 2 : 0) | (a.qbar ? 4 : 0);
+  cudaError_t e = cudaSuccess;
   switch (v) {
-    case 0: launch_v<M, K, 0>(grid, b, tab, maps, s); break;
-    case 1: launch_v<M, K, 1>(grid, b, tab, maps, s); break;
-    case 3: launch_v<M, K, 3>(grid, b, tab, maps, s); break;
-    case 4: launch_v<M, K, 4>(grid, b, tab, maps, s); break;
-    case 5: launch_v<M, K, 5>(grid, b, tab, maps, s); break;
-    default: launch_v<M, K, 8>(grid, b, tab, maps, s); break;
+    case 0: e = launch_v<M, K, 0>(grid, b, tab, maps, s); break;
+    case 1: e = launch_v<M, K, 1>(grid, b, tab, maps, s); break;
+    case 3: e = launch_v<M, K, 3>(grid, b, tab, maps, s); break;
+    case 4: e = launch_v<M, K, 4>(grid, b, tab, maps, s); break;
+    case 5: e = launch_v<M, K, 5>(grid, b, tab, maps, s); break;
+    default: e = launch_v<M, K, 8>(grid, b, tab, maps, s); break;
   }
-  return (int)cudaPeekAtLastError();
+  return e != cudaSuccess ? (int)e : (int)cudaPeekAtLastError();
 }
 
 int launch_gll_stage(int method, int k, const StageArgs& a, cudaStream_t s) {

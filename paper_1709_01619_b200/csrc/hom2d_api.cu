@@ -38,13 +38,14 @@ struct hom2d {
   unsigned long long* lam = nullptr;       // [acc, cur]
   unsigned long long* bad = nullptr;
   long long* dec = nullptr;
+  long long* dmap = nullptr;               // record_decisions, one rank: per-element decision map [nx*nrows]
   double* part = nullptr;                  // error partials
   int max_part = 0;
   double* err3 = nullptr;
   double* qbar = nullptr;                  // HO limiter averages [4][nx*nrows]
   double *glo = nullptr, *ghi = nullptr;   // received ghost rows [4][G*nx*np]
   double *qblo = nullptr, *qbhi = nullptr; // received ghost average rows [4][nx]
-  double* t_host = nullptr;
+  double* t_host = nullptr;               // pinned: [0..3] clock, [5] t_end, [6..7] bad flags
   bool ovr_active = false;                 // hom2d_residual_strip ghost override
   const double *ovr_lo = nullptr, *ovr_hi = nullptr;
   bool poisoned = false;
@@ -77,10 +78,13 @@ hom2d_status fail(hom2d* h, hom2d_status st, const char* fmt, ...) {
     ncclResult_t r_ = (x);                                                              \
     if (r_ != ncclSuccess) return fail(h, HOM2D_ERR_NCCL, "%s: %s", #x, ncclGetErrorString(r_)); \
   } while (0)
+// every entry point: valid, unpoisoned handle, its device current (handles of
+// several devices may live in one process)
 #define GUARD(h)                                                     \
   do {                                                               \
     if (!(h)) return HOM2D_ERR_ARG;                                  \
     if ((h)->poisoned) return HOM2D_ERR_STATE;                       \
+    CU(h, cudaSetDevice((h)->device));                               \
   } while (0)
 
 int points_per_elem(const hom2d_config& c) { return c.method == HOM2D_FV ? 1 : (c.k + 1) * (c.k + 1); }
@@ -139,6 +143,7 @@ size_t carve(hom2d* h, const hom2d_config& c, int nranks, char* base) {
   double* part = cv.take<double>(3 * max_part);
   double* err3 = cv.take<double>(4);
   double* qbar = (c.method != HOM2D_FV) ? cv.take<double>(4 * (size_t)c.nx * nrows) : nullptr;
+  long long* dmap = (c.record_decisions && nranks == 1) ? cv.take<long long>((size_t)c.nx * nrows) : nullptr;
   double *glo = nullptr, *ghi = nullptr, *qblo = nullptr, *qbhi = nullptr;
   if (nranks > 1 || self_exchange_env(c, nranks)) {
     glo = cv.take<double>(4 * (size_t)G * c.nx * np);
@@ -150,7 +155,7 @@ size_t carve(hom2d* h, const hom2d_config& c, int nranks, char* base) {
   }
   if (h && base) {
     h->Qn = Qn; h->Q1 = Q1; h->Q2 = Q2; h->clock = clk; h->lam = lam; h->bad = bad; h->dec = dec;
-    h->part = part; h->max_part = max_part; h->err3 = err3; h->qbar = qbar;
+    h->part = part; h->max_part = max_part; h->err3 = err3; h->qbar = qbar; h->dmap = dmap;
     h->glo = glo; h->ghi = ghi; h->qblo = qblo; h->qbhi = qbhi;
   }
   return cv.off + 512;  // trailing guard
@@ -268,6 +273,7 @@ hom2d_status run_stage(hom2d* h, const double* q, const double* q0, double* out,
   s.a0 = a0; s.a1 = a1; s.bcoef = b; s.dt = dt; s.gamma = h->cfg.gamma;
   s.lam = lam; s.bad = bad;
   s.dec = h->cfg.record_decisions ? h->dec : nullptr;
+  s.dmap = h->cfg.record_decisions ? h->dmap : nullptr;
   s.count_bot = (h->rank == 0);
   s.qbar = qbar;
   s.fv_unlimited = h->cfg.fv_unlimited;
@@ -310,7 +316,8 @@ hom2d_status run_limiter(hom2d* h, double* X, const double* dt = nullptr, bool a
   hom2d_status st = exchange(h, h->qbar, ne, h->cfg.nx, &lo, &hi, &gcs, h->qblo, h->qbhi, 1, h->stream);
   if (st) return st;
   launch_limit(A, X, h->qbar, lo, hi, gcs, h->cfg.bc, h->cfg.limiter_eps, h->cfg.limiter_all_vars,
-               h->cfg.limiter_characteristic, h->cfg.record_decisions ? h->dec : nullptr, h->stream);
+               h->cfg.limiter_characteristic, h->cfg.record_decisions ? h->dec : nullptr,
+               h->cfg.record_decisions ? h->dmap : nullptr, h->stream);
   h->launches++;
   CU(h, cudaPeekAtLastError());
   return HOM2D_OK;
@@ -338,6 +345,7 @@ hom2d_status reset_clock(hom2d* h, double t0) {
   double c[4] = {t0, 0.0, 0.0, 0.0};
   CU(h, cudaMemcpyAsync(h->clock, c, sizeof(c), cudaMemcpyHostToDevice, h->stream));
   CU(h, cudaMemsetAsync(h->dec, 0, 8 * sizeof(long long), h->stream));
+  if (h->dmap) CU(h, cudaMemsetAsync(h->dmap, 0, (size_t)h->cfg.nx * h->nrows * sizeof(long long), h->stream));
   CU(h, cudaMemsetAsync(h->bad, 0xff, sizeof(unsigned long long), h->stream));
   CU(h, cudaStreamSynchronize(h->stream));
   return HOM2D_OK;
@@ -534,6 +542,8 @@ hom2d_status hom2d_compute_dt(hom2d* h, double* dt) {
   CU(h, cudaStreamSynchronize(h->stream));
   double l;
   memcpy(&l, &bits, 8);
+  if (!(l > 0.0 && l < HUGE_VAL))  // NaN / inf wave speed: a non-physical state (the reduction keeps NaN)
+    return fail(h, HOM2D_ERR_NONPHYSICAL, "compute_dt: max wave speed %g", l);
   const double dx = (h->cfg.xmax - h->cfg.xmin) / h->cfg.nx, dy = (h->cfg.ymax - h->cfg.ymin) / h->cfg.ny;
   *dt = h->cfg.cfl * fmin(dx, dy) / l;
   return HOM2D_OK;
@@ -641,17 +651,28 @@ extern "C" hom2d_status hom2d_step(hom2d* h, int32_t max_steps, double t_end, do
     }
     done += batch;
     CU(h, cudaPeekAtLastError());
+    // every rank leaves the loop in the same batch: the flag is min-reduced over
+    // the ranks (bad[1]) before the host looks at it; the local point (bad[0])
+    // names the element when this rank found it
+    if (h->nranks > 1 && h->comm)
+      NC(h, ncclAllReduce(h->bad, h->bad + 1, 1, ncclUint64, ncclMin, h->comm, h->stream));
+    else
+      CU(h, cudaMemcpyAsync(h->bad + 1, h->bad, sizeof(unsigned long long), cudaMemcpyDeviceToDevice, h->stream));
     CU(h, cudaMemcpyAsync(h->t_host, h->clock, 4 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-    CU(h, cudaMemcpyAsync(h->t_host + 4, h->bad, sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->stream));
+    CU(h, cudaMemcpyAsync(h->t_host + 6, h->bad, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, h->stream));
     CU(h, cudaStreamSynchronize(h->stream));
-    unsigned long long badv;
-    memcpy(&badv, h->t_host + 4, 8);
-    if (badv != ~0ull) {
+    unsigned long long badv, bad_any;
+    memcpy(&badv, h->t_host + 6, 8);
+    memcpy(&bad_any, h->t_host + 7, 8);
+    if (bad_any != ~0ull) {
       if (t_out) *t_out = h->t_host[0];
       if (steps_out) *steps_out = (int64_t)(h->t_host[2] - steps0);
+      if (badv == ~0ull)
+        return fail(h, HOM2D_ERR_NONPHYSICAL, "non-physical state on another rank, t=%.17g", h->t_host[0]);
       const long long m = (long long)(badv / h->np);
-      return fail(h, HOM2D_ERR_NONPHYSICAL, "non-physical state at element (i=%lld, j=%lld), point %lld, t=%.17g",
-                  m % h->cfg.nx, m / h->cfg.nx + h->row0, (long long)(badv % h->np), h->t_host[0]);
+      return fail(h, HOM2D_ERR_NONPHYSICAL,
+                  "non-physical state at element (i=%lld, j=%lld), point %lld, rank %d, t=%.17g", m % h->cfg.nx,
+                  m / h->cfg.nx + h->row0, (long long)(badv % h->np), h->rank, h->t_host[0]);
     }
     if (!(h->t_host[0] < t_end)) break;
   }
@@ -704,6 +725,17 @@ hom2d_status hom2d_decisions(hom2d* h, int64_t* counts8) {
     CU(h, cudaMemcpyAsync(counts8, h->part, 8 * sizeof(long long), cudaMemcpyDeviceToHost, h->stream));
     CU(h, cudaStreamSynchronize(h->stream));
   }
+  return HOM2D_OK;
+}
+
+hom2d_status hom2d_decision_map(hom2d* h, int64_t* out, int64_t n) {
+  GUARD(h);
+  if (!out) return HOM2D_ERR_ARG;
+  if (!h->dmap) return fail(h, HOM2D_ERR_STATE, "decision_map needs record_decisions = 1 and one rank");
+  if (n != (int64_t)h->cfg.nx * h->nrows) return fail(h, HOM2D_ERR_ARG, "decision_map: expected %lld entries",
+                                                     (long long)h->cfg.nx * h->nrows);
+  CU(h, cudaMemcpyAsync(out, h->dmap, n * sizeof(long long), cudaMemcpyDeviceToHost, h->stream));
+  CU(h, cudaStreamSynchronize(h->stream));
   return HOM2D_OK;
 }
 

@@ -1,5 +1,6 @@
 // internal.h -- host-side declarations shared by the API and the kernel files.
 #pragma once
+#include <atomic>
 #include <cstdint>
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -32,6 +33,21 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
   return launch_pdl_if(true, kernel, grid, block, smem, s, args...);
 }
 
+// Opt a kernel into more than 48 KB of dynamic shared memory once per device
+// (the attribute is per device; `done` holds one bit per device ordinal).
+// Thread-safe: a race only repeats the idempotent call.  Returns its error.
+template <typename... KArgs>
+cudaError_t smem_optin(void (*kernel)(KArgs...), int bytes, std::atomic<unsigned long long>& done) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_release);
+  return e;
+}
+
 // One RK stage (or a bare residual):  out = a0*q0 + a1*q + bcoef*dt*R(q)
 // (SSP-RK3 of P:868 in Shu-Osher form; residual mode: a0 = a1 = 0, bcoef = 1,
 // dt == nullptr).  Arrays are the local strip in the canonical SoA layout.
@@ -54,6 +70,7 @@ struct StageArgs {
   unsigned long long* lam; // optional: atomicMax of max(|u|,|v|)+c of `out` (bits of a double >= 0)
   unsigned long long* bad; // optional: atomicMin of the first non-physical point index
   long long* dec;          // optional: decision counters [8]
+  long long* dmap;         // optional (FV, with dec, one rank): per-cell minmod outcomes [nx*nrows]
   int count_bot;           // this strip owns the domain's bottom face row (decision counting)
   double* qbar;            // optional (HO limiter runs): element averages of `out`, [4][nx*nrows]
                            // (Alg. 9: 1/4 sum_ab w_a w_b q_ab), fused into the stage epilogue
@@ -108,6 +125,6 @@ void launch_error_final(const double* part, int nblocks, double* out3, cudaStrea
 void launch_averages(const AuxArgs& a, const double* q, double* qbar, cudaStream_t s);
 void launch_limit(const AuxArgs& a, double* q, const double* qbar, const double* qbar_lo, const double* qbar_hi,
                   long long qbar_gcs, int bcx, double eps, int all_vars, int charact, long long* dec,
-                  cudaStream_t s);
+                  long long* emap, cudaStream_t s);
 
 }  // namespace h2d

@@ -306,3 +306,115 @@ def test_multi_row_march_parity(orc, P, method, k):
     assert n_g == n_o == 10
     assert rel_linf(s.get_state(), q_o) <= 1e-10
     s.close()
+
+
+# --------------------------------------------------------------------------- #
+# Round 2: the north_star gate as written -- 100 steps with the limiter on /   #
+# 100 FV shock steps, decisions identical element by element      #
+# --------------------------------------------------------------------------- #
+LIMITED_GATE = [("cpr", 1, 0.2), ("cpr", 2, 0.1), ("ndg", 1, 0.2), ("ndg", 2, 0.1), ("dg", 1, 0.2),
+                ("dg", 2, 0.08), ("sd", 1, 0.27), ("sd", 2, 0.18), ("cpr", 3, 0.06)]
+
+
+@pytest.mark.parametrize("method,k,cfl", LIMITED_GATE)
+def test_limiter_gate_100_steps(orc, P, method, k, cfl):
+    """Radial shock tube on 32^2, transmissive, minmod detection +
+    limiting after every stage: 100 SSP-RK3 steps (no t_end), the
+    state within 1e-10 (north_star) and, after EVERY step, the per-element count
+    of limiter passes that marked the element identical to the oracle's."""
+    box = (-1.0, 1.0, -1.0, 1.0)
+    n = 32
+    oc, s = pair(orc, P, n, n, method, k, bc=1, box=box, cfl=cfl, limiter=1, record=1)
+    q = orc.init_case(oc, orc.SHOCK)
+    s.set_state(q)
+    em = np.zeros(n * n, dtype=np.int64)
+    t = 0.0
+    for step in range(100):
+        q, t, n_o = orc.run(oc, q, 1, t0=t, emap=em)
+        t_g, n_g = s.step(1)
+        assert n_o == n_g == 1
+        assert abs(t_g - t) <= 1e-12 * t
+        g = s.decision_map()
+        bad = np.flatnonzero(g != em)
+        assert bad.size == 0, (step, bad[:10], g[bad[:10]], em[bad[:10]])
+    assert em.sum() > 0 and s.decisions()[0] == em.sum()
+    assert rel_linf(s.get_state(), q) <= 1e-10
+    s.close()
+
+
+def _unpack(m):
+    return np.stack([(m >> (16 * sl)) & 0xFFFF for sl in range(4)])
+
+
+@pytest.mark.parametrize("k,cfl", [(1, 0.58), (2, 0.54)])
+@pytest.mark.parametrize("bc", [0, 1])
+def test_fv_decisions_100_steps(orc, P, k, cfl, bc):
+    """FV MUSCL-2/3 + minmod on the shock tube, 100 steps: state within
+    1e-10 and, per cell, the minmod outcomes of its own slopes (-> 0 / first /
+    second argument) identical to the oracle's; ties (an argument or their
+    difference within 1e-12 of the switch point) counted separately and equal."""
+    box = (-1.0, 1.0, -1.0, 1.0)
+    n = 48
+    oc, s = pair(orc, P, n, n, "fv", k, bc=bc, box=box, cfl=cfl, record=1)
+    q0 = orc.init_case(oc, orc.SHOCK)
+    s.set_state(q0)
+    em = np.zeros(n * n, dtype=np.int64)
+    cnt = np.zeros(8, dtype=np.int64)
+    q_o, t_o, n_o = orc.run(oc, q0, 100, counts=cnt, emap=em)
+    t_g, n_g = s.step(100)
+    assert n_g == n_o == 100
+    assert rel_linf(s.get_state(), q_o) <= 1e-10
+    g = s.decision_map()
+    ug, uo = _unpack(g), _unpack(em)
+    bad = np.flatnonzero((ug != uo).any(axis=0))
+    assert bad.size == 0, (bad[:10], ug[:, bad[:10]], uo[:, bad[:10]])
+    np.testing.assert_array_equal(s.decisions()[1:5], cnt[1:5])
+    assert uo[1:3].sum() > 0 and uo[0].sum() > 0  # every outcome occurs
+
+
+@pytest.mark.parametrize("k", [1, 2])
+@pytest.mark.parametrize("bc", [0, 1])
+def test_fv_rough_data_residual(orc, P, k, bc):
+    """FV residual on strongly perturbed data (20 % cell-to-cell noise), where every
+    minmod branch occurs, including MUSCL-3's beta-bounded arguments (|D+| > 4|D-|)."""
+    import torch
+    nx, ny = 45, 21
+    oc, s = pair(orc, P, nx, ny, "fv", k, bc=bc, record=1)
+    from paper_1709_01619_b200.inputs import perturb
+    q = perturb(orc.init_case(oc), seed=31 + k, amp=0.2)
+    em = np.zeros(nx * ny, dtype=np.int64)
+    cnt = np.zeros(8, dtype=np.int64)
+    r_orc = orc.residual(oc, q, counts=cnt, emap=em)
+    s.set_state(q)  # resets the map
+    r_gpu = s.residual(torch.from_numpy(q).cuda()).cpu().numpy()
+    assert rel_linf_res(r_gpu, r_orc) < 1e-12
+    np.testing.assert_array_equal(_unpack(s.decision_map()), _unpack(em))
+    np.testing.assert_array_equal(s.decisions()[1:5], cnt[1:5])
+
+
+@pytest.mark.parametrize("k", [1, 2])
+@pytest.mark.parametrize("case", [0, 1])
+@pytest.mark.parametrize("bc", [0, 1])
+def test_fv_init_case_parity(orc, P, k, case, bc):
+    """FV initial data: 8x8 Gauss-Legendre cell averages of the closed-form case
+    (vortex P:897-913 / shock tube P:1043-1047), GPU k_init vs the oracle."""
+    box = (-5.0, 5.0, -5.0, 5.0) if case == 0 else (-1.0, 1.0, -1.0, 1.0)
+    oc, s = pair(orc, P, 37, 23, "fv", k, bc=bc, box=box)
+    s.init_case(case)
+    np.testing.assert_allclose(s.get_state(), orc.init_case(oc, case), rtol=1e-13, atol=1e-15)
+
+
+@pytest.mark.parametrize("method,k", [("cpr", 1), ("ndg", 2), ("dg", 3), ("sd", 4), ("cpr", 4), ("sd", 1),
+                                      ("fv", 1), ("fv", 2)])
+@pytest.mark.parametrize("var", [0, 1, 2, 3])
+def test_error_parity_all_norms(orc, P, method, k, var):
+    """hom2d_error: L1, L2 and Linf of every conserved component against the exact
+    vortex at t != 0 (reading R8), GPU vs oracle on a seeded
+    perturbed state."""
+    nx, ny = (13, 11) if method != "fv" else (40, 30)
+    oc, s = pair(orc, P, nx, ny, method, k)
+    from paper_1709_01619_b200.inputs import perturb
+    q = perturb(orc.init_case(oc), seed=7 + var, amp=1e-3)
+    t0 = 0.37
+    s.set_state(q, t0)
+    np.testing.assert_allclose(s.error(P.VORTEX, var), orc.error(oc, q, t0, var=var), rtol=1e-12)

@@ -557,3 +557,103 @@ def test_shock_tube_invariants(orc, method, k, cfl):
     # chain-rule CPR conserves mass only (Q5)
     idx = [0] if method == "cpr" else [0, 3]
     np.testing.assert_allclose(tot[idx], tot0[idx], rtol=1e-13)
+
+
+# --------------------------------------------------------------------------- #
+# Round 2 pins: the L1 / Linf outputs of orc_error and MUSCL-3's beta          #
+# --------------------------------------------------------------------------- #
+@pytest.mark.parametrize("method,k", [("cpr", 1), ("cpr", 3), ("ndg", 2), ("dg", 2), ("dg", 4), ("sd", 3)])
+@pytest.mark.parametrize("var", [0, 2, 3])
+def test_error_norms_closed_form_ho(orc, method, k, var):
+    """Reading R8: the exact vortex at the solution points has
+    zero error; offsets d1, d2 at two points (a1,b1) of element m1 and (a2,b2) of
+    m2 give L1 = (w_a1 w_b1 |d1| + w_a2 w_b2 |d2|) / (4 N_e),
+    L2 = sqrt((w_a1 w_b1 d1^2 + w_a2 w_b2 d2^2) / (4 N_e)), Linf = max(|d1|, |d2|):
+    a wrong weight, normaliser or Linf support fails here."""
+    nx, ny = 7, 5
+    cfg = orc.config(nx=nx, ny=ny, method=method, k=k)
+    q = orc.init_case(cfg)  # nodal values of the exact solution at t = 0 (Q21)
+    assert orc.error(cfg, q, 0.0, var=var) == (0.0, 0.0, 0.0)
+    n = k + 1
+    _, w = orc.nodes(1 if method in ("cpr", "ndg") else 0, n)
+    N = nx * ny * n * n
+    pts = [(3, 0, n - 1, 0.25), (nx * ny - 2, n // 2, 1, -0.625)]  # (element, a, b, offset)
+    for m, a, b, d in pts:
+        q[var * N + m * n * n + b * n + a] += d
+    l1, l2, li = orc.error(cfg, q, 0.0, var=var)
+    ne = nx * ny
+    W = [w[a] * w[b] / 4.0 for _, a, b, _ in pts]
+    D = [d for *_, d in pts]
+    assert l1 == pytest.approx(sum(Wi * abs(di) for Wi, di in zip(W, D)) / ne, rel=1e-13)
+    assert l2 == pytest.approx(math.sqrt(sum(Wi * di * di for Wi, di in zip(W, D)) / ne), rel=1e-13)
+    assert li == pytest.approx(max(abs(di) for di in D), rel=1e-13)
+
+
+@pytest.mark.parametrize("k", [1, 2])
+@pytest.mark.parametrize("var", [0, 1, 3])
+def test_error_norms_closed_form_fv(orc, k, var):
+    """FV: the cell value against the exact 8x8-GL cell average (Q22): the oracle's
+    own initial data has zero error; offsets give L1 = sum|d|/N_e,
+    L2 = sqrt(sum d^2 / N_e), Linf = max|d| (equal cell weights)."""
+    nx, ny = 9, 6
+    cfg = orc.config(nx=nx, ny=ny, method="fv", k=k)
+    q = orc.init_case(cfg)
+    assert orc.error(cfg, q, 0.0, var=var) == (0.0, 0.0, 0.0)
+    N = nx * ny
+    D = {4: 0.5, 17: -0.125, 53: 0.0625}
+    for m, d in D.items():
+        q[var * N + m] += d
+    l1, l2, li = orc.error(cfg, q, 0.0, var=var)
+    assert l1 == pytest.approx(sum(abs(d) for d in D.values()) / N, rel=1e-13)
+    assert l2 == pytest.approx(math.sqrt(sum(d * d for d in D.values()) / N), rel=1e-13)
+    assert li == pytest.approx(0.5, rel=1e-13)
+
+
+def test_error_after_one_period_is_round_off(orc):
+    """exact(x, y, t = 10) is exact(x, y, 0) (one period of the (1, 0) advection on
+    the 10-wide box): the t = 0 initial data has round-off error at t = 10."""
+    cfg = orc.config(nx=6, ny=6, method="dg", k=2)
+    l1, l2, li = orc.error(cfg, orc.init_case(cfg), 10.0, var=0)
+    assert li < 1e-12 and l2 < 1e-12
+
+
+def test_muscl3_beta_binds(orc):
+    """MUSCL-3, kappa = 1/3, beta = (3 - kappa)/(1 - kappa) = 4 (SURVEY C8,
+    P:346-351): with D- = 1, D+ = 5 (|D+| > beta |D-|) the face value is
+    q + [(1-k) mm(D-, 4 D+) + (1+k) mm(D+, 4 D-)]/4 = q + [(2/3) 1 + (4/3) 4]/4
+    = q + 3/2 (beta = 5 would give q + 11/6, beta = 3 q + 7/6); the mirror cell
+    (D- = 5, D+ = 1) gives q - 3/2 at its west face, and D- = 5 D+ gives q + 1
+    at the east face."""
+    ones = np.ones(4)
+    # cells: 0, 1, 6, 7 -> cell 1: D- = 1, D+ = 5; cell 2: D- = 5, D+ = 1
+    qW, qE = orc.muscl_face(2, 0 * ones, 1 * ones, 6 * ones, 7 * ones)
+    np.testing.assert_allclose(qW, 2.5 * ones, rtol=1e-15)
+    np.testing.assert_allclose(qE, 4.5 * ones, rtol=1e-15)
+    # D- = 5 D+ on the west cell: q + [(2/3) mm(5, 4) + (4/3) mm(1, 20)]/4 = q + 1
+    qW, _ = orc.muscl_face(2, -5 * ones, 0 * ones, 1 * ones, 2 * ones)
+    np.testing.assert_allclose(qW, 1.0 * ones, rtol=1e-15)
+    # negative mirror: the minmods keep the common sign
+    qW, _ = orc.muscl_face(2, 0 * ones, -1 * ones, -6 * ones, -7 * ones)
+    np.testing.assert_allclose(qW, -2.5 * ones, rtol=1e-15)
+
+
+def test_fv_decision_map_totals(orc):
+    """The per-cell decision map (SURVEY C12 dumps) partitions the global minmod
+    counters: summed over cells, each outcome slot equals counts[1..4]; a cell's
+    slope is limited once per face it is used at (2 per direction; 3 for the
+    first / last cell of a line, whose ghost neighbour's slope is its own by the
+    wrap / clamp) per component and stage (MUSCL-2: one minmod per slope,
+    MUSCL-3: two)."""
+    for k in (1, 2):
+        for bc in (0, 1):
+            cfg = orc.config(nx=12, ny=9, method="fv", k=k, bc=bc, box=(-1.0, 1.0, -1.0, 1.0), cfl=0.5)
+            q = orc.init_case(cfg, orc.SHOCK)
+            em = np.zeros(cfg.nx * cfg.ny, dtype=np.int64)
+            cnt = np.zeros(8, dtype=np.int64)
+            orc.run(cfg, q, 3, counts=cnt, emap=em)
+            slots = np.stack([(em >> (16 * s)) & 0xFFFF for s in range(4)])
+            np.testing.assert_array_equal(slots.sum(axis=1), cnt[1:5])
+            per_cell = slots.sum(axis=0).reshape(cfg.ny, cfg.nx)
+            fx = np.where((np.arange(cfg.nx) == 0) | (np.arange(cfg.nx) == cfg.nx - 1), 3, 2)
+            fy = np.where((np.arange(cfg.ny) == 0) | (np.arange(cfg.ny) == cfg.ny - 1), 3, 2)
+            np.testing.assert_array_equal(per_cell, 3 * 3 * 4 * k * (fx[None, :] + fy[:, None]))
