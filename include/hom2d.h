@@ -84,6 +84,12 @@ typedef struct {
   int32_t limiter_characteristic; /* HO: 1 = the Eq. (35) slopes limited per characteristic
                                  field of the element average (Cockburn-Shu) instead of per
                                  conserved component (Q12) */
+  int32_t fv_error_recon;     /* FV: 1 = hom2d_error measures the reconstructed solution ("For P^2 FV,
+                                 the error was computed by reconstructing the solution along element
+                                 faces, and then using a quadrature rule"; DESIGN R22): per
+                                 cell the quadratic through the scheme's MUSCL face states with the cell
+                                 mean, per direction, summed, against the exact solution at the 3x3
+                                 Gauss-Legendre points; 0 = cell value vs exact cell average */
 } hom2d_config;
 
 typedef struct {

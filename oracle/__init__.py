@@ -37,7 +37,8 @@ class OrcConfig(C.Structure):
         ("physics", C.c_int32), ("adv_a", C.c_double), ("adv_b", C.c_double),
         ("dt_fixed", C.c_double),
         ("limiter_per_step", C.c_int32), ("limiter_all_vars", C.c_int32), ("fv_unlimited", C.c_int32),
-        ("limiter_characteristic", C.c_int32),
+        ("limiter_characteristic", C.c_int32), ("fv_error_recon", C.c_int32),
+        ("dg_overintegrate", C.c_int32),
     ]
 
 
@@ -96,6 +97,8 @@ def lib():
         L.orc_init_case.argtypes = [cfgp, C.c_int, vp]
         L.orc_point_coords.argtypes = [cfgp, vp, vp]
         L.orc_error.argtypes = [cfgp, vp, C.c_int, d, C.c_int, P(d), P(d), P(d)]
+        L.orc_fv_recon_points.argtypes = [cfgp, vp, C.c_int, vp]
+        L.orc_residual_dg_quad.argtypes = [cfgp, C.c_int, vp, vp]
         _lib = L
     return _lib
 
@@ -108,11 +111,12 @@ def _p(a: np.ndarray):
 def config(nx=10, ny=10, method="cpr", k=1, bc=PERIODIC, box=(-5.0, 5.0, -5.0, 5.0), gamma=1.4,
            cfl=0.24, limiter=0, limiter_eps=1e-3, cpr_chain_rule=1, physics=0, adv=(1.0, 0.5),
            dt_fixed=0.0, limiter_per_step=0, limiter_all_vars=0, fv_unlimited=0,
-           limiter_characteristic=0) -> OrcConfig:
+           limiter_characteristic=0, fv_error_recon=0, dg_overintegrate=0) -> OrcConfig:
     m = METHODS[method] if isinstance(method, str) else int(method)
     return OrcConfig(nx, ny, box[0], box[1], box[2], box[3], bc, m, k, gamma, cfl, limiter,
                      limiter_eps, cpr_chain_rule, physics, adv[0], adv[1], dt_fixed,
-                     limiter_per_step, limiter_all_vars, fv_unlimited, limiter_characteristic)
+                     limiter_per_step, limiter_all_vars, fv_unlimited, limiter_characteristic,
+                     fv_error_recon, dg_overintegrate)
 
 
 def npts(cfg: OrcConfig) -> int:
@@ -292,6 +296,21 @@ def point_coords(cfg):
     X, Y = np.zeros(n), np.zeros(n)
     _chk(lib().orc_point_coords(C.byref(cfg), _p(X), _p(Y)))
     return X, Y
+
+
+def fv_recon_points(cfg, q, var=0):
+    """FV reconstructed solution at the 3x3 Gauss-Legendre points of every cell
+    (reading R22): array [ny*nx, 3 (eta), 3 (xi)]."""
+    out = np.zeros(cfg.nx * cfg.ny * 9)
+    _chk(lib().orc_fv_recon_points(C.byref(cfg), _p(_v4(q)), var, _p(out)))
+    return out.reshape(cfg.nx * cfg.ny, 3, 3)
+
+
+def residual_dg_quad(cfg, q, nq):
+    """DG residual of Eq. (19) with nq-point Gauss-Legendre integrals (f3)."""
+    r = np.zeros(nvalues(cfg))
+    _chk(lib().orc_residual_dg_quad(C.byref(cfg), int(nq), _p(_v4(q)), _p(r)))
+    return r
 
 
 def error(cfg, q, t, case_id=VORTEX, var=0):

@@ -60,6 +60,11 @@ typedef struct {
   int32_t fv_unlimited;      /* FV: 1 = unlimited kappa-scheme (kappa = 0 / 1/3), no minmod (Q10) */
   int32_t limiter_characteristic; /* HO: 1 = Eq. (35) slopes limited in the characteristic fields of
                                      the element average (Cockburn-Shu), not componentwise (Q12) */
+  int32_t fv_error_recon;    /* FV: 1 = error of the reconstructed solution (f4; DESIGN R22),
+                                0 = cell value vs exact cell average */
+  int32_t dg_overintegrate;  /* DG: 1 = volume and surface integrals of Eq. (19) by (k+2)-point
+                                Gauss-Legendre over-integration (SPEC's alternative, f3), 0 = the
+                                n-point collocation of Eq. (20) (Q8) */
 } orc_config;
 
 /* decision counters (parity of branch decisions); a minmod whose
@@ -548,6 +553,98 @@ static void residual_dg(const orc_config *cf, const ops_t *o, const double *Q, d
     }
 }
 
+/* DG residual of Eq. (19) with the integrals by an nq-point Gauss-Legendre rule
+ * (f3 variant: nq = k+2 over-integration; nq = n is residual_dg's collocation).
+ * The solution polynomial q_h is interpolated to the nq x nq quadrature points
+ * (zeta_r, zeta_s) and to nq points along every edge; the fluxes are evaluated
+ * there:
+ *   Vol^x_ab = sum_rs W_r W_s f(q_h(zeta_r, zeta_s)) l'_a(zeta_r) l_b(zeta_s)
+ *   Sur^x_ab = sum_s W_s [l_a(1) F^E(zeta_s) - l_a(-1) F^W(zeta_s)] l_b(zeta_s)
+ * (F^E/W: Rusanov between the two traces q_h(+-1, zeta_s), transmissive ghost =
+ * own trace), y likewise, and with the exact (diagonal) GL mass matrix
+ *   R_ab = (2/dx)(Vol^x - Sur^x)_ab / (w_a w_b) + (2/dy)(Vol^y - Sur^y)_ab / (w_a w_b). */
+static void residual_dg_quad(const orc_config *cf, const ops_t *o, int nq, const double *Q, double *R) {
+  phys_t P = mkphys(cf);
+  int n = o->n, np = n * n;
+  int64_t N = (int64_t)cf->nx * cf->ny * np;
+  double dx = (cf->xmax - cf->xmin) / cf->nx, dy = (cf->ymax - cf->ymin) / cf->ny;
+  double z[MAXN], W[MAXN], Lz[MAXN][MAXN], dLz[MAXN][MAXN];
+  orc_nodes(0, nq, z, W);
+  for (int r = 0; r < nq; ++r) {
+    orc_lagrange(n, o->xi, z[r], Lz[r]);
+    orc_lagrange_deriv(n, o->xi, z[r], dLz[r]);
+  }
+  /* q_h of element m at (x-coordinate weights ex[a], y-coordinate weights ey[b]) */
+#define QH(m_, ex, ey, out)                                                              \
+  for (int c = 0; c < 4; ++c) {                                                         \
+    double acc = 0.0;                                                                   \
+    for (int b = 0; b < n; ++b)                                                         \
+      for (int a = 0; a < n; ++a) acc += (ex)[a] * (ey)[b] * Q[c * N + (m_) * np + b * n + a]; \
+    (out)[c] = acc;                                                                     \
+  }
+  for (int j = 0; j < cf->ny; ++j)
+    for (int i = 0; i < cf->nx; ++i) {
+      int64_t m = (int64_t)j * cf->nx + i;
+      int iw = nb_index(i, -1, cf->nx, cf->bc), ie = nb_index(i, 1, cf->nx, cf->bc);
+      int js = nb_index(j, -1, cf->ny, cf->bc), jn = nb_index(j, 1, cf->ny, cf->bc);
+      int64_t mw = (int64_t)j * cf->nx + iw, me = (int64_t)j * cf->nx + ie;
+      int64_t ms = (int64_t)js * cf->nx + i, mn = (int64_t)jn * cf->nx + i;
+      double f[MAXN][MAXN][4], g[MAXN][MAXN][4];
+      for (int s2 = 0; s2 < nq; ++s2)
+        for (int r = 0; r < nq; ++r) {
+          double q[4];
+          QH(m, Lz[r], Lz[s2], q);
+          flux(&P, 0, q, f[s2][r]);
+          flux(&P, 1, q, g[s2][r]);
+        }
+      double FW[MAXN][4], FE[MAXN][4], FS[MAXN][4], FN[MAXN][4];
+      for (int t = 0; t < nq; ++t) {
+        double qo[4], qn[4];
+        QH(m, o->eL, Lz[t], qo);                       /* own west trace at eta = zeta_t */
+        if (iw >= 0) { QH(mw, o->eR, Lz[t], qn); } else memcpy(qn, qo, sizeof qn);
+        rusanov(&P, 0, qn, qo, FW[t]);
+        QH(m, o->eR, Lz[t], qo);
+        if (ie >= 0) { QH(me, o->eL, Lz[t], qn); } else memcpy(qn, qo, sizeof qn);
+        rusanov(&P, 0, qo, qn, FE[t]);
+        QH(m, Lz[t], o->eL, qo);                       /* own south trace at xi = zeta_t */
+        if (js >= 0) { QH(ms, Lz[t], o->eR, qn); } else memcpy(qn, qo, sizeof qn);
+        rusanov(&P, 1, qn, qo, FS[t]);
+        QH(m, Lz[t], o->eR, qo);
+        if (jn >= 0) { QH(mn, Lz[t], o->eL, qn); } else memcpy(qn, qo, sizeof qn);
+        rusanov(&P, 1, qo, qn, FN[t]);
+      }
+      for (int b = 0; b < n; ++b)
+        for (int a = 0; a < n; ++a)
+          for (int c = 0; c < 4; ++c) {
+            double vx = 0.0, vy = 0.0, sx = 0.0, sy = 0.0;
+            for (int s2 = 0; s2 < nq; ++s2)
+              for (int r = 0; r < nq; ++r) {
+                vx += W[r] * W[s2] * f[s2][r][c] * dLz[r][a] * Lz[s2][b];
+                vy += W[r] * W[s2] * g[s2][r][c] * Lz[r][a] * dLz[s2][b];
+              }
+            for (int t = 0; t < nq; ++t) {
+              sx += W[t] * (o->eR[a] * FE[t][c] - o->eL[a] * FW[t][c]) * Lz[t][b];
+              sy += W[t] * (o->eR[b] * FN[t][c] - o->eL[b] * FS[t][c]) * Lz[t][a];
+            }
+            R[c * N + m * np + b * n + a] = (2.0 / dx) * (vx - sx) / (o->w[a] * o->w[b])
+                                          + (2.0 / dy) * (vy - sy) / (o->w[a] * o->w[b]);
+          }
+    }
+#undef QH
+}
+
+/* the quadrature DG residual with an explicit rule size (tests: nq = n equals
+ * residual_dg up to rounding, nq = k+2 is the over-integrated variant) */
+int orc_residual_dg_quad(const orc_config *cf, int nq, const double *Q, double *R) {
+  int st = check_cfg(cf);
+  if (st) return st;
+  if (cf->method != ORC_DG || nq < cf->k + 1 || nq > 8) return ORC_ERR_ARG;
+  ops_t o;
+  build_ops(cf->method, cf->k, &o);
+  residual_dg_quad(cf, &o, nq, Q, R);
+  return ORC_OK;
+}
+
 /* ------------------------------------------------------------------------- */
 /* SD residual: GL solution points, GLL(k+2) flux points (SURVEY C7;            */
 /* Eqs. (30)-(34), with the Eq. (34) typo f -> g; Algs. 5-6)          */
@@ -707,6 +804,7 @@ int orc_residual_map(const orc_config *cf, const double *Q, double *R, int64_t *
   ops_t o;
   build_ops(cf->method, cf->k, &o);
   if (cf->method == ORC_CPR || cf->method == ORC_NDG) residual_cpr_ndg(cf, &o, Q, R);
+  else if (cf->method == ORC_DG && cf->dg_overintegrate) residual_dg_quad(cf, &o, cf->k + 2, Q, R);
   else if (cf->method == ORC_DG) residual_dg(cf, &o, Q, R);
   else residual_sd(cf, &o, Q, R);
   return ORC_OK;
@@ -1061,6 +1159,51 @@ int orc_point_coords(const orc_config *cf, double *X, double *Y) {
   return ORC_OK;
 }
 
+/* FV reconstructed solution ("For P^2 FV, the error was computed by
+ * reconstructing the solution along element faces, and then using a quadrature
+ * rule to compute an averaged solution"; reading R22 in DESIGN.md).  Per cell
+ * and direction, the scheme's own MUSCL face states (muscl_face: lo = the state
+ * at the cell's i-1/2 face, hi = at its i+1/2 face, limited as in the residual)
+ * and the cell average qbar fix the quadratic on [-1,1]
+ *   q_d(s) = qbar + (hi - lo)/2 s + (hi + lo - 2 qbar)/4 (3 s^2 - 1)
+ * (q_d(-1) = lo, q_d(1) = hi, mean qbar; linear for MUSCL-2, where
+ * hi + lo = 2 qbar).  The cell's solution is q(xi, eta) = q_x(xi) + q_y(eta) -
+ * qbar, evaluated at the 3x3 Gauss-Legendre points (xi_a, eta_b) of the cell,
+ * out[(m*3 + b)*3 + a] (component var). */
+int orc_fv_recon_points(const orc_config *cf, const double *Q, int var, double *out) {
+  int st = check_cfg(cf);
+  if (st) return st;
+  if (cf->method != ORC_FV || var < 0 || var > 3) return ORC_ERR_ARG;
+  int nx = cf->nx, ny = cf->ny;
+  int64_t N = (int64_t)nx * ny;
+  double xg[3], wg[3];
+  orc_nodes(0, 3, xg, wg);
+  for (int j = 0; j < ny; ++j)
+    for (int i = 0; i < nx; ++i) {
+      double s[5][4], qW[4], qE[4], lo[2], hi[2];
+      /* x: faces i-1/2 (cells i-2..i+1; qE is cell i's lo) and i+1/2 (cells i-1..i+2; qW is its hi) */
+      for (int t = 0; t < 5; ++t) getq(Q, N, (int64_t)j * nx + fv_idx(i - 2 + t, nx, cf->bc), 1, 0, s[t]);
+      muscl_face(cf->k, s[0], s[1], s[2], s[3], qW, qE, NULL, cf->fv_unlimited, NULL, NULL);
+      lo[0] = qE[var];
+      muscl_face(cf->k, s[1], s[2], s[3], s[4], qW, qE, NULL, cf->fv_unlimited, NULL, NULL);
+      hi[0] = qW[var];
+      const double qb = s[2][var];
+      for (int t = 0; t < 5; ++t) getq(Q, N, (int64_t)fv_idx(j - 2 + t, ny, cf->bc) * nx + i, 1, 0, s[t]);
+      muscl_face(cf->k, s[0], s[1], s[2], s[3], qW, qE, NULL, cf->fv_unlimited, NULL, NULL);
+      lo[1] = qE[var];
+      muscl_face(cf->k, s[1], s[2], s[3], s[4], qW, qE, NULL, cf->fv_unlimited, NULL, NULL);
+      hi[1] = qW[var];
+      for (int b = 0; b < 3; ++b)
+        for (int a = 0; a < 3; ++a) {
+          double sx = xg[a], sy = xg[b];
+          double qx = qb + 0.5 * (hi[0] - lo[0]) * sx + 0.25 * (hi[0] + lo[0] - 2.0 * qb) * (3.0 * sx * sx - 1.0);
+          double qy = qb + 0.5 * (hi[1] - lo[1]) * sy + 0.25 * (hi[1] + lo[1] - 2.0 * qb) * (3.0 * sy * sy - 1.0);
+          out[((int64_t)j * nx + i) * 9 + b * 3 + a] = qx + qy - qb;
+        }
+    }
+  return ORC_OK;
+}
+
 /* L1/L2/Linf of the error in component var at time t (vortex only).
  * HO methods: pointwise error at the solution points, weighted by the
  * solution-point quadrature, i.e. the RMS over the domain of q_h - q_exact:
@@ -1068,7 +1211,9 @@ int orc_point_coords(const orc_config *cf, double *X, double *Y) {
  *   Linf = max |d_ab|.
  * This reading of "L2 error norm of rho" reproduces Tables
  * 2-3 to the printed 3 digits (tests/golden/paper_tables_2_3.txt).
- * FV: the cell value against the exact cell average (8x8 Gauss-Legendre). */
+ * FV: the cell value against the exact cell average (8x8 Gauss-Legendre); with
+ * fv_error_recon (R22) the same pointwise convention as HO applied to
+ * the reconstructed solution of orc_fv_recon_points at the 3x3 GL points. */
 int orc_error(const orc_config *cf, const double *Q, int case_id, double t, int var,
               double *l1, double *l2, double *linf) {
   int st = check_cfg(cf);
@@ -1078,7 +1223,28 @@ int orc_error(const orc_config *cf, const double *Q, int case_id, double t, int 
   int64_t Ne = (int64_t)nx * ny;
   double dx = (cf->xmax - cf->xmin) / nx, dy = (cf->ymax - cf->ymin) / ny;
   double s1 = 0.0, s2 = 0.0, mx = 0.0;
-  if (cf->method == ORC_FV) {
+  if (cf->method == ORC_FV && cf->fv_error_recon) {
+    double *qr = (double *)malloc(sizeof(double) * 9 * (size_t)Ne);
+    if (!qr) return ORC_ERR_NOMEM;
+    orc_fv_recon_points(cf, Q, var, qr);
+    double xg[3], wg[3];
+    orc_nodes(0, 3, xg, wg);
+    for (int j = 0; j < ny; ++j)
+      for (int i = 0; i < nx; ++i)
+        for (int b = 0; b < 3; ++b)
+          for (int a = 0; a < 3; ++a) {
+            double x = cf->xmin + (i + 0.5) * dx + 0.5 * dx * xg[a];
+            double y = cf->ymin + (j + 0.5) * dy + 0.5 * dy * xg[b];
+            double qe[4];
+            case_state(cf, case_id, x, y, t, qe);
+            double d = qr[((int64_t)j * nx + i) * 9 + b * 3 + a] - qe[var];
+            double wq = 0.25 * wg[a] * wg[b];
+            s1 += wq * fabs(d);
+            s2 += wq * d * d;
+            if (fabs(d) > mx) mx = fabs(d);
+          }
+    free(qr);
+  } else if (cf->method == ORC_FV) {
     for (int j = 0; j < ny; ++j)
       for (int i = 0; i < nx; ++i) {
         double qa[4];

@@ -232,6 +232,69 @@ __global__ void k_err(const AuxArgs A, Nodes nd, GL8v g8, const double* __restri
   }
 }
 
+// FV reconstructed-solution error (reading R22): per cell, the MUSCL
+// face states of the scheme (cell_faces, the stage kernel's reconstruction) and
+// the cell value fix one quadratic per direction,
+//   q_d(s) = qbar + (hi - lo)/2 s + (hi + lo - 2 qbar)/4 (3 s^2 - 1),
+// the cell's solution is q_x(xi) + q_y(eta) - qbar, compared pointwise with the
+// exact vortex at the 3x3 Gauss-Legendre points (weights w_a w_b / 4), like the
+// HO convention R8.  One thread per cell; y-neighbours beyond the strip from the
+// ghost rows (2 rows, component stride gcs), or clamped (transmissive).
+template <int REC>
+__global__ void k_err_fvr(const AuxArgs A, Nodes g3, const double* __restrict__ q, const double* glo,
+                          const double* ghi, long long gcs, int bcx, int var, const double* clk, double* part) {
+  __shared__ double s1[32], s2[32], s3[32];
+  const long long ne = (long long)A.nx * A.nrows;
+  const double dx = (A.xmax - A.xmin) / A.nx, dy = (A.ymax - A.ymin) / A.ny_global;
+  const double t = clk[0];
+  const double* qv = q + var * A.cs;
+  double a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  for (long long m = blockIdx.x * (long long)blockDim.x + threadIdx.x; m < ne; m += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(m % A.nx), jl = (int)(m / A.nx), j = jl + A.row0;
+    int iw = i - 1, ie = i + 1;
+    if (bcx == 0) { iw = iw < 0 ? iw + A.nx : iw; ie = ie >= A.nx ? ie - A.nx : ie; }
+    else { iw = iw < 0 ? 0 : iw; ie = ie >= A.nx ? A.nx - 1 : ie; }
+    const double qb = qv[m];
+    const double qw = qv[(long long)jl * A.nx + iw], qe = qv[(long long)jl * A.nx + ie];
+    const double qs = jl > 0 ? qv[m - A.nx] : (glo ? glo[var * gcs + (long long)A.nx + i] : qb);
+    const double qn = jl + 1 < A.nrows ? qv[m + A.nx] : (ghi ? ghi[var * gcs + i] : qb);
+    double lx, hx, ly, hy;
+    cell_faces<REC>(qw, qb, qe, lx, hx, nullptr, 0);
+    cell_faces<REC>(qs, qb, qn, ly, hy, nullptr, 0);
+    const double xc = A.xmin + (i + 0.5) * dx, yc = A.ymin + (j + 0.5) * dy;
+#pragma unroll
+    for (int b = 0; b < 3; ++b) {
+      const double sy = g3.xi[b];
+      const double qy = qb + 0.5 * (hy - ly) * sy + 0.25 * (hy + ly - 2.0 * qb) * (3.0 * sy * sy - 1.0);
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const double sx = g3.xi[a];
+        const double qx = qb + 0.5 * (hx - lx) * sx + 0.25 * (hx + lx - 2.0 * qb) * (3.0 * sx * sx - 1.0);
+        double v[4];
+        vortex(A, xc + 0.5 * dx * sx, yc + 0.5 * dy * sy, t, v);
+        const double d = (qx + qy - qb) - v[var];
+        const double w = 0.25 * g3.w[a] * g3.w[b];
+        a1 += w * fabs(d);
+        a2 += w * d * d;
+        a3 = nanmax(a3, fabs(d));
+      }
+    }
+  }
+  a1 = warp_sum(a1);
+  a2 = warp_sum(a2);
+  a3 = warp_max(a3);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) { s1[wid] = a1; s2[wid] = a2; s3[wid] = a3; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b1 = 0, b2 = 0, b3 = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { b1 += s1[w]; b2 += s2[w]; b3 = nanmax(b3, s3[w]); }
+    part[3 * blockIdx.x] = b1;
+    part[3 * blockIdx.x + 1] = b2;
+    part[3 * blockIdx.x + 2] = b3;
+  }
+}
+
 __global__ void k_err_final(const double* part, int nb, double* out3) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   double b1 = 0, b2 = 0, b3 = 0;
@@ -503,6 +566,21 @@ int launch_error_partials(const AuxArgs& a, const double* q, int var, const doub
   int nb = grid_for(a.cs, 256);
   if (nb > max_blocks) nb = max_blocks;
   k_err<<<nb, 256, 0, s>>>(a, nodes_for(a.method, a.k), gl8(), q, var, clock, part);
+  return nb;
+}
+
+int launch_error_fv_recon(const AuxArgs& a, const double* q, const double* glo, const double* ghi, long long gcs,
+                          int bcx, int unlimited, int var, const double* clock, double* part, int max_blocks,
+                          cudaStream_t s) {
+  int nb = grid_for((long long)a.nx * a.nrows, 256);
+  if (nb > max_blocks) nb = max_blocks;
+  const Nodes g3 = nodes_for(2 /* Gauss-Legendre */, 2);
+  switch (a.k + (unlimited ? 2 : 0)) {
+    case 1: k_err_fvr<1><<<nb, 256, 0, s>>>(a, g3, q, glo, ghi, gcs, bcx, var, clock, part); break;
+    case 2: k_err_fvr<2><<<nb, 256, 0, s>>>(a, g3, q, glo, ghi, gcs, bcx, var, clock, part); break;
+    case 3: k_err_fvr<3><<<nb, 256, 0, s>>>(a, g3, q, glo, ghi, gcs, bcx, var, clock, part); break;
+    default: k_err_fvr<4><<<nb, 256, 0, s>>>(a, g3, q, glo, ghi, gcs, bcx, var, clock, part); break;
+  }
   return nb;
 }
 

@@ -211,4 +211,52 @@ __device__ __forceinline__ double minmod2(double a, double b, long long* dec, in
   return r;
 }
 
+// FV MUSCL reconstruction, shared by the FV stage kernel
+// and the reconstructed-solution error.
+// the two reconstructed face values of cell i (stencil i-1, i, i+1): lo at its
+// i-1/2 face, hi at its i+1/2 face (the face states of P:346-351; SURVEY C8 with
+// the same arithmetic as the per-face form, so values are bitwise those of
+// reconstructing at each face).  w = how many face evaluations of the paper's
+// form this one reconstruction stands for (decision counting only).
+template <int ORDER>
+__device__ __forceinline__ void cell_faces(double qm, double q0, double qp, double& lo, double& hi, long long* dec,
+                                           int w, long long* mp = nullptr) {
+  // explicit rounding (no contraction freedom): a face state is bitwise the same
+  // wherever it is evaluated (prologue or carried), so results do not depend on
+  // how the rows are split over CTAs / launches / ranks
+  if (ORDER == 3) {  // unlimited kappa = 0 (f3 variant of MUSCL-2)
+    const double d = (q0 - qm) + (qp - q0);
+    hi = __fma_rn(0.25, d, q0);
+    lo = __fma_rn(-0.25, d, q0);
+  } else if (ORDER == 4) {  // unlimited kappa = 1/3 (f3 variant of MUSCL-3)
+    constexpr double kap = 1.0 / 3.0;
+    const double dm = q0 - qm, dp = qp - q0;
+    constexpr double c1 = 0.25 * (1.0 - kap), c2 = 0.25 * (1.0 + kap);
+    hi = __fma_rn(c1, dm, __fma_rn(c2, dp, q0));
+    lo = __fma_rn(-c1, dp, __fma_rn(-c2, dm, q0));
+  } else if (ORDER == 1) {
+    const double s = minmod2(q0 - qm, qp - q0, dec, w, mp);
+    hi = __fma_rn(0.5, s, q0);
+    lo = __fma_rn(-0.5, s, q0);
+  } else {  // kappa = 1/3, beta = (3 - kappa)/(1 - kappa) = 4
+    constexpr double kap = 1.0 / 3.0, beta = (3.0 - kap) / (1.0 - kap);
+    const double dm = q0 - qm, dp = qp - q0;
+    double A, B;
+    if (dec) {
+      A = minmod2(dm, beta * dp, dec, w, mp);
+      B = minmod2(dp, beta * dm, dec, w, mp);
+    } else {  // both minmods share the sign test (beta > 0): one sign-bit comparison
+      const double bdp = beta * dp, bdm = beta * dm;
+      const bool same = (__double2hiint(dm) ^ __double2hiint(dp)) >= 0;
+      const double ma = fabs(dm) <= fabs(bdp) ? dm : bdp, mb = fabs(dp) <= fabs(bdm) ? dp : bdm;
+      A = same ? ma : 0.0;
+      B = same ? mb : 0.0;
+    }
+    // q0 +- ((1 - kappa) X + (1 + kappa) Y) / 4 with the quarter folded into the weights
+    constexpr double c1 = 0.25 * (1.0 - kap), c2 = 0.25 * (1.0 + kap);
+    hi = __fma_rn(c1, A, __fma_rn(c2, B, q0));
+    lo = __fma_rn(-c1, B, __fma_rn(-c2, A, q0));
+  }
+}
+
 }  // namespace h2d

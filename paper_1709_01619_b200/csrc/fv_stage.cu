@@ -30,52 +30,6 @@ namespace {
 constexpr int FTX = H2D_FTX, FRB = 64, FD = H2D_FV_DEPTH, FNS = 3 + FD;  // cells/strip, rows/march, in flight, ring rows
 constexpr int FW = FTX + 4;                    // ring row width: 2 halo cells each side
 
-// the two reconstructed face values of cell i (stencil i-1, i, i+1): lo at its
-// i-1/2 face, hi at its i+1/2 face (the face states of P:346-351; SURVEY C8 with
-// the same arithmetic as the per-face form, so values are bitwise those of
-// reconstructing at each face).  w = how many face evaluations of the paper's
-// form this one reconstruction stands for (decision counting only).
-template <int ORDER>
-__device__ __forceinline__ void cell_faces(double qm, double q0, double qp, double& lo, double& hi, long long* dec,
-                                           int w, long long* mp = nullptr) {
-  // explicit rounding (no contraction freedom): a face state is bitwise the same
-  // wherever it is evaluated (prologue or carried), so results do not depend on
-  // how the rows are split over CTAs / launches / ranks
-  if (ORDER == 3) {  // unlimited kappa = 0 (f3 variant of MUSCL-2)
-    const double d = (q0 - qm) + (qp - q0);
-    hi = __fma_rn(0.25, d, q0);
-    lo = __fma_rn(-0.25, d, q0);
-  } else if (ORDER == 4) {  // unlimited kappa = 1/3 (f3 variant of MUSCL-3)
-    constexpr double kap = 1.0 / 3.0;
-    const double dm = q0 - qm, dp = qp - q0;
-    constexpr double c1 = 0.25 * (1.0 - kap), c2 = 0.25 * (1.0 + kap);
-    hi = __fma_rn(c1, dm, __fma_rn(c2, dp, q0));
-    lo = __fma_rn(-c1, dp, __fma_rn(-c2, dm, q0));
-  } else if (ORDER == 1) {
-    const double s = minmod2(q0 - qm, qp - q0, dec, w, mp);
-    hi = __fma_rn(0.5, s, q0);
-    lo = __fma_rn(-0.5, s, q0);
-  } else {  // kappa = 1/3, beta = (3 - kappa)/(1 - kappa) = 4
-    constexpr double kap = 1.0 / 3.0, beta = (3.0 - kap) / (1.0 - kap);
-    const double dm = q0 - qm, dp = qp - q0;
-    double A, B;
-    if (dec) {
-      A = minmod2(dm, beta * dp, dec, w, mp);
-      B = minmod2(dp, beta * dm, dec, w, mp);
-    } else {  // both minmods share the sign test (beta > 0): one sign-bit comparison
-      const double bdp = beta * dp, bdm = beta * dm;
-      const bool same = (__double2hiint(dm) ^ __double2hiint(dp)) >= 0;
-      const double ma = fabs(dm) <= fabs(bdp) ? dm : bdp, mb = fabs(dp) <= fabs(bdm) ? dp : bdm;
-      A = same ? ma : 0.0;
-      B = same ? mb : 0.0;
-    }
-    // q0 +- ((1 - kappa) X + (1 + kappa) Y) / 4 with the quarter folded into the weights
-    constexpr double c1 = 0.25 * (1.0 - kap), c2 = 0.25 * (1.0 + kap);
-    hi = __fma_rn(c1, A, __fma_rn(c2, B, q0));
-    lo = __fma_rn(-c1, B, __fma_rn(-c2, A, q0));
-  }
-}
-
 // TWICE the Rusanov flux along DIR: fL + fR - lam (qR - qL).  The
 // factor 1/2 moves into the metric of the flux difference (0.5 / dx): scaling
 // by powers of two is exact, so nothing changes but 5 multiplications per face.
@@ -347,6 +301,270 @@ __global__ void __launch_bounds__(FTX, H2D_FV_MINB) fv_stage_kernel(const StageA
   if (HLAM && a.lam) block_max_to(lam, a.lam, sred);
 }
 
+// ---------------------------------------------------------------------------
+// Warp-strip variant: every warp marches its own strip of WS = 64 cells (two
+// adjacent cells per lane) up the rows, with its own cp.async ring and no CTA
+// barrier in the march:
+//  * the ring slots are compile-time (the march is unrolled by the ring size),
+//    so shared-memory addresses are constants off one base;
+//  * a lane reconstructs its two cells in x (one 16-B read of its pair + the
+//    two neighbour values), the face between them is lane-local, the W face of
+//    its first cell takes the left lane's hi state by a shuffle, and the E face
+//    of its second cell is the right lane's W-face flux by a shuffle; the
+//    strip's two end faces are computed by lanes 0 / last (divergent, 1 of 32);
+//  * y faces as in the CTA kernel: the N face of each column is carried to the
+//    next row as its S face.
+// Arithmetic per face / cell is the CTA kernel's (same helpers, same order),
+// so results are bitwise those of fv_stage_kernel.
+#ifndef H2D_FVW_DEPTH
+#define H2D_FVW_DEPTH 1
+#endif
+#ifndef H2D_FVW_MINB
+#define H2D_FVW_MINB 3
+#endif
+namespace {
+constexpr int WPC = 4;                     // warps per CTA (independent strips)
+constexpr int WS = 64, WW = WS + 4;        // cells per warp strip; ring row width (2 halo cells each side)
+constexpr int WD = H2D_FVW_DEPTH, WNS = 3 + WD;  // rows in flight; ring rows
+constexpr int QS = WD + 1;                       // q^n ring rows (row x lands with ring row x+2, read at step x)
+// dynamic shared memory: per warp WNS ring rows x 4 components x WW, then (stages
+// with q^n) QS q-ring rows x 4 x WS, then the block-max scratch
+constexpr int WRING = WNS * 4 * WW, WQ = QS * 4 * WS;
+constexpr size_t fvw_smem(bool hq0) { return sizeof(double) * ((size_t)WPC * (WRING + (hq0 ? WQ : 0)) + WPC); }
+}  // namespace
+
+template <int ORDER, bool REC, int V>
+__global__ void __launch_bounds__(WPC * 32, H2D_FVW_MINB) fv_warp_kernel(const StageArgs a, const int vec) {
+  const bool HQ0 = V == 8 ? a.q0 != nullptr : (V & 1), HLAM = V == 8 ? (a.lam || a.bad) : (V & 2) != 0;
+  extern __shared__ __align__(16) double fv_smem[];
+  double(*const ring)[WNS][4][WW] = reinterpret_cast<double(*)[WNS][4][WW]>(fv_smem);
+  double(*const qring)[QS][4][WS] = reinterpret_cast<double(*)[QS][4][WS]>(fv_smem + WPC * WRING);
+  double* const sred = fv_smem + WPC * WRING + (HQ0 ? WPC * WQ : 0);
+  pdl_wait();
+  pdl_launch();
+  double dtv = 1.0;
+  if (a.dt) {
+    dtv = *a.dt;
+    if (dtv == 0.0) return;
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int i0 = (blockIdx.x * WPC + wid) * WS, jb = a.row_lo + blockIdx.y * a.rows;
+  const double gam = a.gamma, gm1 = a.gamma - 1.0;
+  double lam = 0.0;
+  if (i0 < a.nx) {  // warp-uniform
+    const int TXv = min(WS, a.nx - i0), RBv = min(a.rows, a.row_hi - jb);
+    const int c0 = 2 * lane;                         // local index of the lane's first cell
+    const bool own0 = c0 < TXv, own1 = c0 + 1 < TXv;
+    const int last = (TXv - 1) >> 1;                 // lane holding the strip's last cell
+    const bool evenT = (TXv & 1) == 0;               // last lane's second cell is real (else: the halo cell)
+    long long* const dec = REC ? a.dec : nullptr;
+    double(*const rw)[4][WW] = ring[wid];
+    double(*const qw)[4][WS] = qring[HQ0 ? wid : 0];
+    // halo column of lanes 0..3: slots 0, 1 = cells i0-2, i0-1; TXv+2, TXv+3 = cells i0+TXv, +1
+    int hx = lane < 2 ? i0 - 2 + lane : i0 + TXv + (lane - 2);
+    if (a.bcx == 0) hx = hx < 0 ? hx + a.nx : (hx >= a.nx ? hx - a.nx : hx);
+    else hx = hx < 0 ? 0 : (hx >= a.nx ? a.nx - 1 : hx);
+    const int hslot = lane < 2 ? lane : TXv + lane;
+    auto row_ptr = [&](int jr, long long& cs) -> const double* {
+      cs = a.cs;
+      if (jr < 0) {
+        if (a.ghost_lo) { cs = a.gcs; return a.ghost_lo + (long long)(jr + 2) * a.nx; }
+        jr = 0;
+      } else if (jr >= a.nrows) {
+        if (a.ghost_hi) { cs = a.gcs; return a.ghost_hi + (long long)(jr - a.nrows) * a.nx; }
+        jr = a.nrows - 1;
+      }
+      return a.q + (long long)jr * a.nx;
+    };
+    auto dmap_at = [&](int jr, int ir) -> long long* {
+      if (!REC || !a.dmap) return nullptr;
+      if (ir < 0) ir = a.bcx == 0 ? ir + a.nx : 0;
+      if (ir >= a.nx) ir = a.bcx == 0 ? ir - a.nx : a.nx - 1;
+      if (jr < 0) jr = a.ghost_lo ? jr + a.nrows : 0;
+      if (jr >= a.nrows) jr = a.ghost_hi ? jr - a.nrows : a.nrows - 1;
+      return a.dmap + (long long)jr * a.nx + ir;
+    };
+    // the lane's pair (16 B when aligned) of each component of a row into dst[c][...]
+    auto copy_pair = [&](double* d0, int dstride, const double* g, long long cs) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        double* d = d0 + c * dstride;
+        const double* gc = g + c * cs;
+        if (vec) {
+          if (own1) asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(d)), "l"(gc) : "memory");
+          else if (own0) asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(d)), "l"(gc) : "memory");
+        } else {
+          if (own0) asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(d)), "l"(gc) : "memory");
+          if (own1)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(d + 1)), "l"(gc + 1) : "memory");
+        }
+      }
+    };
+    auto issue_row = [&](int jr, int slot) {
+      long long cs;
+      const double* rb = row_ptr(jr, cs);
+      copy_pair(&rw[slot][0][c0 + 2], WW, rb + i0 + c0, cs);
+      if (lane < 4) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(&rw[slot][c][hslot])),
+                       "l"(rb + c * cs + hx)
+                       : "memory");
+      }
+    };
+    auto issue_q0 = [&](int jr, int slot) {  // q^n row jr (an own row) into q-ring slot
+      copy_pair(&qw[slot][0][c0], WS, a.q0 + (long long)jr * a.nx + i0 + c0, a.cs);
+    };
+    auto commit = [] { asm volatile("cp.async.commit_group;" ::: "memory"); };
+
+    // prologue: rows jb-2 .. jb+1 (ring slot of row r: (r + 2) % WNS) and q^n rows
+    // jb .. jb+WD-1 (q slot r); the S face of row jb and the hi y-state of row jb;
+    // then rows jb+2 .. jb+1+WD, one group each (row jb+2 into row jb-2's slot)
+    for (int r = -2; r <= 1; ++r) issue_row(jb + r, r + 2);
+    if (HQ0)
+      for (int r = 0; r < WD && r < RBv; ++r) issue_q0(jb + r, r);
+    commit();
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncwarp();
+    double GS[2][4], yHi[2][4];
+    {
+      const int wb = (jb == 0 && a.count_bot) ? 1 : 0;
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const bool ok = k ? own1 : own0;
+        double lo[4], hi[4], dm;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const double r0 = rw[0][c][c0 + 2 + k], r1 = rw[1][c][c0 + 2 + k];
+          const double r2 = rw[2][c][c0 + 2 + k], r3 = rw[3][c][c0 + 2 + k];
+          cell_faces<ORDER>(r0, r1, r2, dm, hi[c], ok ? dec : nullptr, wb, ok ? dmap_at(jb - 1, i0 + c0 + k) : nullptr);
+          cell_faces<ORDER>(r1, r2, r3, lo[c], yHi[k][c], ok ? dec : nullptr, 2, ok ? dmap_at(jb, i0 + c0 + k) : nullptr);
+        }
+        rusanov2<1>(hi, lo, gm1, gam, GS[k]);
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int k = 2; k < 2 + WD; ++k) {
+      if (k <= RBv + 1) issue_row(jb + k, (k + 2) % WNS);
+      commit();
+    }
+
+    const double bdt = a.bcoef * dtv;
+    const double hrdx = 0.5 * a.rdx2, hrdy = 0.5 * a.rdy2;
+    // ring slots of rows r, r+1, r+2 and of the row issued at step r (r+2+WD: the
+    // slot of row r-1), q-ring slots of rows r (read) and r+WD (issued)
+    int S0 = 2 % WNS, S1 = 3 % WNS, S2 = 4 % WNS, SI = 1 % WNS, Q0 = 0, QI = WD % QS;
+    auto adv = [](int& x, int n) { x = (x + 1 == n) ? 0 : x + 1; };
+#pragma unroll 1
+    for (int r = 0; r < RBv; ++r) {
+      asm volatile("cp.async.wait_group %0;" ::"n"(WD - 1) : "memory");
+      __syncwarp();
+      if (r + 2 + WD <= RBv + 1) issue_row(jb + r + 2 + WD, SI);
+      if (HQ0 && r + WD < RBv) issue_q0(jb + r + WD, QI);
+      commit();
+      const int jr = jb + r;
+      const long long gidx = (long long)jr * a.nx + (i0 + c0);
+      // x: the pair, its neighbours, the face states of both cells; then the W
+      // face of the first cell, the face between them and (by shuffle) the E
+      // face of the second, reduced at once to the x flux differences Rx
+      double xq[2][4], Rx[2][4];
+      {
+        double lo[2][4], hi[2][4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const double2 p = *reinterpret_cast<const double2*>(&rw[S0][c][c0 + 2]);
+          const double xm = rw[S0][c][c0 + 1], xp = rw[S0][c][c0 + 4];
+          xq[0][c] = p.x;
+          xq[1][c] = p.y;
+          cell_faces<ORDER>(xm, p.x, p.y, lo[0][c], hi[0][c], own0 ? dec : nullptr, 2,
+                            own0 ? dmap_at(jr, i0 + c0) : nullptr);
+          // second cell: own, or (last lane, odd TXv) the halo cell i0+TXv
+          const bool h1 = !own1 && lane == last;
+          const int w1 = own1 ? 2 : (h1 && i0 + TXv == a.nx ? 1 : 0);
+          cell_faces<ORDER>(p.x, p.y, xp, lo[1][c], hi[1][c], (own1 || h1) ? dec : nullptr, w1,
+                            (own1 || h1) ? dmap_at(jr, i0 + c0 + 1) : nullptr);
+        }
+        double FW[4], FM[4], FE[4];
+        {
+          // hi state of the cell left of the pair: the left lane's, or (lane 0) cell i0-1
+          double hL[4];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) hL[c] = __shfl_up_sync(0xffffffffu, hi[1][c], 1);
+          if (lane == 0) {
+            double dm;
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+              cell_faces<ORDER>(rw[S0][c][0], rw[S0][c][1], rw[S0][c][2], dm, hL[c], dec, i0 == 0 ? 1 : 0,
+                                dmap_at(jr, i0 - 1));
+          }
+          rusanov2<0>(hL, lo[0], gm1, gam, FW);
+        }
+        rusanov2<0>(hi[0], lo[1], gm1, gam, FM);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) FE[c] = __shfl_down_sync(0xffffffffu, FW[c], 1);
+        if (lane == last && evenT) {  // the strip's last E face: hi of the last cell, lo of cell i0+TXv
+          double lh[4], dm;
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            cell_faces<ORDER>(rw[S0][c][TXv + 1], rw[S0][c][TXv + 2], rw[S0][c][TXv + 3], lh[c], dm, dec,
+                              (i0 + TXv == a.nx) ? 1 : 0, dmap_at(jr, i0 + TXv));
+          rusanov2<0>(hi[1], lh, gm1, gam, FE);
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          Rx[0][c] = -(FM[c] - FW[c]) * hrdx;  // fluxes are 2 F
+          Rx[1][c] = -(FE[c] - FM[c]) * hrdx;
+        }
+      }
+      // y, per column: the lo / hi states of row r+1 (rows r .. r+2), the N face,
+      // the residual, the RK combination and the store
+      const int wn = (r + 1 < RBv) ? 2 : ((jb + RBv == a.nrows) ? 1 : 0);
+      double o[2][4];
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const bool ok = k ? own1 : own0;
+        double ylo[4], yhn[4], GN[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          cell_faces<ORDER>(xq[k][c], rw[S1][c][c0 + 2 + k], rw[S2][c][c0 + 2 + k], ylo[c], yhn[c],
+                            ok ? dec : nullptr, wn, ok ? dmap_at(jr + 1, i0 + c0 + k) : nullptr);
+        rusanov2<1>(yHi[k], ylo, gm1, gam, GN);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const double R = Rx[k][c] - (GN[c] - GS[k][c]) * hrdy;
+          double v = fma(a.a1, xq[k][c], bdt * R);
+          if (HQ0) v = fma(a.a0, qw[Q0][c][c0 + k], v);
+          o[k][c] = v;
+          GS[k][c] = GN[c];
+          yHi[k][c] = yhn[c];
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        double* g = a.out + c * a.cs + gidx;
+        if (vec && own1) {
+          *reinterpret_cast<double2*>(g) = make_double2(o[0][c], o[1][c]);
+        } else {
+          if (own0) g[0] = o[0][c];
+          if (own1) g[1] = o[1][c];
+        }
+      }
+      if (HLAM) {
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          if (!(k ? own1 : own0)) continue;
+          const Prim w = prims(o[k], gm1);
+          lam = nanmax(lam, fmax(fabs(w.u), fabs(w.v)) + fsqrt(gam * w.p * w.ri));
+          if (a.bad && !admissible(o[k][0], w.p)) atomicMin(a.bad, (unsigned long long)(gidx + k));
+        }
+      }
+      adv(S0, WNS); adv(S1, WNS); adv(S2, WNS); adv(SI, WNS); adv(Q0, QS); adv(QI, QS);
+    }
+  }
+  if (HLAM && a.lam) block_max_to(lam, a.lam, sred);
+}
+
 int march_rows(int nrows, int strips, int rb_max, int ctas_per_sm) {
   static int nsm = 0;
   if (!nsm) {
@@ -361,39 +579,89 @@ int march_rows(int nrows, int strips, int rb_max, int ctas_per_sm) {
   return (int)rows;
 }
 
+#ifndef H2D_FV_WARP
+#define H2D_FV_WARP 1  // warp-strip kernel (0: the CTA-strip kernel)
+#endif
+template <int ORDER, bool REC, int V>
+static cudaError_t fvw_launch(dim3 grid, const StageArgs& a, cudaStream_t s, int vec) {
+  static std::atomic<unsigned long long> attr{0};
+  const size_t sm = fvw_smem(V == 8 ? a.q0 != nullptr : (V & 1) != 0);
+  const cudaError_t e = smem_optin(fv_warp_kernel<ORDER, REC, V>, (int)fvw_smem(true), attr);
+  if (e != cudaSuccess) return e;
+  return launch_pdl_if(!a.no_pdl, fv_warp_kernel<ORDER, REC, V>, grid, dim3(WPC * 32), sm, s, a, vec);
+}
+// rows per CTA such that the grid is (close to) a whole number of waves of
+// ctas_per_sm x #SM resident CTAs: the fewest waves whose marches fit rb_max
+int march_rows_waves(int nrows, int strips, int rb_max, int ctas_per_sm) {
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || nsm <= 0) nsm = 148;
+  }
+  const long long target = (long long)ctas_per_sm * nsm;
+  for (long long w = 1;; ++w) {
+    const long long bpc = w * target / strips;  // row blocks per strip column in w waves
+    if (bpc < 1) continue;
+    const long long rows = (nrows + bpc - 1) / bpc;
+    if (rows <= rb_max) return (int)(rows < 1 ? 1 : rows);
+  }
+}
+
 template <int ORDER, bool REC>
-static void fv_launch_v(int v, dim3 grid, const StageArgs& a, cudaStream_t s) {
+static void fv_launch_v(int v, dim3 grid, const StageArgs& a, cudaStream_t s, int vec) {
+#if H2D_FV_WARP
+  switch (v) {
+    case 0: fvw_launch<ORDER, REC, 0>(grid, a, s, vec); break;
+    case 1: fvw_launch<ORDER, REC, 1>(grid, a, s, vec); break;
+    case 3: fvw_launch<ORDER, REC, 3>(grid, a, s, vec); break;
+    default: fvw_launch<ORDER, REC, 8>(grid, a, s, vec); break;
+  }
+#else
+  (void)vec;
   switch (v) {
     case 0: launch_pdl_if(!a.no_pdl, fv_stage_kernel<ORDER, REC, 0>, grid, dim3(FTX), 0, s, a); break;
     case 1: launch_pdl_if(!a.no_pdl, fv_stage_kernel<ORDER, REC, 1>, grid, dim3(FTX), 0, s, a); break;
     case 3: launch_pdl_if(!a.no_pdl, fv_stage_kernel<ORDER, REC, 3>, grid, dim3(FTX), 0, s, a); break;
     default: launch_pdl_if(!a.no_pdl, fv_stage_kernel<ORDER, REC, 8>, grid, dim3(FTX), 0, s, a); break;
   }
+#endif
 }
 
 template <bool REC>
-static void fv_launch_r(int rec, int v, dim3 grid, const StageArgs& a, cudaStream_t s) {
+static void fv_launch_r(int rec, int v, dim3 grid, const StageArgs& a, cudaStream_t s, int vec) {
   switch (rec) {
-    case 1: fv_launch_v<1, REC>(v, grid, a, s); break;
-    case 2: fv_launch_v<2, REC>(v, grid, a, s); break;
-    case 3: fv_launch_v<3, REC>(v, grid, a, s); break;
-    default: fv_launch_v<4, REC>(v, grid, a, s); break;
+    case 1: fv_launch_v<1, REC>(v, grid, a, s, vec); break;
+    case 2: fv_launch_v<2, REC>(v, grid, a, s, vec); break;
+    case 3: fv_launch_v<3, REC>(v, grid, a, s, vec); break;
+    default: fv_launch_v<4, REC>(v, grid, a, s, vec); break;
   }
 }
 
+static bool al16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
 int launch_fv_stage(int k, const StageArgs& a0, cudaStream_t s) {
   StageArgs a = a0;
-  const int strips = (a.nx + FTX - 1) / FTX;
   const int nr = row_range(a);
   if (nr <= 0) return 0;
+#if H2D_FV_WARP
+  const int strips = ((a.nx + WS - 1) / WS + WPC - 1) / WPC;  // CTAs across x
+  a.rows = march_rows_waves(nr, strips, FRB, H2D_FVW_MINB);
+  // 16-B pair accesses: every row / component start even and every array 16-B aligned
+  const int vec = (a.nx % 2 == 0) && (a.cs % 2 == 0) && (a.gcs % 2 == 0) && al16(a.q) && al16(a.q0) &&
+                  al16(a.out) && al16(a.ghost_lo) && al16(a.ghost_hi);
+#else
+  const int strips = (a.nx + FTX - 1) / FTX;
   a.rows = march_rows(nr, strips, FRB, H2D_FV_MINB);
+  const int vec = 0;
+#endif
   dim3 grid(strips, (nr + a.rows - 1) / a.rows);
   // reconstruction: 1 MUSCL-2, 2 MUSCL-3 (minmod-limited); 3 / 4 the same
   // kappa-schemes unlimited (hom2d_config.fv_unlimited, f3)
   const int rec = k + (a.fv_unlimited ? 2 : 0);
   const int v = (a.q0 ? 1 : 0) | ((a.lam || a.bad) ? 2 : 0);
-  if (a.dec) fv_launch_r<true>(rec, v, grid, a, s);
-  else fv_launch_r<false>(rec, v, grid, a, s);
+  if (a.dec) fv_launch_r<true>(rec, v, grid, a, s, vec);
+  else fv_launch_r<false>(rec, v, grid, a, s, vec);
   return (int)cudaPeekAtLastError();
 }
 

@@ -108,7 +108,7 @@ hom2d_status check_cfg(const hom2d_config* c, int nranks) {
   if (c->ny / nranks < G) return HOM2D_ERR_MESH;
   if (!(c->gamma > 1.0) || !(c->cfl > 0.0)) return HOM2D_ERR_ARG;
   if ((unsigned)c->limiter_per_step > 1u || (unsigned)c->limiter_all_vars > 1u || (unsigned)c->fv_unlimited > 1u ||
-      (unsigned)c->limiter_characteristic > 1u)
+      (unsigned)c->limiter_characteristic > 1u || (unsigned)c->fv_error_recon > 1u)
     return HOM2D_ERR_ARG;
   return HOM2D_OK;
 }
@@ -687,7 +687,18 @@ hom2d_status hom2d_error(hom2d* h, int32_t case_id, int32_t var, double* l1, dou
   GUARD(h);
   if (case_id != HOM2D_CASE_VORTEX) return fail(h, HOM2D_ERR_ARG, "error: exact solution only for the vortex");
   if (var < 0 || var > 3) return fail(h, HOM2D_ERR_ARG, "error: var must be 0..3");
-  const int nb = launch_error_partials(aux(h), h->Qn, var, h->clock, h->part, h->max_part, h->stream);
+  int nb;
+  if (h->cfg.method == HOM2D_FV && h->cfg.fv_error_recon) {
+    // the reconstruction reads one cell row beyond the strip: the FV ghost rows
+    const double *lo, *hi;
+    long long gcs;
+    hom2d_status st = exchange(h, h->Qn, h->nloc, h->cfg.nx, &lo, &hi, &gcs, h->glo, h->ghi, 2, h->stream);
+    if (st) return st;
+    nb = launch_error_fv_recon(aux(h), h->Qn, lo, hi, gcs, h->cfg.bc, h->cfg.fv_unlimited, var, h->clock, h->part,
+                               h->max_part, h->stream);
+  } else {
+    nb = launch_error_partials(aux(h), h->Qn, var, h->clock, h->part, h->max_part, h->stream);
+  }
   launch_error_final(h->part, nb, h->err3, h->stream);
   h->launches += 2;
   CU(h, cudaPeekAtLastError());

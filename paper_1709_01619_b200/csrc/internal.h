@@ -121,6 +121,11 @@ void launch_init_case(const AuxArgs& a, int case_id, double* q, cudaStream_t s);
 int launch_error_partials(const AuxArgs& a, const double* q, int var, const double* clock, double* part,
                           int max_blocks, cudaStream_t s);
 void launch_error_final(const double* part, int nblocks, double* out3, cudaStream_t s);
+// FV reconstructed-solution error partials (hom2d_config.fv_error_recon);
+// glo / ghi: 2 ghost rows each side (component stride gcs), nullptr = transmissive
+int launch_error_fv_recon(const AuxArgs& a, const double* q, const double* glo, const double* ghi, long long gcs,
+                          int bcx, int unlimited, int var, const double* clock, double* part, int max_blocks,
+                          cudaStream_t s);
 // averages Qbar[4][nx*nrows] and the detect+limit pass (HO)
 void launch_averages(const AuxArgs& a, const double* q, double* qbar, cudaStream_t s);
 void launch_limit(const AuxArgs& a, double* q, const double* qbar, const double* qbar_lo, const double* qbar_hi,

@@ -55,6 +55,7 @@ int main(void) {
          offsetof(hom2d_config, limiter_eps), offsetof(hom2d_config, record_decisions),
          offsetof(hom2d_config, limiter_per_step), offsetof(hom2d_config, limiter_characteristic),
          sizeof(hom2d_dist), offsetof(hom2d_dist, cuda_stream));
+  printf("%zu\n", offsetof(hom2d_config, fv_error_recon));
   return 0;
 }
 '''
@@ -68,7 +69,8 @@ int main(void) {
     C = P.Config
     D = P.Dist
     assert vals == [ctypes.sizeof(C), C.gamma.offset, C.limiter_eps.offset, C.record_decisions.offset,
-                    C.limiter_per_step.offset, C.limiter_characteristic.offset, ctypes.sizeof(D), D.cuda_stream.offset]
+                    C.limiter_per_step.offset, C.limiter_characteristic.offset, ctypes.sizeof(D), D.cuda_stream.offset,
+                    C.fv_error_recon.offset]
 
 
 def test_product_does_not_import_oracle():
@@ -104,6 +106,7 @@ def test_missing_extension_fails_loudly(tmp_path):
     (dict(limiter_per_step=2), 1),                # variant switches are 0/1
     (dict(fv_unlimited=5), 1),
     (dict(limiter_characteristic=-1), 1),
+    (dict(fv_error_recon=2), 1),
 ])
 def test_config_validation_status(kw, status):
     """hom2d_strip_plan validates the config on the host exactly as hom2d_create

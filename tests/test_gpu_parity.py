@@ -393,6 +393,34 @@ def test_fv_rough_data_residual(orc, P, k, bc):
 
 
 @pytest.mark.parametrize("k", [1, 2])
+@pytest.mark.parametrize("bc", [0, 1])
+@pytest.mark.parametrize("nx", [64, 65, 130, 131, 257])
+def test_fv_strip_widths(orc, P, k, bc, nx):
+    """FV stage kernel across its x-strip raggedness (64-cell warp strips, 4 per
+    CTA): a full strip, odd / even ragged last strips, several CTAs, odd nx (the
+    8-B path) and even nx (the 16-B pair path); residual and per-cell decision
+    maps against the oracle on rough data, then 20 steps."""
+    import torch
+    ny = 9
+    oc, s = pair(orc, P, nx, ny, "fv", k, bc=bc, record=1)
+    from paper_1709_01619_b200.inputs import perturb
+    q = perturb(orc.init_case(oc), seed=5 + nx, amp=0.2)
+    em = np.zeros(nx * ny, dtype=np.int64)
+    cnt = np.zeros(8, dtype=np.int64)
+    r_orc = orc.residual(oc, q, counts=cnt, emap=em)
+    s.set_state(q)
+    r_gpu = s.residual(torch.from_numpy(q).cuda()).cpu().numpy()
+    assert rel_linf_res(r_gpu, r_orc) < 1e-12
+    np.testing.assert_array_equal(_unpack(s.decision_map()), _unpack(em))
+    np.testing.assert_array_equal(s.decisions()[1:5], cnt[1:5])
+    q1 = perturb(orc.init_case(oc), seed=6 + nx, amp=1e-3)
+    s.set_state(q1)
+    s.step(20)
+    q_o, _, _ = orc.run(oc, q1, 20)
+    assert rel_linf(s.get_state(), q_o) <= 1e-10
+
+
+@pytest.mark.parametrize("k", [1, 2])
 @pytest.mark.parametrize("case", [0, 1])
 @pytest.mark.parametrize("bc", [0, 1])
 def test_fv_init_case_parity(orc, P, k, case, bc):
@@ -418,3 +446,25 @@ def test_error_parity_all_norms(orc, P, method, k, var):
     t0 = 0.37
     s.set_state(q, t0)
     np.testing.assert_allclose(s.error(P.VORTEX, var), orc.error(oc, q, t0, var=var), rtol=1e-12)
+
+
+@pytest.mark.parametrize("k,unl", [(1, 0), (2, 0), (2, 1), (1, 1)])
+@pytest.mark.parametrize("var", [0, 1, 2, 3])
+@pytest.mark.parametrize("self_x", [0, 1])
+def test_fv_recon_error_parity(orc, P, monkeypatch, k, unl, var, self_x):
+    """f4 (reading R22): hom2d_error with fv_error_recon -- the FV solution
+    reconstructed from the scheme's MUSCL face states, compared with the exact
+    vortex at the 3x3 Gauss points of every cell -- GPU vs oracle, all norms and
+    variables, limited and unlimited; self_x = 1 reads the y-neighbour rows through
+    the strip ghost buffers (HOM2D_SELF_EXCHANGE)."""
+    if self_x:
+        monkeypatch.setenv("HOM2D_SELF_EXCHANGE", "1")
+    nx, ny = 41, 30
+    oc = orc.config(nx=nx, ny=ny, method="fv", k=k, cfl=0.37, fv_unlimited=unl, fv_error_recon=1)
+    s = P.Solver(P.make_config(nx, ny, method="fv", k=k, cfl=0.37, fv_unlimited=unl, fv_error_recon=1))
+    from paper_1709_01619_b200.inputs import perturb
+    q = perturb(orc.init_case(oc), seed=17 + var, amp=1e-2)
+    t0 = 0.61
+    s.set_state(q, t0)
+    np.testing.assert_allclose(s.error(P.VORTEX, var), orc.error(oc, q, t0, var=var), rtol=1e-12)
+    s.close()
