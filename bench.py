@@ -126,23 +126,39 @@ class ClockSampler:
 
 
 def cpu_info():
+    """lscpu model and core counts of the host, and the CPUs this process may use."""
+    info = {"model": "unknown"}
     try:
         out = subprocess.run(["lscpu"], capture_output=True, text=True).stdout
+        keys = {"Model name:": "model", "Socket(s):": "sockets", "Core(s) per socket:": "cores_per_socket",
+                "Thread(s) per core:": "threads_per_core", "CPU(s):": "cpus"}
         for line in out.splitlines():
-            if line.startswith("Model name:"):
-                return line.split(":", 1)[1].strip()
+            for k, name in keys.items():
+                if line.startswith(k):
+                    v = line.split(":", 1)[1].strip()
+                    info[name] = int(v) if v.isdigit() else v
     except Exception:
         pass
-    return "unknown"
+    info["usable_cpus"] = usable_cpus()
+    return info
+
+
+def usable_cpus():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
 
 
 DATA = {"vortex": "synthetic (closed-form isentropic vortex, P:897-913)",
         "shock": "synthetic (radial shock tube, P:1043-1047, scaled up; limiter on)"}
 
 
-def oracle_rate(method, k, nx, ny, cfl, steps, case="vortex"):
-    """The CPU oracle as it stands (single thread), DOF-stage/s on a sample grid."""
+def oracle_rate(method, k, nx, ny, cfl, steps, case="vortex", threads=1):
+    """The CPU oracle as it stands, DOF-stage/s on a sample grid, on `threads`
+    host threads (OpenMP over elements; bitwise the single-thread result)."""
     import oracle
+    oracle.set_threads(threads)
     if case == "shock":
         cfg = oracle.config(nx=nx, ny=ny, method=method, k=k, cfl=cfl, bc=oracle.TRANSMISSIVE,
                             box=(-1.0, 1.0, -1.0, 1.0), limiter=1)
@@ -153,6 +169,7 @@ def oracle_rate(method, k, nx, ny, cfl, steps, case="vortex"):
     t0 = time.perf_counter()
     oracle.run(cfg, q, steps)
     dt = time.perf_counter() - t0
+    oracle.set_threads(1)
     ndof = nx * ny * (1 if method == "fv" else (k + 1) ** 2)
     return ndof * 3 * steps / dt, dt
 
@@ -164,6 +181,8 @@ def reference_arm(args, wl):
         return
     import oracle
     method, k, nx, ny, cfl, weak, case = workload(wl)
+    nth = usable_cpus()
+    oracle.set_threads(nth)
     sn = 256 if method != "fv" else 1024
     if case == "shock":
         cfg = oracle.config(nx=sn, ny=sn, method=method, k=k, cfl=cfl, bc=oracle.TRANSMISSIVE,
@@ -178,15 +197,17 @@ def reference_arm(args, wl):
     for _ in range(args.steps):
         q, _, _ = oracle.run(cfg, q, 1)
     el = time.perf_counter() - t0
+    oracle.set_threads(1)
     ndof = sn * sn * (1 if method == "fv" else (k + 1) ** 2)
     v = ndof * 3 * args.steps / el
-    sample = f"{method.upper()} P{k} {case} {sn}x{sn} (sample of {nx}x{ny}), 1 SSP-RK3 step per bench step"
+    sample = (f"{method.upper()} P{k} {case} {sn}x{sn} (sample of {nx}x{ny}), 1 SSP-RK3 step per bench step, "
+              f"{nth} OpenMP threads")
     line = {"impl": "reference", "metric": "fp64 DOF-stage updates/s", "value": v, "unit": "DOF-stage/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
             "higher_is_better": True, "scaling": "weak" if weak else "strong", "vs_baseline": None, "dtype": "f64",
             "data": DATA[case],
             "config": {"workload": f"{wl} (oracle sample {sn}x{sn})", "method": method, "k": k, "nx": sn, "ny": sn},
-            "cpu_baseline": {"value": v, "unit": "DOF-stage/s", "cores": 1, "kind": "oracle", "sample": sample,
+            "cpu_baseline": {"value": v, "unit": "DOF-stage/s", "cores": nth, "kind": "oracle", "sample": sample,
                              "cpu": cpu_info()},
             "e2e": {"value": v, "unit": "DOF-stage/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -365,7 +386,7 @@ def main():
     tr = traffic_from_profiles(wl)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": tr, "peak_source": peak_src, "kernel": (f"gll_stage_kernel<{method},{k}>" if method in ("cpr", "ndg") else
-                           f"fv_stage_kernel<{k}>" if method == "fv" else f"ho_stage_kernel<{method},{k}>"),
+                           f"fv_warp_kernel<{k}>" if method == "fv" else f"gl_stage_kernel<{method},{k}>"),
                 "stage_avg_ms": stage_avg_ms, "bytes_per_launch": ndof_local * BYTES_PER_DOF_STEP / 3.0,
                 "stage_share_of_step": 3 * stage_avg_ms / (ms / args.steps)}
 
@@ -375,10 +396,17 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        sn = 768 if method != "fv" else 3072   # ~15 s of single-core oracle work
-        v, el = oracle_rate(method, k, sn, sn, cfl, 6, case)
-        cpu = {"value": v, "unit": "DOF-stage/s", "cores": 1, "kind": "oracle",
-               "sample": f"{method.upper()} P{k} {case} {sn}x{sn} elements, 6 SSP-RK3 steps ({el:.1f} s)",
+        # the oracle on all usable host threads (the reported value) and
+        # on one thread (definitional), same sample; ~10-20 s of CPU work in total
+        nth = usable_cpus()
+        sn = 768 if method != "fv" else 3072
+        v, el = oracle_rate(method, k, sn, sn, cfl, 6, case, threads=nth)
+        sn1 = 384 if method != "fv" else 1536
+        v1, el1 = oracle_rate(method, k, sn1, sn1, cfl, 4, case, threads=1)
+        cpu = {"value": v, "unit": "DOF-stage/s", "cores": nth, "kind": "oracle",
+               "sample": f"{method.upper()} P{k} {case} {sn}x{sn} elements, 6 SSP-RK3 steps on {nth} OpenMP "
+                         f"threads ({el:.1f} s)",
+               "single_thread": {"value": v1, "sample": f"{sn1}x{sn1} elements, 4 steps ({el1:.1f} s)"},
                "cpu": cpu_info()}
 
     if rank == 0:

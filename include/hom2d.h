@@ -90,6 +90,10 @@ typedef struct {
                                  cell the quadratic through the scheme's MUSCL face states with the cell
                                  mean, per direction, summed, against the exact solution at the 3x3
                                  Gauss-Legendre points; 0 = cell value vs exact cell average */
+  int32_t dg_overintegrate;   /* DG: 1 = the volume and surface integrals of the weak form (Eq. (19),
+                                 P:240-254) by (k+2)-point Gauss-Legendre over-integration (SPEC's
+                                 alternative; DESIGN f3) instead of the n-point collocation of Eq. (20)
+                                 (the default); a separate, slower stage kernel */
 } hom2d_config;
 
 typedef struct {

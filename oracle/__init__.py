@@ -46,7 +46,7 @@ def build(force: bool = False) -> str:
     """Compile liboracle_hom2d.so (plain C, fp64, no FMA contraction)."""
     if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(SRC):
         subprocess.check_call(
-            ["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-std=c99", "-fPIC", "-shared",
+            ["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-std=c99", "-fopenmp", "-fPIC", "-shared",
              "-o", LIB, SRC, "-lm"])
     return LIB
 
@@ -99,6 +99,9 @@ def lib():
         L.orc_error.argtypes = [cfgp, vp, C.c_int, d, C.c_int, P(d), P(d), P(d)]
         L.orc_fv_recon_points.argtypes = [cfgp, vp, C.c_int, vp]
         L.orc_residual_dg_quad.argtypes = [cfgp, C.c_int, vp, vp]
+        L.orc_set_threads.argtypes = [C.c_int]
+        L.orc_get_threads.restype = C.c_int
+        L.orc_set_threads(1)  # definitional single thread unless asked (bench's nproc leg)
         _lib = L
     return _lib
 
@@ -304,6 +307,15 @@ def fv_recon_points(cfg, q, var=0):
     out = np.zeros(cfg.nx * cfg.ny * 9)
     _chk(lib().orc_fv_recon_points(C.byref(cfg), _p(_v4(q)), var, _p(out)))
     return out.reshape(cfg.nx * cfg.ny, 3, 3)
+
+
+def set_threads(n: int):
+    """OpenMP threads of the oracle (timing only; results are bitwise those of 1)."""
+    lib().orc_set_threads(int(n))
+
+
+def get_threads() -> int:
+    return int(lib().orc_get_threads())
 
 
 def residual_dg_quad(cfg, q, nq):

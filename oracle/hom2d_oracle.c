@@ -10,7 +10,10 @@
  * textbook definitions (Newton iteration in long double).
  *
  * Arithmetic: fp64 throughout (the paper: "Double precision is used for all
- * computations"), compiled with -O2 -ffp-contract=off, single thread.
+ * computations"), compiled with -O2 -ffp-contract=off; one thread unless
+ * orc_set_threads asks for more (OpenMP over independent elements / faces /
+ * values, bitwise the single-thread result: a timing option for bench.py's
+ * cpu_baseline, never a different arithmetic).
  *
  * Layout (ABI choice): Q[c*(Ne*np) + m*np + p], c in {rho, rho u,
  * rho v, e} (SoA), element m = j*nx + i (row-major), point p = b*n + a
@@ -27,6 +30,9 @@
  */
 #include <math.h>
 #include <stdint.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 #include <stdlib.h>
 #include <string.h>
 
@@ -73,6 +79,24 @@ enum { DEC_MARKED = 0, DEC_MM_ZERO = 1, DEC_MM_FIRST = 2, DEC_MM_SECOND = 3, DEC
 #define DEC_TIE 1e-12
 
 #define MAXN 9   /* up to 8-point rules (error quadrature) */
+
+/* Threads (timing only: OpenMP over element rows / faces / values; every value is
+ * computed by exactly the same operations whatever the thread count, so results
+ * are bitwise those of one thread -- tests/test_oracle_threads.py).  Default 1. */
+void orc_set_threads(int n) {
+#ifdef _OPENMP
+  omp_set_num_threads(n < 1 ? 1 : n);
+#else
+  (void)n;
+#endif
+}
+int orc_get_threads(void) {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}
 
 /* ------------------------------------------------------------------------- */
 /* Legendre polynomials, Gauss / Gauss-Lobatto points (Fig. 1) */
@@ -462,6 +486,7 @@ static void residual_cpr_ndg(const orc_config *cf, const ops_t *o, const double 
   double dx = (cf->xmax - cf->xmin) / cf->nx, dy = (cf->ymax - cf->ymin) / cf->ny;
   int chain = (cf->method == ORC_CPR) && cf->cpr_chain_rule;
   double FW[MAXN][4], FE[MAXN][4], FS[MAXN][4], FN[MAXN][4];
+#pragma omp parallel for private(FW, FE, FS, FN) schedule(static)
   for (int j = 0; j < cf->ny; ++j)
     for (int i = 0; i < cf->nx; ++i) {
       int64_t m = (int64_t)j * cf->nx + i;
@@ -525,6 +550,7 @@ static void residual_dg(const orc_config *cf, const ops_t *o, const double *Q, d
   int64_t N = (int64_t)cf->nx * cf->ny * np;
   double dx = (cf->xmax - cf->xmin) / cf->nx, dy = (cf->ymax - cf->ymin) / cf->ny;
   double FW[MAXN][4], FE[MAXN][4], FS[MAXN][4], FN[MAXN][4];
+#pragma omp parallel for private(FW, FE, FS, FN) schedule(static)
   for (int j = 0; j < cf->ny; ++j)
     for (int i = 0; i < cf->nx; ++i) {
       int64_t m = (int64_t)j * cf->nx + i;
@@ -582,6 +608,7 @@ static void residual_dg_quad(const orc_config *cf, const ops_t *o, int nq, const
       for (int a = 0; a < n; ++a) acc += (ex)[a] * (ey)[b] * Q[c * N + (m_) * np + b * n + a]; \
     (out)[c] = acc;                                                                     \
   }
+#pragma omp parallel for schedule(static)
   for (int j = 0; j < cf->ny; ++j)
     for (int i = 0; i < cf->nx; ++i) {
       int64_t m = (int64_t)j * cf->nx + i;
@@ -668,6 +695,7 @@ static void residual_sd(const orc_config *cf, const ops_t *o, const double *Q, d
   int64_t N = (int64_t)cf->nx * cf->ny * np;
   double dx = (cf->xmax - cf->xmin) / cf->nx, dy = (cf->ymax - cf->ymin) / cf->ny;
   double phi[2][MAXN][MAXN][4];   /* [dir][line][flux point][c] */
+#pragma omp parallel for private(phi) schedule(static)
   for (int j = 0; j < cf->ny; ++j)
     for (int i = 0; i < cf->nx; ++i) {
       int64_t m = (int64_t)j * cf->nx + i;
@@ -763,6 +791,7 @@ static void residual_fv(const orc_config *cf, const double *Q, double *R, int64_
   /* face fluxes stored separately, then differenced (the paper's 2 kernels) */
   double *Fx = (double *)malloc(sizeof(double) * 4 * (size_t)(nx + 1) * ny);
   double *Gy = (double *)malloc(sizeof(double) * 4 * (size_t)nx * (ny + 1));
+#pragma omp parallel for if (!cnt && !emap) schedule(static)
   for (int j = 0; j < ny; ++j)
     for (int f = 0; f <= nx; ++f) {   /* face f between cells f-1 and f */
       double s[4][4], qW[4], qE[4], F[4];
@@ -773,6 +802,7 @@ static void residual_fv(const orc_config *cf, const double *Q, double *R, int64_
       rusanov(&P, 0, qW, qE, F);
       for (int c = 0; c < 4; ++c) Fx[((size_t)j * (nx + 1) + f) * 4 + c] = F[c];
     }
+#pragma omp parallel for if (!cnt && !emap) schedule(static)
   for (int f = 0; f <= ny; ++f)
     for (int i = 0; i < nx; ++i) {
       double s[4][4], qW[4], qE[4], F[4];
@@ -783,6 +813,7 @@ static void residual_fv(const orc_config *cf, const double *Q, double *R, int64_
       rusanov(&P, 1, qW, qE, F);
       for (int c = 0; c < 4; ++c) Gy[((size_t)f * nx + i) * 4 + c] = F[c];
     }
+#pragma omp parallel for schedule(static)
   for (int j = 0; j < ny; ++j)
     for (int i = 0; i < nx; ++i)
       for (int c = 0; c < 4; ++c)
@@ -974,12 +1005,15 @@ static void ssprk3_post(double *q, int64_t n, double dt, orc_rhs_fn rhs, orc_pos
   double *r = (double *)malloc(sizeof(double) * n);
   memcpy(q0, q, sizeof(double) * n);
   rhs(q, r, ctx);
+#pragma omp parallel for schedule(static)
   for (int64_t i = 0; i < n; ++i) q[i] = q0[i] + dt * r[i];                          /* q1 */
   if (post) post(q, ctx);
   rhs(q, r, ctx);
+#pragma omp parallel for schedule(static)
   for (int64_t i = 0; i < n; ++i) q[i] = 0.75 * q0[i] + 0.25 * (q[i] + dt * r[i]);   /* q2 */
   if (post) post(q, ctx);
   rhs(q, r, ctx);
+#pragma omp parallel for schedule(static)
   for (int64_t i = 0; i < n; ++i) q[i] = q0[i] / 3.0 + (2.0 / 3.0) * (q[i] + dt * r[i]); /* q^{n+1} */
   if (post_last) post_last(q, ctx);
   free(q0);

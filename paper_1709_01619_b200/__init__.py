@@ -51,7 +51,7 @@ class Config(C.Structure):
         ("limiter", C.c_int32), ("limiter_eps", C.c_double),
         ("cpr_chain_rule", C.c_int32), ("record_decisions", C.c_int32),
         ("limiter_per_step", C.c_int32), ("limiter_all_vars", C.c_int32), ("fv_unlimited", C.c_int32),
-        ("limiter_characteristic", C.c_int32), ("fv_error_recon", C.c_int32),
+        ("limiter_characteristic", C.c_int32), ("fv_error_recon", C.c_int32), ("dg_overintegrate", C.c_int32),
     ]
 
 
@@ -113,11 +113,12 @@ def load(path: str = LIB_PATH):
 
 def make_config(nx, ny, method="cpr", k=1, bc=PERIODIC, box=(-5.0, 5.0, -5.0, 5.0), gamma=1.4, cfl=0.24,
                 limiter=0, limiter_eps=1e-3, cpr_chain_rule=1, record_decisions=0, limiter_per_step=0,
-                limiter_all_vars=0, fv_unlimited=0, limiter_characteristic=0, fv_error_recon=0) -> Config:
+                limiter_all_vars=0, fv_unlimited=0, limiter_characteristic=0, fv_error_recon=0,
+                dg_overintegrate=0) -> Config:
     m = METHODS[method] if isinstance(method, str) else int(method)
     return Config(nx, ny, box[0], box[1], box[2], box[3], bc, m, k, gamma, cfl, limiter, limiter_eps,
                   cpr_chain_rule, record_decisions, limiter_per_step, limiter_all_vars, fv_unlimited,
-                  limiter_characteristic, fv_error_recon)
+                  limiter_characteristic, fv_error_recon, dg_overintegrate)
 
 
 def strip_plan(cfg: Config, rank: int, nranks: int) -> StripPlan:

@@ -302,20 +302,21 @@ __global__ void __launch_bounds__(FTX, H2D_FV_MINB) fv_stage_kernel(const StageA
 }
 
 // ---------------------------------------------------------------------------
-// Warp-strip variant: every warp marches its own strip of WS = 64 cells (two
-// adjacent cells per lane) up the rows, with its own cp.async ring and no CTA
-// barrier in the march:
-//  * the ring slots are compile-time (the march is unrolled by the ring size),
-//    so shared-memory addresses are constants off one base;
-//  * a lane reconstructs its two cells in x (one 16-B read of its pair + the
-//    two neighbour values), the face between them is lane-local, the W face of
-//    its first cell takes the left lane's hi state by a shuffle, and the E face
-//    of its second cell is the right lane's W-face flux by a shuffle; the
-//    strip's two end faces are computed by lanes 0 / last (divergent, 1 of 32);
+// Warp-strip kernel (the default): every warp marches its own strip of WS = 62
+// cells up the rows -- two adjacent cells per lane, lane 31 on the right halo --
+// with its own cp.async rings (stage input with a 2-cell halo each side, q^n)
+// and no CTA barrier in the march:
+//  * a lane reconstructs its two cells in x from one 16-B read of its pair and
+//    its neighbours (and the hi state of the cell on its left, recomputed, not
+//    shuffled); the face between its cells is lane-local, the E face of its
+//    second cell is the right lane's W-face flux by a shuffle -- every x face is
+//    evaluated once and no lane runs a face alone;
 //  * y faces as in the CTA kernel: the N face of each column is carried to the
-//    next row as its S face.
-// Arithmetic per face / cell is the CTA kernel's (same helpers, same order),
-// so results are bitwise those of fv_stage_kernel.
+//    next row as its S face;
+//  * q^n arrives through its own ring one row ahead (no global load latency in
+//    the epilogue); the march length is chosen so the grid is a whole number of
+//    waves.
+// Arithmetic per face / cell is the CTA kernel's (same helpers, same order).
 #ifndef H2D_FVW_DEPTH
 #define H2D_FVW_DEPTH 1
 #endif
@@ -324,12 +325,16 @@ __global__ void __launch_bounds__(FTX, H2D_FV_MINB) fv_stage_kernel(const StageA
 #endif
 namespace {
 constexpr int WPC = 4;                     // warps per CTA (independent strips)
-constexpr int WS = 64, WW = WS + 4;        // cells per warp strip; ring row width (2 halo cells each side)
+// a warp strip is WS = 62 cells: lanes 0..30 own two cells each, lane 31 (and, in a
+// ragged strip, every lane past the last cell) works on the halo cells to the
+// right, so the strip's E face comes to the last owning lane by the same shuffle
+// as every other E face -- no divergent face evaluation; WL = 64 pair slots
+constexpr int WS = 62, WL = 64, WW = WL + 4;  // cells per warp strip; ring row width (2 halo cells each side)
 constexpr int WD = H2D_FVW_DEPTH, WNS = 3 + WD;  // rows in flight; ring rows
 constexpr int QS = WD + 1;                       // q^n ring rows (row x lands with ring row x+2, read at step x)
 // dynamic shared memory: per warp WNS ring rows x 4 components x WW, then (stages
 // with q^n) QS q-ring rows x 4 x WS, then the block-max scratch
-constexpr int WRING = WNS * 4 * WW, WQ = QS * 4 * WS;
+constexpr int WRING = WNS * 4 * WW, WQ = QS * 4 * WL;
 constexpr size_t fvw_smem(bool hq0) { return sizeof(double) * ((size_t)WPC * (WRING + (hq0 ? WQ : 0)) + WPC); }
 }  // namespace
 
@@ -338,7 +343,7 @@ __global__ void __launch_bounds__(WPC * 32, H2D_FVW_MINB) fv_warp_kernel(const S
   const bool HQ0 = V == 8 ? a.q0 != nullptr : (V & 1), HLAM = V == 8 ? (a.lam || a.bad) : (V & 2) != 0;
   extern __shared__ __align__(16) double fv_smem[];
   double(*const ring)[WNS][4][WW] = reinterpret_cast<double(*)[WNS][4][WW]>(fv_smem);
-  double(*const qring)[QS][4][WS] = reinterpret_cast<double(*)[QS][4][WS]>(fv_smem + WPC * WRING);
+  double(*const qring)[QS][4][WL] = reinterpret_cast<double(*)[QS][4][WL]>(fv_smem + WPC * WRING);
   double* const sred = fv_smem + WPC * WRING + (HQ0 ? WPC * WQ : 0);
   pdl_wait();
   pdl_launch();
@@ -355,11 +360,9 @@ __global__ void __launch_bounds__(WPC * 32, H2D_FVW_MINB) fv_warp_kernel(const S
     const int TXv = min(WS, a.nx - i0), RBv = min(a.rows, a.row_hi - jb);
     const int c0 = 2 * lane;                         // local index of the lane's first cell
     const bool own0 = c0 < TXv, own1 = c0 + 1 < TXv;
-    const int last = (TXv - 1) >> 1;                 // lane holding the strip's last cell
-    const bool evenT = (TXv & 1) == 0;               // last lane's second cell is real (else: the halo cell)
     long long* const dec = REC ? a.dec : nullptr;
     double(*const rw)[4][WW] = ring[wid];
-    double(*const qw)[4][WS] = qring[HQ0 ? wid : 0];
+    double(*const qw)[4][WL] = qring[HQ0 ? wid : 0];
     // halo column of lanes 0..3: slots 0, 1 = cells i0-2, i0-1; TXv+2, TXv+3 = cells i0+TXv, +1
     int hx = lane < 2 ? i0 - 2 + lane : i0 + TXv + (lane - 2);
     if (a.bcx == 0) hx = hx < 0 ? hx + a.nx : (hx >= a.nx ? hx - a.nx : hx);
@@ -413,7 +416,7 @@ __global__ void __launch_bounds__(WPC * 32, H2D_FVW_MINB) fv_warp_kernel(const S
       }
     };
     auto issue_q0 = [&](int jr, int slot) {  // q^n row jr (an own row) into q-ring slot
-      copy_pair(&qw[slot][0][c0], WS, a.q0 + (long long)jr * a.nx + i0 + c0, a.cs);
+      copy_pair(&qw[slot][0][c0], WL, a.q0 + (long long)jr * a.nx + i0 + c0, a.cs);
     };
     auto commit = [] { asm volatile("cp.async.commit_group;" ::: "memory"); };
 
@@ -465,54 +468,41 @@ __global__ void __launch_bounds__(WPC * 32, H2D_FVW_MINB) fv_warp_kernel(const S
       commit();
       const int jr = jb + r;
       const long long gidx = (long long)jr * a.nx + (i0 + c0);
-      // x: the pair, its neighbours, the face states of both cells; then the W
-      // face of the first cell, the face between them and (by shuffle) the E
-      // face of the second, reduced at once to the x flux differences Rx
+      // x: the pair, its neighbours, the face states of both cells and the hi
+      // state of the cell left of the pair (recomputed, no shuffle); then the W
+      // face of the first cell, the face between them and (by shuffle: the right
+      // lane's W face) the E face of the second, reduced at once to the x flux
+      // differences Rx.  A lane's cell past the strip's last cell is the halo
+      // cell i0+TXv (first fake cell; its lo state gives the strip's E face) or
+      // beyond (unused values)
       double xq[2][4], Rx[2][4];
       {
-        double lo[2][4], hi[2][4];
+        double lo[2][4], hi[2][4], hL[4];
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           const double2 p = *reinterpret_cast<const double2*>(&rw[S0][c][c0 + 2]);
-          const double xm = rw[S0][c][c0 + 1], xp = rw[S0][c][c0 + 4];
+          const double2 m2 = *reinterpret_cast<const double2*>(&rw[S0][c][c0]);
+          const double xp = rw[S0][c][c0 + 4];
           xq[0][c] = p.x;
           xq[1][c] = p.y;
-          cell_faces<ORDER>(xm, p.x, p.y, lo[0][c], hi[0][c], own0 ? dec : nullptr, 2,
-                            own0 ? dmap_at(jr, i0 + c0) : nullptr);
-          // second cell: own, or (last lane, odd TXv) the halo cell i0+TXv
-          const bool h1 = !own1 && lane == last;
-          const int w1 = own1 ? 2 : (h1 && i0 + TXv == a.nx ? 1 : 0);
-          cell_faces<ORDER>(p.x, p.y, xp, lo[1][c], hi[1][c], (own1 || h1) ? dec : nullptr, w1,
+          double dm;
+          // left cell: counted by its owner (the left lane), here only the domain's
+          // W ghost of the first lane (P:346-351 face form: the bottom/left ghost face)
+          cell_faces<ORDER>(m2.x, m2.y, p.x, dm, hL[c], lane == 0 ? dec : nullptr, i0 == 0 ? 1 : 0,
+                            lane == 0 ? dmap_at(jr, i0 - 1) : nullptr);
+          const bool h0 = !own0 && c0 == TXv, h1 = !own1 && c0 + 1 == TXv;  // the halo cell i0+TXv
+          const int wh = i0 + TXv == a.nx ? 1 : 0;
+          cell_faces<ORDER>(m2.y, p.x, p.y, lo[0][c], hi[0][c], (own0 || h0) ? dec : nullptr, own0 ? 2 : wh,
+                            (own0 || h0) ? dmap_at(jr, i0 + c0) : nullptr);
+          cell_faces<ORDER>(p.x, p.y, xp, lo[1][c], hi[1][c], (own1 || h1) ? dec : nullptr, own1 ? 2 : wh,
                             (own1 || h1) ? dmap_at(jr, i0 + c0 + 1) : nullptr);
         }
         double FW[4], FM[4], FE[4];
-        {
-          // hi state of the cell left of the pair: the left lane's, or (lane 0) cell i0-1
-          double hL[4];
-#pragma unroll
-          for (int c = 0; c < 4; ++c) hL[c] = __shfl_up_sync(0xffffffffu, hi[1][c], 1);
-          if (lane == 0) {
-            double dm;
-#pragma unroll
-            for (int c = 0; c < 4; ++c)
-              cell_faces<ORDER>(rw[S0][c][0], rw[S0][c][1], rw[S0][c][2], dm, hL[c], dec, i0 == 0 ? 1 : 0,
-                                dmap_at(jr, i0 - 1));
-          }
-          rusanov2<0>(hL, lo[0], gm1, gam, FW);
-        }
+        rusanov2<0>(hL, lo[0], gm1, gam, FW);
         rusanov2<0>(hi[0], lo[1], gm1, gam, FM);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) FE[c] = __shfl_down_sync(0xffffffffu, FW[c], 1);
-        if (lane == last && evenT) {  // the strip's last E face: hi of the last cell, lo of cell i0+TXv
-          double lh[4], dm;
-#pragma unroll
-          for (int c = 0; c < 4; ++c)
-            cell_faces<ORDER>(rw[S0][c][TXv + 1], rw[S0][c][TXv + 2], rw[S0][c][TXv + 3], lh[c], dm, dec,
-                              (i0 + TXv == a.nx) ? 1 : 0, dmap_at(jr, i0 + TXv));
-          rusanov2<0>(hi[1], lh, gm1, gam, FE);
-        }
-#pragma unroll
         for (int c = 0; c < 4; ++c) {
+          FE[c] = __shfl_down_sync(0xffffffffu, FW[c], 1);
           Rx[0][c] = -(FM[c] - FW[c]) * hrdx;  // fluxes are 2 F
           Rx[1][c] = -(FE[c] - FM[c]) * hrdx;
         }
@@ -520,14 +510,21 @@ __global__ void __launch_bounds__(WPC * 32, H2D_FVW_MINB) fv_warp_kernel(const S
       // y, per column: the lo / hi states of row r+1 (rows r .. r+2), the N face,
       // the residual, the RK combination and the store
       const int wn = (r + 1 < RBv) ? 2 : ((jb + RBv == a.nrows) ? 1 : 0);
-      double o[2][4];
+      double o[2][4], y1[2][4], y2[2][4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const double2 p1 = *reinterpret_cast<const double2*>(&rw[S1][c][c0 + 2]);
+        const double2 p2 = *reinterpret_cast<const double2*>(&rw[S2][c][c0 + 2]);
+        y1[0][c] = p1.x; y1[1][c] = p1.y;
+        y2[0][c] = p2.x; y2[1][c] = p2.y;
+      }
 #pragma unroll
       for (int k = 0; k < 2; ++k) {
         const bool ok = k ? own1 : own0;
         double ylo[4], yhn[4], GN[4];
 #pragma unroll
         for (int c = 0; c < 4; ++c)
-          cell_faces<ORDER>(xq[k][c], rw[S1][c][c0 + 2 + k], rw[S2][c][c0 + 2 + k], ylo[c], yhn[c],
+          cell_faces<ORDER>(xq[k][c], y1[k][c], y2[k][c], ylo[c], yhn[c],
                             ok ? dec : nullptr, wn, ok ? dmap_at(jr + 1, i0 + c0 + k) : nullptr);
         rusanov2<1>(yHi[k], ylo, gm1, gam, GN);
 #pragma unroll

@@ -22,6 +22,7 @@ struct hom2d {
   cudaStream_t stream = nullptr;
   cudaStream_t xstream = nullptr;          // nranks > 1: halo exchange stream (highest priority)
   bool self_x = false;                     // HOM2D_SELF_EXCHANGE test mode (see self_exchange_env)
+  bool self_nccl = false;                  // HOM2D_SELF_EXCHANGE=2: the same through a 1-rank NCCL communicator
   cudaEvent_t ev_in = nullptr, ev_halo = nullptr;
   // CUDA graphs of 2^i steps (single GPU, untimed): launch-bound small grids
   cudaStream_t gstream = nullptr;
@@ -89,13 +90,16 @@ hom2d_status fail(hom2d* h, hom2d_status st, const char* fmt, ...) {
 
 int points_per_elem(const hom2d_config& c) { return c.method == HOM2D_FV ? 1 : (c.k + 1) * (c.k + 1); }
 
-// Test mode (HOM2D_SELF_EXCHANGE=1, one rank, periodic): the overlapped multi-GPU
-// stage path -- exchange stream, events, interior / boundary launches, ghost
-// buffers -- with the NCCL send/recv replaced by device copies of the strip's own
-// wrap rows, so the stream plumbing is exercised (bitwise) on one GPU.
-bool self_exchange_env(const hom2d_config& c, int nranks) {
+// Test modes (one rank, periodic): the overlapped multi-GPU stage path --
+// exchange stream, events, interior / boundary launches, ghost buffers -- on one
+// GPU, bitwise against the plain path.  HOM2D_SELF_EXCHANGE=1: the NCCL send/recv
+// replaced by device copies of the strip's own wrap rows; =2: the real NCCL data
+// plane on a 1-rank communicator (ncclCommInitRank, the grouped ncclSend/ncclRecv
+// of exchange() with rank 0 as both strip neighbours, every ncclAllReduce).
+int self_exchange_env(const hom2d_config& c, int nranks) {
   const char* v = getenv("HOM2D_SELF_EXCHANGE");
-  return nranks == 1 && c.bc == HOM2D_PERIODIC && v && v[0] == '1';
+  if (nranks != 1 || c.bc != HOM2D_PERIODIC || !v) return 0;
+  return v[0] == '1' ? 1 : v[0] == '2' ? 2 : 0;
 }
 
 hom2d_status check_cfg(const hom2d_config* c, int nranks) {
@@ -108,7 +112,8 @@ hom2d_status check_cfg(const hom2d_config* c, int nranks) {
   if (c->ny / nranks < G) return HOM2D_ERR_MESH;
   if (!(c->gamma > 1.0) || !(c->cfl > 0.0)) return HOM2D_ERR_ARG;
   if ((unsigned)c->limiter_per_step > 1u || (unsigned)c->limiter_all_vars > 1u || (unsigned)c->fv_unlimited > 1u ||
-      (unsigned)c->limiter_characteristic > 1u || (unsigned)c->fv_error_recon > 1u)
+      (unsigned)c->limiter_characteristic > 1u || (unsigned)c->fv_error_recon > 1u ||
+      (unsigned)c->dg_overintegrate > 1u)
     return HOM2D_ERR_ARG;
   return HOM2D_OK;
 }
@@ -196,7 +201,7 @@ hom2d_status exchange(hom2d* h, const double* X, long long comp_stride, long lon
     *hi = h->ovr_hi;
     return HOM2D_OK;
   }
-  if (R == 1 && h->self_x) {  // test mode: the periodic wrap rows through the ghost buffers, on xs
+  if (R == 1 && h->self_x && !h->comm) {  // test mode: the periodic wrap rows through the ghost buffers, on xs
     const long long cnt = (long long)G * row_vals;
     for (int c = 0; c < 4; ++c) {
       CU(h, cudaMemcpyAsync(rlo + c * cnt, X + c * comp_stride + (long long)(h->nrows - G) * row_vals,
@@ -208,7 +213,7 @@ hom2d_status exchange(hom2d* h, const double* X, long long comp_stride, long lon
     *hi = rhi;
     return HOM2D_OK;
   }
-  if (R == 1) {
+  if (R == 1 && !h->comm) {
     *gcs = comp_stride;
     *lo = (h->cfg.bc == HOM2D_PERIODIC) ? X + (long long)(h->nrows - G) * row_vals : nullptr;
     *hi = (h->cfg.bc == HOM2D_PERIODIC) ? X : nullptr;
@@ -237,6 +242,7 @@ hom2d_status exchange(hom2d* h, const double* X, long long comp_stride, long lon
 int launch_stage(hom2d* h, const StageArgs& s) {
   if (h->cfg.method == HOM2D_FV) return launch_fv_stage(h->cfg.k, s, h->stream);
   int method = h->cfg.method;
+  if (method == HOM2D_DG && h->cfg.dg_overintegrate) return launch_dgoi_stage(h->cfg.k, s, h->stream);
   if (method == HOM2D_CPR && !h->cfg.cpr_chain_rule) method = HOM2D_NDG;  // flux-differentiation CPR == NDG
   return (method == HOM2D_CPR || method == HOM2D_NDG) ? launch_gll_stage(method, h->cfg.k, s, h->stream)
                                                       : launch_gl_stage(method, h->cfg.k, s, h->stream);
@@ -324,7 +330,7 @@ hom2d_status run_limiter(hom2d* h, double* X, const double* dt = nullptr, bool a
 }
 
 hom2d_status allreduce_max_lam(hom2d* h) {
-  if (h->nranks > 1 && h->comm) NC(h, ncclAllReduce(h->lam, h->lam, 1, ncclUint64, ncclMax, h->comm, h->stream));
+  if (h->comm) NC(h, ncclAllReduce(h->lam, h->lam, 1, ncclUint64, ncclMax, h->comm, h->stream));
   return HOM2D_OK;
 }
 
@@ -412,12 +418,14 @@ hom2d_status hom2d_create(const hom2d_config* cfg, const hom2d_dist* dist, void*
   if (ce != cudaSuccess) { delete h; return HOM2D_ERR_CUDA; }
   carve(h, *cfg, R, (char*)workspace);
   if (cudaMallocHost(&h->t_host, 8 * sizeof(double)) != cudaSuccess) { delete h; return HOM2D_ERR_CUDA; }
-  h->self_x = self_exchange_env(*cfg, R);
+  const int sxm = self_exchange_env(*cfg, R);
+  h->self_x = sxm != 0;
+  h->self_nccl = sxm == 2;
   if ((R > 1 && dist->nccl_id) || h->self_x) {  // (no id: strip-only handle, see hom2d_residual_strip)
-    if (R > 1) {
+    if (R > 1 || h->self_nccl) {
       ncclUniqueId id;
-      memcpy(&id, dist->nccl_id, sizeof(id));
-      if (ncclCommInitRank(&h->comm, R, id, h->rank) != ncclSuccess) {
+      if (R > 1) memcpy(&id, dist->nccl_id, sizeof(id));
+      if ((R == 1 && ncclGetUniqueId(&id) != ncclSuccess) || ncclCommInitRank(&h->comm, R, id, h->rank) != ncclSuccess) {
         cudaFreeHost(h->t_host);
         delete h;
         return HOM2D_ERR_NCCL;
@@ -654,7 +662,7 @@ extern "C" hom2d_status hom2d_step(hom2d* h, int32_t max_steps, double t_end, do
     // every rank leaves the loop in the same batch: the flag is min-reduced over
     // the ranks (bad[1]) before the host looks at it; the local point (bad[0])
     // names the element when this rank found it
-    if (h->nranks > 1 && h->comm)
+    if (h->comm)
       NC(h, ncclAllReduce(h->bad, h->bad + 1, 1, ncclUint64, ncclMin, h->comm, h->stream));
     else
       CU(h, cudaMemcpyAsync(h->bad + 1, h->bad, sizeof(unsigned long long), cudaMemcpyDeviceToDevice, h->stream));
@@ -702,7 +710,7 @@ hom2d_status hom2d_error(hom2d* h, int32_t case_id, int32_t var, double* l1, dou
   launch_error_final(h->part, nb, h->err3, h->stream);
   h->launches += 2;
   CU(h, cudaPeekAtLastError());
-  if (h->nranks > 1 && h->comm) {
+  if (h->comm) {
     NC(h, ncclAllReduce(h->err3, h->err3, 2, ncclDouble, ncclSum, h->comm, h->stream));
     NC(h, ncclAllReduce(h->err3 + 2, h->err3 + 2, 1, ncclDouble, ncclMax, h->comm, h->stream));
   }
@@ -731,7 +739,7 @@ hom2d_status hom2d_decisions(hom2d* h, int64_t* counts8) {
   if (!counts8) return HOM2D_ERR_ARG;
   CU(h, cudaMemcpyAsync(counts8, h->dec, 8 * sizeof(long long), cudaMemcpyDeviceToHost, h->stream));
   CU(h, cudaStreamSynchronize(h->stream));
-  if (h->nranks > 1 && h->comm) {  // sum over ranks through the device scratch
+  if (h->comm) {  // sum over ranks through the device scratch
     NC(h, ncclAllReduce(h->dec, h->part, 8, ncclInt64, ncclSum, h->comm, h->stream));
     CU(h, cudaMemcpyAsync(counts8, h->part, 8 * sizeof(long long), cudaMemcpyDeviceToHost, h->stream));
     CU(h, cudaStreamSynchronize(h->stream));

@@ -55,7 +55,7 @@ int main(void) {
          offsetof(hom2d_config, limiter_eps), offsetof(hom2d_config, record_decisions),
          offsetof(hom2d_config, limiter_per_step), offsetof(hom2d_config, limiter_characteristic),
          sizeof(hom2d_dist), offsetof(hom2d_dist, cuda_stream));
-  printf("%zu\n", offsetof(hom2d_config, fv_error_recon));
+  printf("%zu %zu\n", offsetof(hom2d_config, fv_error_recon), offsetof(hom2d_config, dg_overintegrate));
   return 0;
 }
 '''
@@ -70,7 +70,7 @@ int main(void) {
     D = P.Dist
     assert vals == [ctypes.sizeof(C), C.gamma.offset, C.limiter_eps.offset, C.record_decisions.offset,
                     C.limiter_per_step.offset, C.limiter_characteristic.offset, ctypes.sizeof(D), D.cuda_stream.offset,
-                    C.fv_error_recon.offset]
+                    C.fv_error_recon.offset, C.dg_overintegrate.offset]
 
 
 def test_product_does_not_import_oracle():
@@ -107,6 +107,7 @@ def test_missing_extension_fails_loudly(tmp_path):
     (dict(fv_unlimited=5), 1),
     (dict(limiter_characteristic=-1), 1),
     (dict(fv_error_recon=2), 1),
+    (dict(dg_overintegrate=3), 1),
 ])
 def test_config_validation_status(kw, status):
     """hom2d_strip_plan validates the config on the host exactly as hom2d_create

@@ -450,7 +450,7 @@ def test_error_parity_all_norms(orc, P, method, k, var):
 
 @pytest.mark.parametrize("k,unl", [(1, 0), (2, 0), (2, 1), (1, 1)])
 @pytest.mark.parametrize("var", [0, 1, 2, 3])
-@pytest.mark.parametrize("self_x", [0, 1])
+@pytest.mark.parametrize("self_x", [0, 1, 2])
 def test_fv_recon_error_parity(orc, P, monkeypatch, k, unl, var, self_x):
     """f4 (reading R22): hom2d_error with fv_error_recon -- the FV solution
     reconstructed from the scheme's MUSCL face states, compared with the exact
@@ -458,7 +458,7 @@ def test_fv_recon_error_parity(orc, P, monkeypatch, k, unl, var, self_x):
     variables, limited and unlimited; self_x = 1 reads the y-neighbour rows through
     the strip ghost buffers (HOM2D_SELF_EXCHANGE)."""
     if self_x:
-        monkeypatch.setenv("HOM2D_SELF_EXCHANGE", "1")
+        monkeypatch.setenv("HOM2D_SELF_EXCHANGE", str(self_x))
     nx, ny = 41, 30
     oc = orc.config(nx=nx, ny=ny, method="fv", k=k, cfl=0.37, fv_unlimited=unl, fv_error_recon=1)
     s = P.Solver(P.make_config(nx, ny, method="fv", k=k, cfl=0.37, fv_unlimited=unl, fv_error_recon=1))

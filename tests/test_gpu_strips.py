@@ -71,9 +71,12 @@ def test_overlapped_stage_path_bitwise(P, monkeypatch, method, k, limiter):
     while the interior rows run, the boundary bands wait on its event, and the
     limiter's average rows take the same route.  30 steps (90 stages) must equal
     the single-launch path bitwise; the exchange stream's copies racing a kernel
-    that writes its source or the ghost buffers would break this."""
+    that writes its source or the ghost buffers would break this.  =2: the same
+    through NCCL itself -- a 1-rank communicator (ncclCommInitRank), the grouped
+    ncclSend/ncclRecv of every stage with rank 0 as both neighbours, the lambda /
+    non-physical-flag ncclAllReduce of every step."""
     out = []
-    for sx in ("0", "1"):
+    for sx in ("0", "1", "2"):
         monkeypatch.setenv("HOM2D_SELF_EXCHANGE", sx)
         cfg = P.make_config(23, 14, method=method, k=k, cfl=0.05, limiter=limiter)
         s = P.Solver(cfg)
@@ -82,3 +85,25 @@ def test_overlapped_stage_path_bitwise(P, monkeypatch, method, k, limiter):
         out.append(s.get_state())
         s.close()
     np.testing.assert_array_equal(out[0], out[1])
+    np.testing.assert_array_equal(out[0], out[2])
+
+
+@pytest.mark.parametrize("method,k", [("cpr", 2), ("fv", 2)])
+def test_nccl_self_collectives(P, monkeypatch, method, k):
+    """HOM2D_SELF_EXCHANGE=2: hom2d_error's sum/max allreduces, hom2d_decisions'
+    sum allreduce and the non-physical flag's min allreduce on a 1-rank NCCL
+    communicator give the single-GPU results exactly."""
+    res = []
+    for sx in ("0", "2"):
+        monkeypatch.setenv("HOM2D_SELF_EXCHANGE", sx)
+        s = P.Solver(P.make_config(16, 12, method=method, k=k, cfl=0.05, record_decisions=1))
+        s.init_case(P.VORTEX)
+        s.step(7)
+        res.append((s.error(P.VORTEX, 0), s.error(P.VORTEX, 3), tuple(s.decisions()), s.time()))
+        q = s.get_state()
+        q[3 * (q.size // 4) + 5] = -1.0
+        s.set_state(q, s.time())
+        with pytest.raises(P.NonPhysicalState):
+            s.step(3)
+        s.close()
+    assert res[0] == res[1]

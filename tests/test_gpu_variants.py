@@ -115,3 +115,61 @@ def test_programmatic_launch_bitwise_equals_plain(orc, P, monkeypatch, method, k
     monkeypatch.setenv("HOM2D_NO_PDL", "0")
     P.Solver(P.make_config(8, 8)).close()  # leave PDL on for the tests that follow
     np.testing.assert_array_equal(out[0], out[1])
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 4])
+@pytest.mark.parametrize("bc", [0, 1])
+def test_dg_overintegration_residual(orc, P, k, bc):
+    """f3: DG with (k+2)-point over-integration of Eq. (19) (dgoi_stage.cu) against
+    the oracle's residual_dg_quad on seeded data, ragged grid."""
+    import torch
+    from paper_1709_01619_b200.inputs import perturb
+    oc, s = pair(orc, P, 19, 13, "dg", k, 0.08, bc=bc, dg_overintegrate=1)
+    q = perturb(orc.init_case(oc), seed=41 + k, amp=1e-2)
+    r_gpu = s.residual(torch.from_numpy(q).cuda()).cpu().numpy()
+    assert rel_linf_res(r_gpu, orc.residual(oc, q)) < 1e-12
+
+
+@pytest.mark.parametrize("k,cfl", [(1, 0.24), (2, 0.13), (3, 0.08), (4, 0.05)])
+def test_dg_overintegration_100_steps(orc, P, k, cfl):
+    from paper_1709_01619_b200.inputs import perturb
+    oc, s = pair(orc, P, 10, 10, "dg", k, cfl, dg_overintegrate=1)
+    q = perturb(orc.init_case(oc), seed=6, amp=1e-3)
+    s.set_state(q)
+    t_g, n_g = s.step(100)
+    q_o, t_o, n_o = orc.run(oc, q, 100)
+    assert n_g == n_o == 100 and abs(t_g - t_o) <= 1e-12 * t_o
+    assert rel_linf(s.get_state(), q_o) <= 1e-10
+
+
+@pytest.mark.parametrize("k,cfl", [(1, 0.2), (2, 0.08)])
+def test_dg_overintegration_shock_limited(orc, P, k, cfl):
+    """over-integrated DG with the limiter after every stage (the fused element
+    averages of dgoi_stage_kernel feed k_limit): state and marks per element."""
+    box = (-1.0, 1.0, -1.0, 1.0)
+    oc, s = pair(orc, P, 24, 24, "dg", k, cfl, bc=1, box=box, limiter=1, dg_overintegrate=1)
+    q0 = orc.init_case(oc, orc.SHOCK)
+    s.set_state(q0)
+    cnt = np.zeros(8, dtype=np.int64)
+    em = np.zeros(24 * 24, dtype=np.int64)
+    q_o, t_o, n_o = orc.run(oc, q0, 40, 0.25, counts=cnt, emap=em)
+    _, n_g = s.step(40, 0.25)
+    assert n_g == n_o
+    assert rel_linf(s.get_state(), q_o) <= 1e-10
+    np.testing.assert_array_equal(s.decision_map(), em)
+
+
+def test_dg_overintegration_self_exchange_bitwise(orc, P, monkeypatch):
+    """the strip path (interior rows, then the boundary bands after the ghost-row
+    exchange) of the over-integrated kernel equals the single launch bitwise"""
+    from paper_1709_01619_b200.inputs import perturb
+    outs = []
+    for sx in ("0", "1", "2"):
+        monkeypatch.setenv("HOM2D_SELF_EXCHANGE", sx)
+        oc, s = pair(orc, P, 12, 10, "dg", 2, 0.1, dg_overintegrate=1)
+        s.set_state(perturb(orc.init_case(oc), seed=8, amp=1e-3))
+        s.step(10)
+        outs.append(s.get_state())
+        s.close()
+    np.testing.assert_array_equal(outs[0], outs[1])
+    np.testing.assert_array_equal(outs[0], outs[2])

@@ -81,3 +81,18 @@ def test_derivative_and_interpolation(k):
         np.testing.assert_allclose(t["sd_I"] @ xs ** d, xf ** d, atol=1e-13)
     for d in range(n + 1):
         np.testing.assert_allclose(t["sd_D"] @ xf ** d, d * xs ** max(d - 1, 0) * (d > 0), atol=1e-12)
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 4])
+def test_overintegration_tables(k):
+    """DG (k+2)-point over-integration (f3): the Gauss rule and the GL-basis values
+    and derivatives at its points (exact on polynomials of degree <= k)."""
+    n = k + 1
+    t = T[k]
+    z, W = L.leggauss(n + 1)
+    np.testing.assert_allclose(t["oi_z"], z, atol=2e-16)
+    np.testing.assert_allclose(t["oi_W"], W, atol=1e-15)
+    xs = t["xi_gl"]
+    for d in range(n):
+        np.testing.assert_allclose(t["oi_L"] @ xs ** d, z ** d, atol=1e-14)
+        np.testing.assert_allclose(t["oi_dL"] @ xs ** d, d * z ** max(d - 1, 0) * (d > 0), atol=1e-13)
