@@ -333,13 +333,13 @@ constexpr int WS = 62, WL = 64, WW = WL + 4;  // cells per warp strip; ring row 
 constexpr int WD = H2D_FVW_DEPTH, WNS = 3 + WD;  // rows in flight; ring rows
 constexpr int QS = WD + 1;                       // q^n ring rows (row x lands with ring row x+2, read at step x)
 // dynamic shared memory: per warp WNS ring rows x 4 components x WW, then (stages
-// with q^n) QS q-ring rows x 4 x WS, then the block-max scratch
+// with q^n) QS q-ring rows x 4 x WL, then the block-max scratch
 constexpr int WRING = WNS * 4 * WW, WQ = QS * 4 * WL;
 constexpr size_t fvw_smem(bool hq0) { return sizeof(double) * ((size_t)WPC * (WRING + (hq0 ? WQ : 0)) + WPC); }
 }  // namespace
 
 template <int ORDER, bool REC, int V>
-__global__ void __launch_bounds__(WPC * 32, H2D_FVW_MINB) fv_warp_kernel(const StageArgs a, const int vec) {
+__global__ void __launch_bounds__(WPC * 32, H2D_FVW_MINB) fv_warp_kernel(const StageArgs a) {
   const bool HQ0 = V == 8 ? a.q0 != nullptr : (V & 1), HLAM = V == 8 ? (a.lam || a.bad) : (V & 2) != 0;
   extern __shared__ __align__(16) double fv_smem[];
   double(*const ring)[WNS][4][WW] = reinterpret_cast<double(*)[WNS][4][WW]>(fv_smem);
@@ -363,11 +363,6 @@ __global__ void __launch_bounds__(WPC * 32, H2D_FVW_MINB) fv_warp_kernel(const S
     long long* const dec = REC ? a.dec : nullptr;
     double(*const rw)[4][WW] = ring[wid];
     double(*const qw)[4][WL] = qring[HQ0 ? wid : 0];
-    // halo column of lanes 0..3: slots 0, 1 = cells i0-2, i0-1; TXv+2, TXv+3 = cells i0+TXv, +1
-    int hx = lane < 2 ? i0 - 2 + lane : i0 + TXv + (lane - 2);
-    if (a.bcx == 0) hx = hx < 0 ? hx + a.nx : (hx >= a.nx ? hx - a.nx : hx);
-    else hx = hx < 0 ? 0 : (hx >= a.nx ? a.nx - 1 : hx);
-    const int hslot = lane < 2 ? lane : TXv + lane;
     auto row_ptr = [&](int jr, long long& cs) -> const double* {
       cs = a.cs;
       if (jr < 0) {
@@ -388,35 +383,40 @@ __global__ void __launch_bounds__(WPC * 32, H2D_FVW_MINB) fv_warp_kernel(const S
       return a.dmap + (long long)jr * a.nx + ir;
     };
     // the lane's pair (16 B when aligned) of each component of a row into dst[c][...]
+    // copies without branches (a TMA bulk-copy ring with one mbarrier per slot
+    // was measured 7-13 % slower: one lane issuing 8-16 small bulk copies per
+    // step): the lane's pair is one 16-B cp.async whose source size is 16, 8
+    // (last own cell) or 0 (a lane past the strip: zero fill, never read as
+    // data); the halo is one 8-B cp.async per lane, lanes 4..31 with source size
+    // 0 into the unused ring slot WW-2
+    // halo column of lanes 0..3: slots 0, 1 = cells i0-2, i0-1; TXv+2, TXv+3 = cells i0+TXv, +1
+    int hx = lane < 2 ? i0 - 2 + lane : i0 + TXv + (lane - 2);
+    if (a.bcx == 0) hx = hx < 0 ? hx + a.nx : (hx >= a.nx ? hx - a.nx : hx);
+    else hx = hx < 0 ? 0 : (hx >= a.nx ? a.nx - 1 : hx);
+    const int psz = own1 ? 16 : (own0 ? 8 : 0);
+    const int hsz = lane < 4 ? 8 : 0;
+    const int hs = lane < 4 ? (lane < 2 ? lane : TXv + lane) : WW - 2;
+    const int pc = own0 ? c0 : 0;  // a valid source column for lanes past the strip
+    const int hxx = lane < 4 ? hx : i0;
     auto copy_pair = [&](double* d0, int dstride, const double* g, long long cs) {
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        double* d = d0 + c * dstride;
-        const double* gc = g + c * cs;
-        if (vec) {
-          if (own1) asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(d)), "l"(gc) : "memory");
-          else if (own0) asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(d)), "l"(gc) : "memory");
-        } else {
-          if (own0) asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(d)), "l"(gc) : "memory");
-          if (own1)
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(d + 1)), "l"(gc + 1) : "memory");
-        }
-      }
+      for (int c = 0; c < 4; ++c)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(d0 + c * dstride)),
+                     "l"(g + c * cs), "r"(psz)
+                     : "memory");
     };
     auto issue_row = [&](int jr, int slot) {
       long long cs;
       const double* rb = row_ptr(jr, cs);
-      copy_pair(&rw[slot][0][c0 + 2], WW, rb + i0 + c0, cs);
-      if (lane < 4) {
+      copy_pair(&rw[slot][0][c0 + 2], WW, rb + i0 + pc, cs);
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
-          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(&rw[slot][c][hslot])),
-                       "l"(rb + c * cs + hx)
-                       : "memory");
-      }
+      for (int c = 0; c < 4; ++c)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(&rw[slot][c][hs])),
+                     "l"(rb + c * cs + hxx), "r"(hsz)
+                     : "memory");
     };
     auto issue_q0 = [&](int jr, int slot) {  // q^n row jr (an own row) into q-ring slot
-      copy_pair(&qw[slot][0][c0], WL, a.q0 + (long long)jr * a.nx + i0 + c0, a.cs);
+      copy_pair(&qw[slot][0][c0], WL, a.q0 + (long long)jr * a.nx + i0 + pc, a.cs);
     };
     auto commit = [] { asm volatile("cp.async.commit_group;" ::: "memory"); };
 
@@ -540,20 +540,17 @@ __global__ void __launch_bounds__(WPC * 32, H2D_FVW_MINB) fv_warp_kernel(const S
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         double* g = a.out + c * a.cs + gidx;
-        if (vec && own1) {
-          *reinterpret_cast<double2*>(g) = make_double2(o[0][c], o[1][c]);
-        } else {
-          if (own0) g[0] = o[0][c];
-          if (own1) g[1] = o[1][c];
-        }
+        if (own1) *reinterpret_cast<double2*>(g) = make_double2(o[0][c], o[1][c]);
+        if (own0 && !own1) g[0] = o[0][c];
       }
       if (HLAM) {
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
-          if (!(k ? own1 : own0)) continue;
+          const bool ok = k ? own1 : own0;
           const Prim w = prims(o[k], gm1);
-          lam = nanmax(lam, fmax(fabs(w.u), fabs(w.v)) + fsqrt(gam * w.p * w.ri));
-          if (a.bad && !admissible(o[k][0], w.p)) atomicMin(a.bad, (unsigned long long)(gidx + k));
+          const double sp = fmax(fabs(w.u), fabs(w.v)) + fsqrt(gam * w.p * w.ri);
+          lam = ok ? nanmax(lam, sp) : lam;
+          if (ok && a.bad && !admissible(o[k][0], w.p)) atomicMin(a.bad, (unsigned long long)(gidx + k));
         }
       }
       adv(S0, WNS); adv(S1, WNS); adv(S2, WNS); adv(SI, WNS); adv(Q0, QS); adv(QI, QS);
@@ -576,17 +573,6 @@ int march_rows(int nrows, int strips, int rb_max, int ctas_per_sm) {
   return (int)rows;
 }
 
-#ifndef H2D_FV_WARP
-#define H2D_FV_WARP 1  // warp-strip kernel (0: the CTA-strip kernel)
-#endif
-template <int ORDER, bool REC, int V>
-static cudaError_t fvw_launch(dim3 grid, const StageArgs& a, cudaStream_t s, int vec) {
-  static std::atomic<unsigned long long> attr{0};
-  const size_t sm = fvw_smem(V == 8 ? a.q0 != nullptr : (V & 1) != 0);
-  const cudaError_t e = smem_optin(fv_warp_kernel<ORDER, REC, V>, (int)fvw_smem(true), attr);
-  if (e != cudaSuccess) return e;
-  return launch_pdl_if(!a.no_pdl, fv_warp_kernel<ORDER, REC, V>, grid, dim3(WPC * 32), sm, s, a, vec);
-}
 // rows per CTA such that the grid is (close to) a whole number of waves of
 // ctas_per_sm x #SM resident CTAs: the fewest waves whose marches fit rb_max
 int march_rows_waves(int nrows, int strips, int rb_max, int ctas_per_sm) {
@@ -605,33 +591,44 @@ int march_rows_waves(int nrows, int strips, int rb_max, int ctas_per_sm) {
   }
 }
 
+#ifndef H2D_FV_WARP
+#define H2D_FV_WARP 1  // warp-strip kernel where the layout allows (0: the CTA-strip kernel always)
+#endif
+template <int ORDER, bool REC, int V>
+static cudaError_t fvw_launch(dim3 grid, const StageArgs& a, cudaStream_t s) {
+  static std::atomic<unsigned long long> attr{0};
+  const size_t sm = fvw_smem(V == 8 ? a.q0 != nullptr : (V & 1) != 0);
+  const cudaError_t e = smem_optin(fv_warp_kernel<ORDER, REC, V>, (int)fvw_smem(true), attr);
+  if (e != cudaSuccess) return e;
+  return launch_pdl_if(!a.no_pdl, fv_warp_kernel<ORDER, REC, V>, grid, dim3(WPC * 32), sm, s, a);
+}
+
 template <int ORDER, bool REC>
-static void fv_launch_v(int v, dim3 grid, const StageArgs& a, cudaStream_t s, int vec) {
-#if H2D_FV_WARP
-  switch (v) {
-    case 0: fvw_launch<ORDER, REC, 0>(grid, a, s, vec); break;
-    case 1: fvw_launch<ORDER, REC, 1>(grid, a, s, vec); break;
-    case 3: fvw_launch<ORDER, REC, 3>(grid, a, s, vec); break;
-    default: fvw_launch<ORDER, REC, 8>(grid, a, s, vec); break;
+static void fv_launch_v(int v, dim3 grid, const StageArgs& a, cudaStream_t s, bool warp) {
+  if (warp) {
+    switch (v) {
+      case 0: fvw_launch<ORDER, REC, 0>(grid, a, s); break;
+      case 1: fvw_launch<ORDER, REC, 1>(grid, a, s); break;
+      case 3: fvw_launch<ORDER, REC, 3>(grid, a, s); break;
+      default: fvw_launch<ORDER, REC, 8>(grid, a, s); break;
+    }
+    return;
   }
-#else
-  (void)vec;
   switch (v) {
     case 0: launch_pdl_if(!a.no_pdl, fv_stage_kernel<ORDER, REC, 0>, grid, dim3(FTX), 0, s, a); break;
     case 1: launch_pdl_if(!a.no_pdl, fv_stage_kernel<ORDER, REC, 1>, grid, dim3(FTX), 0, s, a); break;
     case 3: launch_pdl_if(!a.no_pdl, fv_stage_kernel<ORDER, REC, 3>, grid, dim3(FTX), 0, s, a); break;
     default: launch_pdl_if(!a.no_pdl, fv_stage_kernel<ORDER, REC, 8>, grid, dim3(FTX), 0, s, a); break;
   }
-#endif
 }
 
 template <bool REC>
-static void fv_launch_r(int rec, int v, dim3 grid, const StageArgs& a, cudaStream_t s, int vec) {
+static void fv_launch_r(int rec, int v, dim3 grid, const StageArgs& a, cudaStream_t s, bool warp) {
   switch (rec) {
-    case 1: fv_launch_v<1, REC>(v, grid, a, s, vec); break;
-    case 2: fv_launch_v<2, REC>(v, grid, a, s, vec); break;
-    case 3: fv_launch_v<3, REC>(v, grid, a, s, vec); break;
-    default: fv_launch_v<4, REC>(v, grid, a, s, vec); break;
+    case 1: fv_launch_v<1, REC>(v, grid, a, s, warp); break;
+    case 2: fv_launch_v<2, REC>(v, grid, a, s, warp); break;
+    case 3: fv_launch_v<3, REC>(v, grid, a, s, warp); break;
+    default: fv_launch_v<4, REC>(v, grid, a, s, warp); break;
   }
 }
 
@@ -641,24 +638,25 @@ int launch_fv_stage(int k, const StageArgs& a0, cudaStream_t s) {
   StageArgs a = a0;
   const int nr = row_range(a);
   if (nr <= 0) return 0;
-#if H2D_FV_WARP
-  const int strips = ((a.nx + WS - 1) / WS + WPC - 1) / WPC;  // CTAs across x
-  a.rows = march_rows_waves(nr, strips, FRB, H2D_FVW_MINB);
-  // 16-B pair accesses: every row / component start even and every array 16-B aligned
-  const int vec = (a.nx % 2 == 0) && (a.cs % 2 == 0) && (a.gcs % 2 == 0) && al16(a.q) && al16(a.q0) &&
-                  al16(a.out) && al16(a.ghost_lo) && al16(a.ghost_hi);
-#else
-  const int strips = (a.nx + FTX - 1) / FTX;
-  a.rows = march_rows(nr, strips, FRB, H2D_FV_MINB);
-  const int vec = 0;
-#endif
+  // the warp kernel moves cell pairs as 16-B units: every row / component start
+  // even and every array 16-B aligned (odd widths, e.g. 45 or 131 cells: the CTA kernel)
+  const bool warp = H2D_FV_WARP && (a.nx % 2 == 0) && (a.cs % 2 == 0) && (a.gcs % 2 == 0) && al16(a.q) &&
+                    al16(a.q0) && al16(a.out) && al16(a.ghost_lo) && al16(a.ghost_hi);
+  int strips;
+  if (warp) {
+    strips = ((a.nx + WS - 1) / WS + WPC - 1) / WPC;  // CTAs across x
+    a.rows = march_rows_waves(nr, strips, FRB, H2D_FVW_MINB);
+  } else {
+    strips = (a.nx + FTX - 1) / FTX;
+    a.rows = march_rows(nr, strips, FRB, H2D_FV_MINB);
+  }
   dim3 grid(strips, (nr + a.rows - 1) / a.rows);
   // reconstruction: 1 MUSCL-2, 2 MUSCL-3 (minmod-limited); 3 / 4 the same
   // kappa-schemes unlimited (hom2d_config.fv_unlimited, f3)
   const int rec = k + (a.fv_unlimited ? 2 : 0);
   const int v = (a.q0 ? 1 : 0) | ((a.lam || a.bad) ? 2 : 0);
-  if (a.dec) fv_launch_r<true>(rec, v, grid, a, s, vec);
-  else fv_launch_r<false>(rec, v, grid, a, s, vec);
+  if (a.dec) fv_launch_r<true>(rec, v, grid, a, s, warp);
+  else fv_launch_r<false>(rec, v, grid, a, s, warp);
   return (int)cudaPeekAtLastError();
 }
 
