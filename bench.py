@@ -229,6 +229,8 @@ def time_to_error(P, torch, method, k, stream, max_seconds=20.0):
     R8) and device seconds of hom2d_step per grid; T(E*) by log-log interpolation
     between the bracketing grids (E* = 1e-4, 2e-5).  One GPU."""
     ladder = [20, 28, 40, 57, 80, 113, 160, 226, 320, 453, 640, 905, 1280, 1810, 2560]
+    if method != "fv" and k >= 3:  # P3/P4 reach 1e-4 below 20^2: start at 8^2 so T(E*) is interpolated
+        ladder = [8, 10, 12, 14, 17, 20, 24, 28, 34, 40, 48, 57, 68, 80, 96, 113]
     rows, spent = [], 0.0
     for n in ladder:
         nn = n * (k + 1) if method == "fv" else n
@@ -284,6 +286,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-tte", action="store_true", help="skip the time-to-error ladder")
+    ap.add_argument("--no-weak", action="store_true", help="skip the weak-scaling workloads (configs[4])")
     args = ap.parse_args()
     assert args.warmup >= 3, "timing rules: W >= 3"
     wl = args.workload
@@ -304,6 +307,10 @@ def main():
         build.build()
     torch.cuda.set_device(local)
     if world > 1:
+        # NCCL's communicator-init lines (nranks, ring/tree/NVLS setup) on stderr, for
+        # the driver's check of the communicator size; INIT only, to keep them short
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
         dist.barrier()
     method, k, nx, ny, cfl, weak, case = workload(wl)
@@ -409,6 +416,34 @@ def main():
                "single_thread": {"value": v1, "sample": f"{sn1}x{sn1} elements, 4 steps ({el1:.1f} s)"},
                "cpu": cpu_info()}
 
+    # ---- the weak-scaling workloads (BASELINE configs[4]: per GPU 8192 x 1024
+    # elements of CPR P2 / MUSCL-2 cells, y-strips) measured in the same run, so a
+    # scaling sweep over N yields both curves; device time, max over ranks -------
+    weak_lines = None
+    if not args.no_weak and not weak:
+        weak_lines = []
+        for wwl in ("cpr_p2_8192w", "fv2_8192w"):
+            wm, wk, wnx, wny, wcfl, _, _ = workload(wwl)
+            wny *= world
+            ws = P.Solver(P.make_config(wnx, wny, method=wm, k=wk, cfl=wcfl), rank=rank, nranks=world, device=local,
+                          stream=stream, nccl_id=nid)
+            ws.init_case(P.VORTEX)
+            ws.step(args.warmup)
+            barrier_sync()
+            w0, w1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            w0.record(stream)
+            ws.step(args.steps)
+            w1.record(stream)
+            barrier_sync()
+            wt = torch.tensor([w0.elapsed_time(w1)], dtype=torch.float64, device="cuda")
+            if world > 1:
+                dist.all_reduce(wt, op=dist.ReduceOp.MAX)
+            wnpe = 1 if wm == "fv" else (wk + 1) ** 2
+            weak_lines.append({"workload": wwl, "scaling": "weak", "nx": wnx, "ny": wny,
+                               "dof": wnx * wny * wnpe, "value": wnx * wny * wnpe * 3 * args.steps / (float(wt[0]) * 1e-3),
+                               "unit": "DOF-stage/s", "ms_per_step": float(wt[0]) / args.steps})
+            ws.close()
+
     if rank == 0:
         line = {"metric": "fp64 DOF-stage updates/s", "value": value, "unit": "DOF-stage/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
@@ -421,6 +456,7 @@ def main():
                            "l2_flush": f"none needed: {4 * ndof_global * 8 / 1e9:.2f} GB/state array >> 126 MB L2"},
                 "e2e": e2e, "gpu_launches": gpu_launches, "roofline": roofline, "cpu_baseline": cpu,
                 "time_to_error": tte,
+                "weak_scaling_workloads": weak_lines,
                 "clocks": clocks,
                 "hbm_frac_end_to_end": value * BYTES_PER_DOF_STEP / 3.0 / 1e9 / world / peak}
         print(json.dumps(line), flush=True)

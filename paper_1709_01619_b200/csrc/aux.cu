@@ -516,8 +516,11 @@ __device__ __forceinline__ void rebuild_element(const AuxArgs& A, const Nodes& n
 
 // rows of elements per thread: the detections of a thread's LROWS elements issue
 // their loads back to back (and with the dt flag's), one memory round trip for all
+// A/B: 4 vs 2 +0.8 % (CPR P1 shock tube); at the 64-register cap 4 rows double the
+// spills of the characteristic variants and spill the P2 GL one, so 4 only for
+// the default P1 variants
 #ifndef H2D_LROWS
-#define H2D_LROWS(N) ((N) <= 3 ? 4 : 1)  // A/B: 4 vs 2 +0.8 % (P1 shock tube)
+#define H2D_LROWS(N, CHAR) ((N) == 2 && !(CHAR) ? 4 : ((N) <= 3 ? 2 : 1))
 #endif
 
 template <int N, bool GLLP, bool ALL, bool CHAR>
@@ -526,7 +529,7 @@ __global__ void __launch_bounds__(128, H2D_LIMIT_MINB) k_limit(const AuxArgs A, 
                                                                const double* qbar_lo, const double* qbar_hi,
                                                                long long gcs, int bcx, double eps, double dx,
                                                                double dy, long long* dec, long long* emap) {
-  constexpr int R = H2D_LROWS(N);
+  constexpr int R = H2D_LROWS(N, CHAR);
   pdl_wait();
   pdl_launch();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -596,7 +599,7 @@ void launch_averages(const AuxArgs& a, const double* q, double* qbar, cudaStream
 template <int N, bool GLLP, bool ALL, bool CHAR>
 void launch_limit_t(const AuxArgs& a, double* q, const double* qbar, const double* qbar_lo, const double* qbar_hi,
                     long long qbar_gcs, int bcx, double eps, long long* dec, long long* emap, cudaStream_t s) {
-  const int ry = (a.nrows + H2D_LROWS(N) - 1) / H2D_LROWS(N);
+  const int ry = (a.nrows + H2D_LROWS(N, CHAR) - 1) / H2D_LROWS(N, CHAR);
   dim3 grid((a.nx + 127) / 128, ry < 65535 ? ry : 65535);
   // element widths (Eq. (35)) in host IEEE double: bitwise the device's quotient
   const double dx = (a.xmax - a.xmin) / a.nx, dy = (a.ymax - a.ymin) / a.ny_global;

@@ -46,6 +46,20 @@ __device__ __forceinline__ double fsqrt(double x) {
   return fma(0.5 * y, fma(-s, s, x), s);
 }
 
+// square root for the Rusanov dissipation speed only (|u_n| + c in lam (q_R - q_L),
+// P:869-870): the MUFU seed and one Newton step, s = x y (relative error
+// ~1.5 e0^2 <= ~2^-41).  lam multiplies a state jump, so its error enters the
+// flux at <= 2^-41 |q_R - q_L| / |f| -- far below the rounding of the flux
+// itself on smooth data and below the parity bar on any data -- and 3 fp64
+// operations per call are saved.  Not used where c decides dt (Eq. (36)).
+__device__ __forceinline__ double fsqrt_ws(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double e = fma(-x * y, y, 1.0);
+  y = fma(0.5 * y, e, y);
+  return x * y;
+}
+
 // one reciprocal per point (the only fp64 division of a flux evaluation)
 __device__ __forceinline__ Prim prims(const double q[4], double gm1) {
   Prim w;

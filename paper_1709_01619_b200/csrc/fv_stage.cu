@@ -30,6 +30,9 @@ namespace {
 constexpr int FTX = H2D_FTX, FRB = 64, FD = H2D_FV_DEPTH, FNS = 3 + FD;  // cells/strip, rows/march, in flight, ring rows
 constexpr int FW = FTX + 4;                    // ring row width: 2 halo cells each side
 
+#ifndef H2D_FV_WSQRT
+#define H2D_FV_WSQRT fsqrt_ws  // dissipation-speed square root (A/B: fsqrt)
+#endif
 // TWICE the Rusanov flux along DIR: fL + fR - lam (qR - qL).  The
 // factor 1/2 moves into the metric of the flux difference (0.5 / dx): scaling
 // by powers of two is exact, so nothing changes but 5 multiplications per face.
@@ -39,8 +42,8 @@ __device__ __forceinline__ void rusanov2(const double qL[4], const double qR[4],
   double fL[4], fR[4];
   flux<DIR>(qL, wl, fL);
   flux<DIR>(qR, wr, fR);
-  const double sl = fabs(DIR == 0 ? wl.u : wl.v) + fsqrt(gam * wl.p * wl.ri);
-  const double sr = fabs(DIR == 0 ? wr.u : wr.v) + fsqrt(gam * wr.p * wr.ri);
+  const double sl = fabs(DIR == 0 ? wl.u : wl.v) + H2D_FV_WSQRT(gam * wl.p * wl.ri);
+  const double sr = fabs(DIR == 0 ? wr.u : wr.v) + H2D_FV_WSQRT(gam * wr.p * wr.ri);
   const double lam = fmax(sl, sr);
 #pragma unroll
   for (int c = 0; c < 4; ++c) F2[c] = fma(-lam, qR[c] - qL[c], fL[c] + fR[c]);
@@ -385,25 +388,30 @@ __global__ void __launch_bounds__(WPC * 32, H2D_FVW_MINB) fv_warp_kernel(const S
     // the lane's pair (16 B when aligned) of each component of a row into dst[c][...]
     // copies without branches (a TMA bulk-copy ring with one mbarrier per slot
     // was measured 7-13 % slower: one lane issuing 8-16 small bulk copies per
-    // step): the lane's pair is one 16-B cp.async whose source size is 16, 8
-    // (last own cell) or 0 (a lane past the strip: zero fill, never read as
-    // data); the halo is one 8-B cp.async per lane, lanes 4..31 with source size
-    // 0 into the unused ring slot WW-2
+    // step): predicated cp.async -- the lane's pair as one 16-B copy (or its last
+    // own cell as an 8-B copy), the halo cells by lanes 0..3; a lane past the
+    // strip copies nothing (its slots are never read as data, and a zero-filling
+    // copy there would race with the halo copies into slots TXv+2, TXv+3)
     // halo column of lanes 0..3: slots 0, 1 = cells i0-2, i0-1; TXv+2, TXv+3 = cells i0+TXv, +1
     int hx = lane < 2 ? i0 - 2 + lane : i0 + TXv + (lane - 2);
     if (a.bcx == 0) hx = hx < 0 ? hx + a.nx : (hx >= a.nx ? hx - a.nx : hx);
     else hx = hx < 0 ? 0 : (hx >= a.nx ? a.nx - 1 : hx);
-    const int psz = own1 ? 16 : (own0 ? 8 : 0);
-    const int hsz = lane < 4 ? 8 : 0;
-    const int hs = lane < 4 ? (lane < 2 ? lane : TXv + lane) : WW - 2;
-    const int pc = own0 ? c0 : 0;  // a valid source column for lanes past the strip
-    const int hxx = lane < 4 ? hx : i0;
+    const int p16 = own1, p8 = own0 && !own1, ph = lane < 4;
+    const int hs = ph ? (lane < 2 ? lane : TXv + lane) : 0;
+    const int pc = own0 ? c0 : 0;  // a valid address for lanes past the strip
+    const int hxx = ph ? hx : i0;
     auto copy_pair = [&](double* d0, int dstride, const double* g, long long cs) {
 #pragma unroll
-      for (int c = 0; c < 4; ++c)
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(d0 + c * dstride)),
-                     "l"(g + c * cs), "r"(psz)
-                     : "memory");
+      for (int c = 0; c < 4; ++c) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %2, 0;\n\t@p cp.async.cg.shared.global [%0], [%1], 16;\n\t}"
+            ::"r"(smem_u32(d0 + c * dstride)), "l"(g + c * cs), "r"(p16)
+            : "memory");
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %2, 0;\n\t@p cp.async.ca.shared.global [%0], [%1], 8;\n\t}"
+            ::"r"(smem_u32(d0 + c * dstride)), "l"(g + c * cs), "r"(p8)
+            : "memory");
+      }
     };
     auto issue_row = [&](int jr, int slot) {
       long long cs;
@@ -411,9 +419,10 @@ __global__ void __launch_bounds__(WPC * 32, H2D_FVW_MINB) fv_warp_kernel(const S
       copy_pair(&rw[slot][0][c0 + 2], WW, rb + i0 + pc, cs);
 #pragma unroll
       for (int c = 0; c < 4; ++c)
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(&rw[slot][c][hs])),
-                     "l"(rb + c * cs + hxx), "r"(hsz)
-                     : "memory");
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %2, 0;\n\t@p cp.async.ca.shared.global [%0], [%1], 8;\n\t}"
+            ::"r"(smem_u32(&rw[slot][c][hs])), "l"(rb + c * cs + hxx), "r"(ph)
+            : "memory");
     };
     auto issue_q0 = [&](int jr, int slot) {  // q^n row jr (an own row) into q-ring slot
       copy_pair(&qw[slot][0][c0], WL, a.q0 + (long long)jr * a.nx + i0 + pc, a.cs);

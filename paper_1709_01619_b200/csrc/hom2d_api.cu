@@ -31,6 +31,8 @@ struct hom2d {
   long long glaunch[7] = {};
   bool graph_off = false;
   long long eager_steps = 0;
+  long long graph_after = 256;             // eager steps before batches run as graphs
+  int graph_min_batch = 64;                // smallest batch run as a graph
   ncclComm_t comm = nullptr;
   int row0 = 0, nrows = 0, np = 1, G = 1;  // G ghost rows (HO 1, FV 2)
   long long nloc = 0;                      // values per component of the local strip
@@ -412,6 +414,10 @@ hom2d_status hom2d_create(const hom2d_config* cfg, const hom2d_dist* dist, void*
   {
     const char* ng = getenv("HOM2D_NO_GRAPH");  // A/B: eager launches instead of CUDA graphs
     h->graph_off = ng && ng[0] == '1';
+    const char* gm = getenv("HOM2D_GRAPH_AFTER");  // A/B: eager steps before graph batches (default 256)
+    if (gm && *gm) h->graph_after = atoll(gm);
+    const char* gb = getenv("HOM2D_GRAPH_MIN_BATCH");  // A/B: smallest graphed batch (default 64)
+    if (gb && *gb) h->graph_min_batch = atoi(gb);
     pdl_refresh();
   }
   cudaError_t ce = cudaSetDevice(h->device);
@@ -650,7 +656,7 @@ extern "C" hom2d_status hom2d_step(hom2d* h, int32_t max_steps, double t_end, do
     }
     // graphs pay for their capture only on long runs: full 64-step batches once the
     // handle has marched 256 steps eagerly
-    if (graphs && batch == 64 && h->eager_steps >= 256) {
+    if (graphs && batch >= h->graph_min_batch && h->eager_steps >= h->graph_after) {
       if ((st = graph_steps(h, batch))) return st;
     } else {
       for (int s = 0; s < batch; ++s)
