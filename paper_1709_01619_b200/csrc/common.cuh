@@ -206,6 +206,19 @@ __device__ __forceinline__ void count_dec(long long* dec, int which, int w = 1) 
 // as a tie (slot 4), not by outcome: its branch may legitimately differ between
 // two fp64 evaluation orders.
 #define DEC_TIE 1e-12
+// |a| <= |b| (minmod's magnitude test); H2D_ICMP: on the integer pipe (sign-masked
+// bit patterns compare like magnitudes for non-NaN values) instead of a DSETP
+#ifndef H2D_ICMP
+#define H2D_ICMP 0
+#endif
+__device__ __forceinline__ bool mag_le(double a, double b) {
+#if H2D_ICMP
+  const unsigned long long m = 0x7fffffffffffffffull;
+  return ((unsigned long long)__double_as_longlong(a) & m) <= ((unsigned long long)__double_as_longlong(b) & m);
+#else
+  return fabs(a) <= fabs(b);
+#endif
+}
 // (w: how many of the paper's face evaluations this one call stands for; mp:
 // optional per-cell decision-map entry, the outcome added as w << 16*(slot),
 // slot 0 -> 0, 1 -> first argument, 2 -> second, 3 tie -- hom2d_decision_map)
@@ -213,7 +226,7 @@ __device__ __forceinline__ double minmod2(double a, double b, long long* dec, in
   // value without branches: the argument of smaller magnitude when both have the
   // same strict sign (equal magnitudes: equal values), else 0.  Equal sign BITS
   // suffice: a zero argument has the smaller magnitude, so m is then +-0 anyway.
-  const double m = fabs(a) <= fabs(b) ? a : b;
+  const double m = mag_le(a, b) ? a : b;
   const double r = (__double2hiint(a) ^ __double2hiint(b)) >= 0 ? m : 0.0;
   if (dec) {
     int which = 1;
@@ -262,7 +275,7 @@ __device__ __forceinline__ void cell_faces(double qm, double q0, double qp, doub
     } else {  // both minmods share the sign test (beta > 0): one sign-bit comparison
       const double bdp = beta * dp, bdm = beta * dm;
       const bool same = (__double2hiint(dm) ^ __double2hiint(dp)) >= 0;
-      const double ma = fabs(dm) <= fabs(bdp) ? dm : bdp, mb = fabs(dp) <= fabs(bdm) ? dp : bdm;
+      const double ma = mag_le(dm, bdp) ? dm : bdp, mb = mag_le(dp, bdm) ? dp : bdm;
       A = same ? ma : 0.0;
       B = same ? mb : 0.0;
     }

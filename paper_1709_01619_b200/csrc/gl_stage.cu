@@ -53,6 +53,9 @@ namespace {
 #define H2D_LMINB2 4
 #endif
 enum { LM_DG = 2, LM_SD = 4 };
+#ifndef H2D_WSQRT
+#define H2D_WSQRT fsqrt_ws  // Rusanov dissipation speed (common.cuh; A/B: fsqrt)
+#endif
 template <int M, int K> struct LTile {
   static constexpr int TX = K == 1 ? 64 : K == 2 ? H2D_LTX2 : (M == LM_DG ? H2D_DG_TX : H2D_SD_TX), RB = 64;
   static constexpr int MINB = K == 1 ? H2D_LMINB1 : K == 2 ? H2D_LMINB2 : H2D_LMINB;
@@ -169,7 +172,7 @@ template <int DIR>
 __device__ __forceinline__ void node_eval(const double q[4], double gm1, double gam, double f[4], double& s) {
   const Prim w = prims(q, gm1);
   flux<DIR>(q, w, f);
-  s = fabs(DIR == 0 ? w.u : w.v) + fsqrt(gam * w.p * w.ri);
+  s = fabs(DIR == 0 ? w.u : w.v) + H2D_WSQRT(gam * w.p * w.ri);  // Rusanov dissipation speed only
 }
 __device__ __forceinline__ void rus(const double qL[4], const double fL[4], double sL, const double qR[4],
                                     const double fR[4], double sR, double F[4]) {

@@ -162,12 +162,15 @@ __device__ __forceinline__ void ld4(const double* p, double v[4]) {
   v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
 }
 
+#ifndef H2D_WSQRT
+#define H2D_WSQRT fsqrt_ws  // Rusanov dissipation speed (common.cuh; A/B: fsqrt)
+#endif
 // node evaluation: the DIR flux and the DIR normal wave speed |u_n| + c
 template <int DIR>
 __device__ __forceinline__ void node_eval(const double q[4], double gm1, double gam, double f[4], double& s) {
   const Prim w = prims(q, gm1);
   flux<DIR>(q, w, f);
-  s = fabs(DIR == 0 ? w.u : w.v) + fsqrt(gam * w.p * w.ri);
+  s = fabs(DIR == 0 ? w.u : w.v) + H2D_WSQRT(gam * w.p * w.ri);  // Rusanov dissipation speed only
 }
 
 __device__ __forceinline__ void rus(const double qL[4], const double fL[4], double sL, const double qR[4],
@@ -424,8 +427,8 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
         pE = prims(qe, gm1);
         flux<0>(qw, pW, fW);
         flux<0>(qe, pE, fE);
-        sw = fabs(pW.u) + fsqrt(gam * pW.p * pW.ri);
-        se = fabs(pE.u) + fsqrt(gam * pE.p * pE.ri);
+        sw = fabs(pW.u) + H2D_WSQRT(gam * pW.p * pW.ri);
+        se = fabs(pE.u) + H2D_WSQRT(gam * pE.p * pE.ri);
         double fl[4], sl, gd[4], sd, gu[4], su;
         node_eval<0>(ql, gm1, gam, fl, sl);
         node_eval<1>(qd, gm1, gam, gd, sd);
