@@ -31,7 +31,9 @@ struct hom2d {
   long long glaunch[7] = {};
   bool graph_off = false;
   long long eager_steps = 0;
-  long long graph_after = 256;             // eager steps before batches run as graphs
+  long long graph_after = 2048;            // eager steps before batches run as graphs (their capture sits
+                                           // in the device timeline: ~2 ms, repaid after ~2-4k steps;
+                                           // profiles/round2_small_grids.md)
   int graph_min_batch = 64;                // smallest batch run as a graph
   ncclComm_t comm = nullptr;
   int row0 = 0, nrows = 0, np = 1, G = 1;  // G ghost rows (HO 1, FV 2)
@@ -414,7 +416,7 @@ hom2d_status hom2d_create(const hom2d_config* cfg, const hom2d_dist* dist, void*
   {
     const char* ng = getenv("HOM2D_NO_GRAPH");  // A/B: eager launches instead of CUDA graphs
     h->graph_off = ng && ng[0] == '1';
-    const char* gm = getenv("HOM2D_GRAPH_AFTER");  // A/B: eager steps before graph batches (default 256)
+    const char* gm = getenv("HOM2D_GRAPH_AFTER");  // A/B: eager steps before graph batches (default 2048)
     if (gm && *gm) h->graph_after = atoll(gm);
     const char* gb = getenv("HOM2D_GRAPH_MIN_BATCH");  // A/B: smallest graphed batch (default 64)
     if (gb && *gb) h->graph_min_batch = atoi(gb);
@@ -654,8 +656,8 @@ extern "C" hom2d_status hom2d_step(hom2d* h, int32_t max_steps, double t_end, do
       const double est = std::ceil((t_end - h->t_host[0]) / h->t_host[1]) + 1.0;
       if (est < batch) batch = est < 1.0 ? 1 : (int)est;
     }
-    // graphs pay for their capture only on long runs: full 64-step batches once the
-    // handle has marched 256 steps eagerly
+    // graphs pay for their capture only on long runs: 64-step batches once the
+    // handle has marched graph_after steps eagerly
     if (graphs && batch >= h->graph_min_batch && h->eager_steps >= h->graph_after) {
       if ((st = graph_steps(h, batch))) return st;
     } else {

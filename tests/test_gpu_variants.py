@@ -78,10 +78,15 @@ def test_shock_limiter_variants(orc, P, method, k, cfl, variant):
 
 
 @pytest.mark.parametrize("method,k,limiter", [("cpr", 3, 0), ("dg", 2, 0), ("fv", 1, 0), ("sd", 1, 1)])
-def test_graph_replay_bitwise_equals_eager(orc, P, monkeypatch, method, k, limiter):
-    """hom2d_step replays a cached 64-step CUDA graph on long single-GPU runs; the
+@pytest.mark.parametrize("after,min_batch", [("256", "64"), ("0", "1")])
+def test_graph_replay_bitwise_equals_eager(orc, P, monkeypatch, method, k, limiter, after, min_batch):
+    """hom2d_step replays cached CUDA graphs of 2^i steps on long single-GPU runs
+    (HOM2D_GRAPH_AFTER / HOM2D_GRAPH_MIN_BATCH move the switch-over: after 256
+    eager steps in 64-step batches, or from the first step in any batch); the
     state, t and step count equal the eager launch sequence bitwise, including
     the t_end-clipped last batch."""
+    monkeypatch.setenv("HOM2D_GRAPH_AFTER", after)
+    monkeypatch.setenv("HOM2D_GRAPH_MIN_BATCH", min_batch)
     box, bc, case, cfl = ((-1.0, 1.0, -1.0, 1.0), 1, P.SHOCK, 0.2) if limiter else ((-5.0, 5.0, -5.0, 5.0), 0,
                                                                                    P.VORTEX, 0.08)
     out = []
