@@ -32,11 +32,11 @@ namespace {
 // smem, so narrower strips keep 2+ CTAs per SM (A/B on 4096^2: DG 16 > 32 by
 // 37 % at P3, 3-6 % at P2/P4; SD 32 > 16 by 10 % at P3, 16 > 32 by 13 % at P4)
 #ifndef H2D_DG_TX
-#define H2D_DG_TX (K == 3 ? 14 : 12)  // P3: 14-element strips = 16-slot TMA rows, 4 CTAs/SM (+7.5 % over 16);
-                                     // P4: 12 (60 threads, 4 CTAs/SM; +16 % over 16)
+#define H2D_DG_TX (K == 3 ? 14 : 11)  // P3: 14-element strips = 16-slot TMA rows, 4 CTAs/SM (+7.5 % over 16);
+                                     // P4: 11 (55 threads; 4 CTAs/SM with the 16-B stage stride: +2.7 % over 12)
 #endif
 #ifndef H2D_SD_TX
-#define H2D_SD_TX (K == 3 ? 14 : 12)  // A/B: P3 14 +2.5 % over 32; P4 12 +4 % over 16
+#define H2D_SD_TX (K == 3 ? 14 : 11)  // A/B: P3 14 +2.5 % over 32; P4 11 +4.9 % over 12 (4 vs 3 CTAs/SM)
 #endif
 #ifndef H2D_LMINB
 #define H2D_LMINB 1
@@ -52,12 +52,16 @@ namespace {
 #ifndef H2D_LMINB2
 #define H2D_LMINB2 4
 #endif
+#ifndef H2D_DG_TX2
+#define H2D_DG_TX2 30  // DG P2: 90 threads, 4 CTAs/SM (its g buffer: 32 fits 3; +2.7 %)
+#endif
 enum { LM_DG = 2, LM_SD = 4 };
 #ifndef H2D_WSQRT
 #define H2D_WSQRT fsqrt_ws  // Rusanov dissipation speed (common.cuh; A/B: fsqrt)
 #endif
 template <int M, int K> struct LTile {
-  static constexpr int TX = K == 1 ? 64 : K == 2 ? H2D_LTX2 : (M == LM_DG ? H2D_DG_TX : H2D_SD_TX), RB = 64;
+  static constexpr int TX = K == 1 ? 64 : K == 2 ? (M == LM_DG ? H2D_DG_TX2 : H2D_LTX2) : (M == LM_DG ? H2D_DG_TX : H2D_SD_TX),
+                       RB = 64;
   static constexpr int MINB = K == 1 ? H2D_LMINB1 : K == 2 ? H2D_LMINB2 : H2D_LMINB;
 };
 
@@ -117,7 +121,7 @@ struct L {
   static constexpr int RSW = (NSL + 7) & ~7;
   static constexpr int FIXO = 4 * RSW * 16;
   static constexpr int STG = SWZ ? FIXO + 8 * 16 : 4 * CREG;
-  static constexpr int STGA = (STG + 127) & ~127;
+  static constexpr int STGA = H2D_STGA(STG);  // stage stride (see H2D_STGA)
   static constexpr int OR_ = 0;
   static constexpr int OFW = OR_ + NSTG * STGA;            // W-face fluxes [TX+1][N][4]
   static constexpr int OFN = OFW + (TX + 1) * N * 4;       // N-face fluxes, double-buffered [2][TX][N][4]

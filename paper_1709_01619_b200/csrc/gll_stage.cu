@@ -69,6 +69,16 @@ template <> struct GTile<3> { static constexpr int TX = H2D_TX3, RB = 64, MINB =
 template <> struct GTile<4> { static constexpr int TX = H2D_TX4, RB = 64, MINB = H2D_MINB4; };  // 5 TX threads
 
 enum { GM_CPR = 1, GM_NDG = 3 };
+// NDG strip widths (its g buffer makes its shared memory larger than CPR's)
+#ifndef H2D_NDG_TX1
+#define H2D_NDG_TX1 64
+#endif
+#ifndef H2D_NDG_TX2
+#define H2D_NDG_TX2 32
+#endif
+#ifndef H2D_NDG_TX4
+#define H2D_NDG_TX4 H2D_TX4
+#endif
 constexpr int NSTG = 3;  // ring depth (rows): current, N neighbour, one in flight
 
 struct GMaps {   // P3: 3-D tensor maps {16 points, TX+2 elements, 4 components}
@@ -80,7 +90,10 @@ struct G {
   static constexpr int N = K + 1, NP = N * N;
   // NDG P3 keeps g of every point in smem: 14-element strips (16-slot TMA rows)
   // keep it at 4 CTAs/SM
-  static constexpr int TX = (M == GM_NDG && K == 3) ? H2D_NDG_TX3 : GTile<K>::TX, RB = GTile<K>::RB, NT = TX * N;
+  static constexpr int TX = (M == GM_NDG) ? (K == 1 ? H2D_NDG_TX1 : K == 2 ? H2D_NDG_TX2 : K == 3 ? H2D_NDG_TX3
+                                                                                     : H2D_NDG_TX4)
+                                          : GTile<K>::TX,
+                       RB = GTile<K>::RB, NT = TX * N;
   static constexpr bool SWZ = (NP == 16);           // element row of one component == 128 B
   static constexpr int NSL = TX + 2;                 // W halo, TX elements, E halo
   // 1-D path: W piece | main piece | E piece per component (aligned supersets)
@@ -93,7 +106,7 @@ struct G {
   static constexpr int RSW = (NSL + 7) & ~7;
   static constexpr int FIXO = 4 * RSW * 16;
   static constexpr int STG = SWZ ? FIXO + 8 * 16 : 4 * CREG;
-  static constexpr int STGA = (STG + 127) & ~127;    // 1024-byte aligned stages
+  static constexpr int STGA = H2D_STGA(STG);          // stage stride (see H2D_STGA)
   static constexpr int OR_ = 0;
   static constexpr int OFW = OR_ + NSTG * STGA;       // W-face fluxes [TX+1][N][4]
   static constexpr int OJN = OFW + (TX + 1) * N * 4;  // N jumps of the current row [TX][N][4]

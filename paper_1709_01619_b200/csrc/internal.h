@@ -82,6 +82,14 @@ struct StageArgs {
   int rows;                // marching kernels: element rows per CTA (set by the launcher)
 };
 
+// ring-stage stride of the marching HO kernels (doubles): the 128-B-swizzled P3
+// rows need 1024-B aligned stages; the 1-D bulk-copy paths (P1, P2, P4) only
+// 16-B alignment (H2D_STGA_1K=1: the round-1 1024-B stride everywhere)
+#ifndef H2D_STGA_1K
+#define H2D_STGA_1K 0
+#endif
+#define H2D_STGA(STG) ((SWZ || H2D_STGA_1K) ? (((STG) + 127) & ~127) : (((STG) + 1) & ~1))
+
 // normalise the launch's row range; returns its row count
 inline int row_range(StageArgs& a) {
   if (a.row_hi <= 0) { a.row_lo = 0; a.row_hi = a.nrows; }
