@@ -425,8 +425,13 @@ def main():
         for wwl in ("cpr_p2_8192w", "fv2_8192w"):
             wm, wk, wnx, wny, wcfl, _, _ = workload(wwl)
             wny *= world
+            wid = None
+            if world > 1:  # a fresh NCCL unique id per communicator (an id initialises one communicator only)
+                obj = [P.nccl_unique_id() if rank == 0 else None]
+                dist.broadcast_object_list(obj, src=0)
+                wid = obj[0]
             ws = P.Solver(P.make_config(wnx, wny, method=wm, k=wk, cfl=wcfl), rank=rank, nranks=world, device=local,
-                          stream=stream, nccl_id=nid)
+                          stream=stream, nccl_id=wid)
             ws.init_case(P.VORTEX)
             ws.step(args.warmup)
             barrier_sync()

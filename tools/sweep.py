@@ -252,7 +252,7 @@ def main():
     from paper_1709_01619_b200 import build
     build.build()
     torch.cuda.set_device(0)
-    out = args.out or os.path.join(ROOT, "profiles", f"round1_sweep_{args.what.replace('-', '_')}.json")
+    out = args.out or os.path.join(ROOT, "profiles", f"round2_sweep_{args.what.replace('-', '_')}.json")
     if args.what == "order":
         order_sweep(P, torch, out)
     elif args.what == "shock":
