@@ -15,7 +15,7 @@ def order_table(d):
     out = ["## BASELINE configs[1]: isentropic vortex to t = 1, time to L2(rho) error (reading R8)", "",
            "Device seconds of `hom2d_step` (CUDA events) on the finest grid needed, log-log interpolated "
            "between bracketing grids; FV ladder NDoF-matched ((k+1)·n cells per side). CFL: Table 1 "
-           "(P1/P2), the max-CFL protocol (P3/P4, `round1_cfl_protocol.md`). At these sizes every run is "
+           "(P1/P2), the max-CFL protocol (P3/P4, `round1_cfl_protocol.md; P3/P4 ladders from 8² this round`). At these sizes every run is "
            "launch/latency-bound (<= ~10^6 DOF).", "",
            "| method | k | T(E=1e-4) s | T(E=2e-5) s | grids (n: L2, s) |", "|---|---|---|---|---|"]
     for r in d["results"]:
