@@ -18,6 +18,18 @@ namespace h2d {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// first row and row bound of this CTA's march: row blocks past the first band's
+// (a.nb1) march the optional second band
+__device__ __forceinline__ int band_start(const StageArgs& a, int& hi) {
+  const int by = blockIdx.y;
+  if (a.row_hi2 > a.row_lo2 && by >= a.nb1) {
+    hi = a.row_hi2;
+    return a.row_lo2 + (by - a.nb1) * a.rows;
+  }
+  hi = a.row_hi;
+  return a.row_lo + by * a.rows;
+}
+
 struct Prim {
   double ri, u, v, p;  // 1/rho, velocities, pressure
 };

@@ -65,12 +65,14 @@ __global__ void __launch_bounds__(OI_NT) dgoi_stage_kernel(const StageArgs a, co
     if (dtv == 0.0) return;
   }
   const int tid = threadIdx.x;
-  const long long nel = (long long)a.nx * (a.row_hi - a.row_lo);
+  const long long n1 = (long long)a.nx * (a.row_hi - a.row_lo);
+  const long long nel = n1 + (long long)a.nx * (a.row_hi2 > a.row_lo2 ? a.row_hi2 - a.row_lo2 : 0);
   const long long e = (long long)blockIdx.x * OI_NT + tid;
   const double gm1 = a.gamma - 1.0, gam = a.gamma;
   double lam = 0.0;
   if (e < nel) {
-    const int i = (int)(e % a.nx), jr = a.row_lo + (int)(e / a.nx);
+    const int i = (int)(e % a.nx);
+    const int jr = e < n1 ? a.row_lo + (int)(e / a.nx) : a.row_lo2 + (int)((e - n1) / a.nx);
     const long long m = (long long)jr * a.nx + i;
 #define SQ(c, p) sq[((c) * np + (p)) * OI_NT + tid]
 #define SR(c, p) sR[((c) * np + (p)) * OI_NT + tid]

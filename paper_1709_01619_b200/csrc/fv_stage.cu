@@ -73,8 +73,9 @@ __global__ void __launch_bounds__(FTX, H2D_FV_MINB) fv_stage_kernel(const StageA
     if (dtv == 0.0) return;
   }
   const int tid = threadIdx.x;
-  const int i0 = blockIdx.x * FTX, jb = a.row_lo + blockIdx.y * a.rows;
-  const int TXv = min(FTX, a.nx - i0), RBv = min(a.rows, a.row_hi - jb);
+  int bhi;
+  const int i0 = blockIdx.x * FTX, jb = band_start(a, bhi);
+  const int TXv = min(FTX, a.nx - i0), RBv = min(a.rows, bhi - jb);
   const double gam = a.gamma, gm1 = a.gamma - 1.0;
   const bool own = tid < TXv;
 
@@ -356,11 +357,12 @@ __global__ void __launch_bounds__(WPC * 32, H2D_FVW_MINB) fv_warp_kernel(const S
     if (dtv == 0.0) return;
   }
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int i0 = (blockIdx.x * WPC + wid) * WS, jb = a.row_lo + blockIdx.y * a.rows;
+  int bhi;
+  const int i0 = (blockIdx.x * WPC + wid) * WS, jb = band_start(a, bhi);
   const double gam = a.gamma, gm1 = a.gamma - 1.0;
   double lam = 0.0;
   if (i0 < a.nx) {  // warp-uniform
-    const int TXv = min(WS, a.nx - i0), RBv = min(a.rows, a.row_hi - jb);
+    const int TXv = min(WS, a.nx - i0), RBv = min(a.rows, bhi - jb);
     const int c0 = 2 * lane;                         // local index of the lane's first cell
     const bool own0 = c0 < TXv, own1 = c0 + 1 < TXv;
     long long* const dec = REC ? a.dec : nullptr;
@@ -659,7 +661,7 @@ int launch_fv_stage(int k, const StageArgs& a0, cudaStream_t s) {
     strips = (a.nx + FTX - 1) / FTX;
     a.rows = march_rows(nr, strips, FRB, H2D_FV_MINB);
   }
-  dim3 grid(strips, (nr + a.rows - 1) / a.rows);
+  dim3 grid(strips, band_blocks(a));
   // reconstruction: 1 MUSCL-2, 2 MUSCL-3 (minmod-limited); 3 / 4 the same
   // kappa-schemes unlimited (hom2d_config.fv_unlimited, f3)
   const int rec = k + (a.fv_unlimited ? 2 : 0);

@@ -227,8 +227,9 @@ __global__ void __launch_bounds__(L<M, K>::NT, LTile<M, K>::MINB) gl_stage_kerne
   double* sQ0 = sm + H::OQ0;
 
   const int tid = threadIdx.x;
-  const int i0 = blockIdx.x * TX, jb = a.row_lo + blockIdx.y * a.rows;
-  const int TXv = min(TX, a.nx - i0), RBv = min(a.rows, a.row_hi - jb);
+  int bhi;
+  const int i0 = blockIdx.x * TX, jb = band_start(a, bhi);
+  const int TXv = min(TX, a.nx - i0), RBv = min(a.rows, bhi - jb);
   const double gam = a.gamma, gm1 = a.gamma - 1.0;
   const int lx = tid / N, b = tid - lx * N;
   const bool own = lx < TXv;
@@ -702,7 +703,7 @@ static int launch_l(const StageArgs& a, cudaStream_t s) {
   const int nr = row_range(b);
   if (nr <= 0) return 0;
   b.rows = march_rows(nr, strips, H::RB);
-  dim3 grid(strips, (nr + b.rows - 1) / b.rows);
+  dim3 grid(strips, band_blocks(b));
   const int v = (a.q0 ? 1 : 0) | ((a.lam || a.bad) ? 2 : 0) | (a.qbar ? 4 : 0);
   cudaError_t e = cudaSuccess;
   switch (v) {

@@ -297,13 +297,14 @@ hom2d_status run_stage(hom2d* h, const double* q, const double* q0, double* out,
     in.row_lo = G; in.row_hi = h->nrows - G;
     e = launch_stage(h, in);
     if (!e && async) e = (int)cudaStreamWaitEvent(h->stream, h->ev_halo, 0);
-    StageArgs lo = s, hi = s;
-    lo.row_lo = 0; lo.row_hi = G;
-    hi.row_lo = h->nrows - G; hi.row_hi = h->nrows;
-    lo.no_pdl = hi.no_pdl = async ? 1 : 0;  // they follow the wait on the exchange stream's event
-    if (!e) e = launch_stage(h, lo);
-    if (!e) e = launch_stage(h, hi);
-    h->launches += 3;
+    // both boundary bands [0, G) and [nrows-G, nrows) in ONE launch (the second
+    // band's CTAs follow the first's in the grid): one launch latency per stage
+    StageArgs bd = s;
+    bd.row_lo = 0; bd.row_hi = G;
+    bd.row_lo2 = h->nrows - G; bd.row_hi2 = h->nrows;
+    bd.no_pdl = async ? 1 : 0;  // it follows the wait on the exchange stream's event
+    if (!e) e = launch_stage(h, bd);
+    h->launches += 2;
   }
   if (timed) cudaEventRecord(h->ev[2 * h->ev_used++ + 1], h->stream);
   if (e) return fail(h, HOM2D_ERR_CUDA, "stage kernel launch: %s", cudaGetErrorString((cudaError_t)e));

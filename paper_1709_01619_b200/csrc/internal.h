@@ -80,6 +80,9 @@ struct StageArgs {
   int row_lo, row_hi;      // this launch updates strip rows [row_lo, row_hi) (row_hi == 0: all rows);
                           // it may read rows row_lo-G .. row_hi+G-1 (ghost rows outside the strip)
   int rows;                // marching kernels: element rows per CTA (set by the launcher)
+  int row_lo2, row_hi2;    // optional second row band (row_hi2 > row_lo2): the strip's two boundary
+                           // bands of the multi-GPU path in one launch
+  int nb1;                 // row blocks of the first band (set by the launcher)
 };
 
 // ring-stage stride of the marching HO kernels (doubles): the 128-B-swizzled P3
@@ -93,7 +96,13 @@ struct StageArgs {
 // normalise the launch's row range; returns its row count
 inline int row_range(StageArgs& a) {
   if (a.row_hi <= 0) { a.row_lo = 0; a.row_hi = a.nrows; }
-  return a.row_hi - a.row_lo;
+  if (a.row_hi2 < a.row_lo2) a.row_hi2 = a.row_lo2;
+  return (a.row_hi - a.row_lo) + (a.row_hi2 - a.row_lo2);
+}
+// grid rows of a marching launch over the band(s) at `rows` rows per CTA (sets a.nb1)
+inline int band_blocks(StageArgs& a) {
+  a.nb1 = (a.row_hi - a.row_lo + a.rows - 1) / a.rows;
+  return a.nb1 + (a.row_hi2 - a.row_lo2 + a.rows - 1) / a.rows;
 }
 
 // rows per CTA for a marching kernel: enough CTAs to fill the GPU (ctas_per_sm
