@@ -718,6 +718,10 @@ static int launch_l(const StageArgs& a, cudaStream_t s) {
 }
 
 int launch_gl_stage(int method, int k, const StageArgs& a, cudaStream_t s) {
+  if (k == 1) {  // P1: the element-per-lane warp kernel where it applies (p1_stage.cu)
+    const int e = launch_p1_stage(method, a, s);
+    if (e >= 0) return e;
+  }
   if (method == LM_DG) {
     switch (k) {
       case 1: return launch_l<LM_DG, 1>(a, s);

@@ -759,6 +759,10 @@ static int launch_g(const StageArgs& a, cudaStream_t s) {
 }
 
 int launch_gll_stage(int method, int k, const StageArgs& a, cudaStream_t s) {
+  if (k == 1) {  // P1: the element-per-lane warp kernel where it applies (p1_stage.cu)
+    const int e = launch_p1_stage(method, a, s);
+    if (e >= 0) return e;
+  }
   if (method == GM_CPR) {
     switch (k) {
       case 1: return launch_g<GM_CPR, 1>(a, s);

@@ -119,7 +119,10 @@ bool make_map(CUtensorMap* m, const double* base, long long nelem, long long cs,
 int launch_gl_stage(int method, int k, const StageArgs& a, cudaStream_t s);   // DG, SD (marching)
 int launch_gll_stage(int method, int k, const StageArgs& a, cudaStream_t s);  // CPR, NDG
 int launch_fv_stage(int k, const StageArgs& a, cudaStream_t s);
-int launch_dgoi_stage(int k, const StageArgs& a, cudaStream_t s);  // DG, (k+2)-point over-integration (f3)
+int launch_dgoi_stage(int k, const StageArgs& a, cudaStream_t s);
+// P1 element-per-lane kernel (CPR, NDG, DG, SD); -1 if it does not apply (layout, variant)
+int launch_p1_stage(int method, const StageArgs& a, cudaStream_t s);
+int march_rows_waves(int nrows, int strips, int rb_max, int ctas_per_sm);  // DG, (k+2)-point over-integration (f3)
 
 struct AuxArgs {
   int method, k, nx, nrows, row0, ny_global;
