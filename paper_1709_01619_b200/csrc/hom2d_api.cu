@@ -10,6 +10,7 @@
 #include <vector>
 
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include "../../include/hom2d.h"
 #include "internal.h"
@@ -58,6 +59,13 @@ struct hom2d {
   std::vector<cudaEvent_t> ev;             // stage-kernel timing: pairs (start, stop)
   int ev_used = 0;
   char msg[512] = {0};
+};
+
+// NVTX ranges (host timeline: hom2d_step / stage / exchange / limiter / error
+// query; visible to nsys / ncu --nvtx, no cost without a tool attached)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
 };
 
 namespace {
@@ -224,6 +232,7 @@ hom2d_status exchange(hom2d* h, const double* X, long long comp_stride, long lon
     return HOM2D_OK;
   }
   if (!h->comm) return fail(h, HOM2D_ERR_STATE, "strip-only handle (created without an NCCL id)");
+  NvtxRange nv("hom2d halo exchange");
   const hom2d_strip_plan_t P = plan_of(h->cfg, h->rank, R);
   const long long cnt = (long long)G * row_vals;
   NC(h, ncclGroupStart());
@@ -260,6 +269,7 @@ int launch_stage(hom2d* h, const StageArgs& s) {
 // launch split, so the result is bitwise the single-launch one.
 hom2d_status run_stage(hom2d* h, const double* q, const double* q0, double* out, double a0, double a1, double b,
                        const double* dt, unsigned long long* lam, unsigned long long* bad, double* qbar = nullptr) {
+  NvtxRange nv("hom2d stage");
   StageArgs s{};
   const long long row_vals = (long long)h->cfg.nx * h->np;
   const int G = h->G;
@@ -315,6 +325,7 @@ hom2d_status run_stage(hom2d* h, const double* q, const double* q0, double* out,
 // already wrote them, avg_done), (exchange average rows), detect + limit.
 // dt != nullptr: skipped on the device when the step was clipped out (*dt == 0).
 hom2d_status run_limiter(hom2d* h, double* X, const double* dt = nullptr, bool avg_done = false) {
+  NvtxRange nv("hom2d limiter");
   AuxArgs A = aux(h);
   A.dt = dt;
   if (!avg_done) {
@@ -640,6 +651,7 @@ hom2d_status graph_steps(hom2d* h, int n) {
 
 extern "C" hom2d_status hom2d_step(hom2d* h, int32_t max_steps, double t_end, double* t_out, int64_t* steps_out) {
   GUARD(h);
+  NvtxRange nv("hom2d_step");
   if (max_steps < 0) return fail(h, HOM2D_ERR_ARG, "max_steps < 0");
   // graphs: single GPU (NCCL calls stay eagerly enqueued), no per-stage timing events
   const bool graphs = !h->graph_off && !h->comm && !h->self_x && h->ev.empty();
@@ -702,6 +714,7 @@ extern "C" {
 
 hom2d_status hom2d_error(hom2d* h, int32_t case_id, int32_t var, double* l1, double* l2, double* linf) {
   GUARD(h);
+  NvtxRange nv("hom2d_error");
   if (case_id != HOM2D_CASE_VORTEX) return fail(h, HOM2D_ERR_ARG, "error: exact solution only for the vortex");
   if (var < 0 || var > 3) return fail(h, HOM2D_ERR_ARG, "error: var must be 0..3");
   int nb;
