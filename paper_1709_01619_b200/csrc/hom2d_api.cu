@@ -668,6 +668,11 @@ extern "C" hom2d_status hom2d_step(hom2d* h, int32_t max_steps, double t_end, do
     if (std::isfinite(t_end) && h->t_host[1] > 0.0) {
       const double est = std::ceil((t_end - h->t_host[0]) / h->t_host[1]) + 1.0;
       if (est < batch) batch = est < 1.0 ? 1 : (int)est;
+    } else if (std::isfinite(t_end)) {
+      // no dt yet (fresh handle): one step first, so the next batch can be sized
+      // from it -- otherwise a short run to t_end launches up to 63 clipped-out
+      // (no-op) steps, ~10 us each on the paper's grids
+      batch = 1;
     }
     // graphs pay for their capture only on long runs: 64-step batches once the
     // handle has marched graph_after steps eagerly
