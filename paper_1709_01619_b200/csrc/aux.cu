@@ -475,7 +475,9 @@ __device__ __forceinline__ bool detect_element(const AuxArgs& A, const Nodes& nd
 // field of the average; all four components rebuilt
 template <int N, bool CHAR>
 __device__ __forceinline__ void rebuild_element(const AuxArgs& A, const Nodes& nd, double* __restrict__ q,
-                                             const Nbr& nbr, double dx, double dy, long long* dec, long long* emap) {
+                                             const Nbr& nbr, double dx, double dy, long long* dec, long long* emap,
+                                             bool wantlam = false, double* lam = nullptr,
+                                             unsigned long long* bad = nullptr) {
   constexpr int NP = N * N;
   const long long ne = nbr.ne, m = nbr.m;
   const double* __restrict__ qbar = nbr.qbar;
@@ -512,6 +514,18 @@ __device__ __forceinline__ void rebuild_element(const AuxArgs& A, const Nodes& n
       for (int a = 0; a < N; ++a)
         Qc[b * N + a] = qv[c] + (0.5 * dx) * nd.xi[a] * sx[c] + (0.5 * dy) * nd.xi[b] * sy[c];
   }
+  if (wantlam) {  // the dt wave speed and non-physical check of the rebuilt points (same values)
+    const double gm1 = A.gamma - 1.0;
+    for (int b = 0; b < N; ++b)
+      for (int a = 0; a < N; ++a) {
+        double v[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) v[c] = qv[c] + (0.5 * dx) * nd.xi[a] * sx[c] + (0.5 * dy) * nd.xi[b] * sy[c];
+        const Prim w = prims(v, gm1);
+        *lam = nanmax(*lam, fmax(fabs(w.u), fabs(w.v)) + fsqrt(A.gamma * w.p * w.ri));
+        if (!admissible(v[0], w.p)) *bad = min(*bad, (unsigned long long)(m * NP + b * N + a));
+      }
+  }
 }
 
 // rows of elements per thread: the detections of a thread's LROWS elements issue
@@ -523,30 +537,56 @@ __device__ __forceinline__ void rebuild_element(const AuxArgs& A, const Nodes& n
 #define H2D_LROWS(N, CHAR) ((N) == 2 && !(CHAR) ? 4 : ((N) <= 3 ? 2 : 1))
 #endif
 
+// LamFuse (limiter runs, after stage 3): the dt wave speed and the non-physical
+// check of the LIMITED state without another pass over it -- unmarked elements
+// keep their stage-3 output, whose per-line speeds / first bad points the stage
+// kernel wrote (laml / badl, N entries per element); marked elements are
+// evaluated here at their rebuilt points; block max -> atomicMax(lam_out)
+
+
 template <int N, bool GLLP, bool ALL, bool CHAR>
 __global__ void __launch_bounds__(128, H2D_LIMIT_MINB) k_limit(const AuxArgs A, Nodes nd, double* __restrict__ q,
                                                                const double* __restrict__ qbar,
                                                                const double* qbar_lo, const double* qbar_hi,
                                                                long long gcs, int bcx, double eps, double dx,
-                                                               double dy, long long* dec, long long* emap) {
+                                                               double dy, long long* dec, long long* emap,
+                                                               const LamFuse lf) {
   constexpr int R = H2D_LROWS(N, CHAR);
+  __shared__ double sred[32];
   pdl_wait();
   pdl_launch();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= A.nx) return;
-  const bool done = A.dt && *A.dt == 0.0;  // past t_end (graph replay): no writes
-  for (int j0 = blockIdx.y * R; j0 < A.nrows; j0 += gridDim.y * R) {
-    bool trip[R];
+  const bool active = i < A.nx, fuse = lf.lam_out != nullptr;
+  const bool done = A.dt && *A.dt == 0.0;  // past t_end (graph replay): no writes (uniform)
+  double lam = 0.0;
+  unsigned long long bad = ~0ull;
+  if (active) {
+    for (int j0 = blockIdx.y * R; j0 < A.nrows; j0 += gridDim.y * R) {
+      bool trip[R];
 #pragma unroll
-    for (int r = 0; r < R; ++r)
-      trip[r] = j0 + r < A.nrows &&
-                detect_element<N, GLLP, ALL>(A, nd, q, Nbr(A, qbar, qbar_lo, qbar_hi, gcs, bcx, i, j0 + r), eps);
-    if (done) return;
+      for (int r = 0; r < R; ++r)
+        trip[r] = j0 + r < A.nrows &&
+                  detect_element<N, GLLP, ALL>(A, nd, q, Nbr(A, qbar, qbar_lo, qbar_hi, gcs, bcx, i, j0 + r), eps);
+      if (done) return;
 #pragma unroll
-    for (int r = 0; r < R; ++r)
-      if (trip[r])
-        rebuild_element<N, CHAR>(A, nd, q, Nbr(A, qbar, qbar_lo, qbar_hi, gcs, bcx, i, j0 + r), dx, dy, dec, emap);
+      for (int r = 0; r < R; ++r) {
+        if (trip[r]) {
+          rebuild_element<N, CHAR>(A, nd, q, Nbr(A, qbar, qbar_lo, qbar_hi, gcs, bcx, i, j0 + r), dx, dy, dec, emap,
+                                   fuse, &lam, &bad);
+        } else if (fuse && j0 + r < A.nrows) {
+          const long long li = ((long long)(j0 + r) * A.nx + i) * N;
+#pragma unroll
+          for (int b = 0; b < N; ++b) {
+            lam = nanmax(lam, lf.laml[li + b]);
+            bad = min(bad, lf.badl[li + b]);
+          }
+        }
+      }
+    }
   }
+  if (done || !fuse) return;  // (uniform)
+  if (lf.bad_out && bad != ~0ull) atomicMin(lf.bad_out, bad);
+  block_max_to(lam, lf.lam_out, sred);
 }
 }  // namespace
 
@@ -598,43 +638,44 @@ void launch_averages(const AuxArgs& a, const double* q, double* qbar, cudaStream
 
 template <int N, bool GLLP, bool ALL, bool CHAR>
 void launch_limit_t(const AuxArgs& a, double* q, const double* qbar, const double* qbar_lo, const double* qbar_hi,
-                    long long qbar_gcs, int bcx, double eps, long long* dec, long long* emap, cudaStream_t s) {
+                    long long qbar_gcs, int bcx, double eps, long long* dec, long long* emap, const LamFuse& lf,
+                    cudaStream_t s) {
   const int ry = (a.nrows + H2D_LROWS(N, CHAR) - 1) / H2D_LROWS(N, CHAR);
   dim3 grid((a.nx + 127) / 128, ry < 65535 ? ry : 65535);
   // element widths (Eq. (35)) in host IEEE double: bitwise the device's quotient
   const double dx = (a.xmax - a.xmin) / a.nx, dy = (a.ymax - a.ymin) / a.ny_global;
   launch_pdl(k_limit<N, GLLP, ALL, CHAR>, grid, dim3(128), 0, s, a, nodes_for(a.method, a.k), q, qbar, qbar_lo,
-             qbar_hi, qbar_gcs, bcx, eps, dx, dy, dec, emap);
+             qbar_hi, qbar_gcs, bcx, eps, dx, dy, dec, emap, lf);
 }
 
 template <int N, bool GLLP>
 void launch_limit_g(const AuxArgs& a, double* q, const double* qbar, const double* qbar_lo, const double* qbar_hi,
                     long long qbar_gcs, int bcx, double eps, int all_vars, int charact, long long* dec,
-                    long long* emap, cudaStream_t s) {
-  if (all_vars && charact) launch_limit_t<N, GLLP, true, true>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, dec, emap, s);
-  else if (all_vars) launch_limit_t<N, GLLP, true, false>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, dec, emap, s);
-  else if (charact) launch_limit_t<N, GLLP, false, true>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, dec, emap, s);
-  else launch_limit_t<N, GLLP, false, false>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, dec, emap, s);
+                    long long* emap, const LamFuse& lf, cudaStream_t s) {
+  if (all_vars && charact) launch_limit_t<N, GLLP, true, true>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, dec, emap, lf, s);
+  else if (all_vars) launch_limit_t<N, GLLP, true, false>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, dec, emap, lf, s);
+  else if (charact) launch_limit_t<N, GLLP, false, true>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, dec, emap, lf, s);
+  else launch_limit_t<N, GLLP, false, false>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, dec, emap, lf, s);
 }
 
 template <int N>
 void launch_limit_n(const AuxArgs& a, double* q, const double* qbar, const double* qbar_lo, const double* qbar_hi,
                     long long qbar_gcs, int bcx, double eps, int all_vars, int charact, long long* dec,
-                    long long* emap, cudaStream_t s) {
+                    long long* emap, const LamFuse& lf, cudaStream_t s) {
   if (a.method == 1 || a.method == 3)
-    launch_limit_g<N, true>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, all_vars, charact, dec, emap, s);
+    launch_limit_g<N, true>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, all_vars, charact, dec, emap, lf, s);
   else
-    launch_limit_g<N, false>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, all_vars, charact, dec, emap, s);
+    launch_limit_g<N, false>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, all_vars, charact, dec, emap, lf, s);
 }
 
 void launch_limit(const AuxArgs& a, double* q, const double* qbar, const double* qbar_lo, const double* qbar_hi,
                   long long qbar_gcs, int bcx, double eps, int all_vars, int charact, long long* dec,
-                  long long* emap, cudaStream_t s) {
+                  long long* emap, cudaStream_t s, const LamFuse& lf) {
   switch (a.k) {
-    case 1: return launch_limit_n<2>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, all_vars, charact, dec, emap, s);
-    case 2: return launch_limit_n<3>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, all_vars, charact, dec, emap, s);
-    case 3: return launch_limit_n<4>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, all_vars, charact, dec, emap, s);
-    default: return launch_limit_n<5>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, all_vars, charact, dec, emap, s);
+    case 1: return launch_limit_n<2>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, all_vars, charact, dec, emap, lf, s);
+    case 2: return launch_limit_n<3>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, all_vars, charact, dec, emap, lf, s);
+    case 3: return launch_limit_n<4>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, all_vars, charact, dec, emap, lf, s);
+    default: return launch_limit_n<5>(a, q, qbar, qbar_lo, qbar_hi, qbar_gcs, bcx, eps, all_vars, charact, dec, emap, lf, s);
   }
 }
 

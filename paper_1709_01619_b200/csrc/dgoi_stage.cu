@@ -250,6 +250,22 @@ __global__ void __launch_bounds__(OI_NT) dgoi_stage_kernel(const StageArgs a, co
 #pragma unroll
       for (int c = 0; c < 4; ++c) a.qbar[c * ne + m] = avg[c];
     }
+    if (a.qbar && a.laml) {  // limiter runs: the element's wave speed / first bad point (LamFuse)
+      unsigned long long bl = ~0ull;
+      double ll = 0.0;
+      for (int p = 0; p < np; ++p) {
+        double v[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) v[c] = a.out[c * a.cs + m * np + p];
+        const Prim w = prims(v, gm1);
+        ll = nanmax(ll, fmax(fabs(w.u), fabs(w.v)) + fsqrt(gam * w.p * w.ri));
+        if (!admissible(v[0], w.p)) bl = min(bl, (unsigned long long)(m * np + p));
+      }
+      for (int b = 0; b < n; ++b) {
+        a.laml[m * n + b] = b == 0 ? ll : 0.0;
+        a.badl[m * n + b] = b == 0 ? bl : ~0ull;
+      }
+    }
     if (a.bad && bidx != ~0ull) atomicMin(a.bad, bidx);
 #undef SQ
 #undef SR

@@ -620,10 +620,24 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
         for (int x = 0; x < N; ++x) {
           const double o[4] = {ov[0][x], ov[1][x], ov[2][x], ov[3][x]};
           const Prim w = prims(o, gm1);
-          lam = fmax(lam, fmax(fabs(w.u), fabs(w.v)) + fsqrt(gam * w.p * w.ri));
+          lam = nanmax(lam, fmax(fabs(w.u), fabs(w.v)) + fsqrt(gam * w.p * w.ri));
           if (!admissible(o[0], w.p)) bidx = min(bidx, (unsigned long long)(base + x));
         }
         if (a.bad && bidx != ~0ull) atomicMin(a.bad, bidx);
+      }
+      if (HAVG && a.laml) {  // limiter runs: this line's wave speed / first bad point for k_limit (LamFuse)
+        unsigned long long bidx = ~0ull;
+        double ll = 0.0;
+#pragma unroll
+        for (int x = 0; x < N; ++x) {
+          const double o[4] = {ov[0][x], ov[1][x], ov[2][x], ov[3][x]};
+          const Prim w = prims(o, gm1);
+          ll = nanmax(ll, fmax(fabs(w.u), fabs(w.v)) + fsqrt(gam * w.p * w.ri));
+          if (!admissible(o[0], w.p)) bidx = min(bidx, (unsigned long long)(base + x));
+        }
+        const long long li = (jr * a.nx + i0 + lx) * N + b;
+        a.laml[li] = ll;
+        a.badl[li] = bidx;
       }
       // a thread's line of one component is N contiguous doubles: one 32-B (P3) or
       // 16-B (P1) store per component when aligned

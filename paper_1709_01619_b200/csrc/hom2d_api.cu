@@ -49,6 +49,8 @@ struct hom2d {
   int max_part = 0;
   double* err3 = nullptr;
   double* qbar = nullptr;                  // HO limiter averages [4][nx*nrows]
+  double* laml = nullptr;                 // limiter runs: stage-3 per-line wave speeds (LamFuse)
+  unsigned long long* badl = nullptr;
   double *glo = nullptr, *ghi = nullptr;   // received ghost rows [4][G*nx*np]
   double *qblo = nullptr, *qbhi = nullptr; // received ghost average rows [4][nx]
   double* t_host = nullptr;               // pinned: [0..3] clock, [5] t_end, [6..7] bad flags
@@ -160,6 +162,11 @@ size_t carve(hom2d* h, const hom2d_config& c, int nranks, char* base) {
   double* part = cv.take<double>(3 * max_part);
   double* err3 = cv.take<double>(4);
   double* qbar = (c.method != HOM2D_FV) ? cv.take<double>(4 * (size_t)c.nx * nrows) : nullptr;
+  // limiter runs: per element line, the stage-3 wave speed / first bad point (LamFuse)
+  const bool lim = c.limiter && c.method != HOM2D_FV;
+  const size_t nl = lim ? (size_t)c.nx * nrows * (c.k + 1) : 0;
+  double* laml = lim ? cv.take<double>(nl) : nullptr;
+  auto* badl = lim ? cv.take<unsigned long long>(nl) : nullptr;
   long long* dmap = (c.record_decisions && nranks == 1) ? cv.take<long long>((size_t)c.nx * nrows) : nullptr;
   double *glo = nullptr, *ghi = nullptr, *qblo = nullptr, *qbhi = nullptr;
   if (nranks > 1 || self_exchange_env(c, nranks)) {
@@ -173,6 +180,7 @@ size_t carve(hom2d* h, const hom2d_config& c, int nranks, char* base) {
   if (h && base) {
     h->Qn = Qn; h->Q1 = Q1; h->Q2 = Q2; h->clock = clk; h->lam = lam; h->bad = bad; h->dec = dec;
     h->part = part; h->max_part = max_part; h->err3 = err3; h->qbar = qbar; h->dmap = dmap;
+    h->laml = laml; h->badl = badl;
     h->glo = glo; h->ghi = ghi; h->qblo = qblo; h->qbhi = qbhi;
   }
   return cv.off + 512;  // trailing guard
@@ -268,7 +276,8 @@ int launch_stage(hom2d* h, const StageArgs& s) {
 // ghost rows have arrived.  Per-element arithmetic does not depend on the
 // launch split, so the result is bitwise the single-launch one.
 hom2d_status run_stage(hom2d* h, const double* q, const double* q0, double* out, double a0, double a1, double b,
-                       const double* dt, unsigned long long* lam, unsigned long long* bad, double* qbar = nullptr) {
+                       const double* dt, unsigned long long* lam, unsigned long long* bad, double* qbar = nullptr,
+                       bool lamfuse = false) {
   NvtxRange nv("hom2d stage");
   StageArgs s{};
   const long long row_vals = (long long)h->cfg.nx * h->np;
@@ -296,6 +305,8 @@ hom2d_status run_stage(hom2d* h, const double* q, const double* q0, double* out,
   s.dmap = h->cfg.record_decisions ? h->dmap : nullptr;
   s.count_bot = (h->rank == 0);
   s.qbar = qbar;
+  s.laml = lamfuse ? h->laml : nullptr;
+  s.badl = lamfuse ? h->badl : nullptr;
   s.fv_unlimited = h->cfg.fv_unlimited;
   int e = 0;
   if (!split) {
@@ -324,7 +335,8 @@ hom2d_status run_stage(hom2d* h, const double* q, const double* q0, double* out,
 // HO limiter on X in place: averages (unless the stage kernel that produced X
 // already wrote them, avg_done), (exchange average rows), detect + limit.
 // dt != nullptr: skipped on the device when the step was clipped out (*dt == 0).
-hom2d_status run_limiter(hom2d* h, double* X, const double* dt = nullptr, bool avg_done = false) {
+hom2d_status run_limiter(hom2d* h, double* X, const double* dt = nullptr, bool avg_done = false,
+                         bool lamfuse = false) {
   NvtxRange nv("hom2d limiter");
   AuxArgs A = aux(h);
   A.dt = dt;
@@ -339,7 +351,8 @@ hom2d_status run_limiter(hom2d* h, double* X, const double* dt = nullptr, bool a
   if (st) return st;
   launch_limit(A, X, h->qbar, lo, hi, gcs, h->cfg.bc, h->cfg.limiter_eps, h->cfg.limiter_all_vars,
                h->cfg.limiter_characteristic, h->cfg.record_decisions ? h->dec : nullptr,
-               h->cfg.record_decisions ? h->dmap : nullptr, h->stream);
+               h->cfg.record_decisions ? h->dmap : nullptr, h->stream,
+               lamfuse ? LamFuse{h->laml, h->badl, h->lam, h->bad} : LamFuse());
   h->launches++;
   CU(h, cudaPeekAtLastError());
   return HOM2D_OK;
@@ -602,10 +615,11 @@ hom2d_status enqueue_step(hom2d* h) {
   if (!lim) {
     if ((st = run_stage(h, h->Q2, h->Qn, h->Qn, 1.0 / 3.0, 2.0 / 3.0, 2.0 / 3.0, dt, h->lam, h->bad))) return st;
   } else {
-    if ((st = run_stage(h, h->Q2, h->Qn, h->Qn, 1.0 / 3.0, 2.0 / 3.0, 2.0 / 3.0, dt, nullptr, nullptr, qb))) return st;
-    if ((st = run_limiter(h, h->Qn, dt, true))) return st;
-    launch_lambda(aux(h), h->Qn, h->lam, h->bad, h->stream);  // dt of the limited state
-    h->launches++;
+    // the dt wave speed / non-physical check of the LIMITED state: unmarked elements
+    // from the stage-3 epilogue (per line), rebuilt elements in k_limit -- no pass
+    if ((st = run_stage(h, h->Q2, h->Qn, h->Qn, 1.0 / 3.0, 2.0 / 3.0, 2.0 / 3.0, dt, nullptr, nullptr, qb, true)))
+      return st;
+    if ((st = run_limiter(h, h->Qn, dt, true, true))) return st;
   }
   return allreduce_max_lam(h);
 }

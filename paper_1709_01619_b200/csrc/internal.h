@@ -83,6 +83,8 @@ struct StageArgs {
   int row_lo2, row_hi2;    // optional second row band (row_hi2 > row_lo2): the strip's two boundary
                            // bands of the multi-GPU path in one launch
   int nb1;                 // row blocks of the first band (set by the launcher)
+  double* laml;            // optional (limiter runs, stage 3): per element line, the largest
+  unsigned long long* badl;  // max(|u|,|v|)+c of `out` and its first non-physical point (LamFuse)
 };
 
 // ring-stage stride of the marching HO kernels (doubles): the 128-B-swizzled P3
@@ -149,8 +151,20 @@ int launch_error_fv_recon(const AuxArgs& a, const double* q, const double* glo, 
                           cudaStream_t s);
 // averages Qbar[4][nx*nrows] and the detect+limit pass (HO)
 void launch_averages(const AuxArgs& a, const double* q, double* qbar, cudaStream_t s);
+// LamFuse (limiter runs, after stage 3): the dt wave speed and the non-physical
+// check of the LIMITED state without another pass over it -- unmarked elements
+// keep their stage-3 output, whose per-line speeds / first bad points the stage
+// kernel wrote (laml / badl, N entries per element); marked elements are
+// evaluated by k_limit at their rebuilt points.  lam_out == nullptr: off.
+struct LamFuse {
+  const double* laml = nullptr;
+  const unsigned long long* badl = nullptr;
+  unsigned long long* lam_out = nullptr;
+  unsigned long long* bad_out = nullptr;
+};
 void launch_limit(const AuxArgs& a, double* q, const double* qbar, const double* qbar_lo, const double* qbar_hi,
                   long long qbar_gcs, int bcx, double eps, int all_vars, int charact, long long* dec,
-                  long long* emap, cudaStream_t s);
+                  long long* emap, cudaStream_t s,
+                  const LamFuse& lf = LamFuse());
 
 }  // namespace h2d

@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(PWPC * 32, H2D_P1W_MINB) p1_warp_kernel(const 
       // GLL (CPR, NDG): the element's own points are its traces -- primitives and
       // sound speed once per point, fluxes formed where needed
       Prim wp[4];
-      double cp[4];
+      double cp[4] = {0.0, 0.0, 0.0, 0.0};
       if constexpr (GLL) {
 #pragma unroll
         for (int p = 0; p < 4; ++p) {
@@ -432,6 +432,21 @@ __global__ void __launch_bounds__(PWPC * 32, H2D_P1W_MINB) p1_warp_kernel(const 
           if (own && !admissible(v[0], w.p)) bidx = min(bidx, (unsigned long long)(m * 4 + p));
         }
         if (a.bad && bidx != ~0ull) atomicMin(a.bad, bidx);
+      }
+      if (HAVG && own && a.laml) {  // limiter runs: the element's wave speed / first bad point (LamFuse)
+        unsigned long long bidx = ~0ull;
+        double ll = 0.0;
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+          const double v[4] = {o[0][p], o[1][p], o[2][p], o[3][p]};
+          const Prim w = prims(v, gm1);
+          ll = nanmax(ll, fmax(fabs(w.u), fabs(w.v)) + fsqrt(gam * w.p * w.ri));
+          if (!admissible(v[0], w.p)) bidx = min(bidx, (unsigned long long)(m * 4 + p));
+        }
+        a.laml[m * 2] = ll;
+        a.laml[m * 2 + 1] = 0.0;
+        a.badl[m * 2] = bidx;
+        a.badl[m * 2 + 1] = ~0ull;
       }
       if (HAVG && own) {  // Alg. 9: 1/4 sum_ab w_a w_b q_ab (GLL and GL P1 weights are 1)
         const long long ne = (long long)a.nx * a.nrows;
