@@ -30,6 +30,38 @@ __device__ __forceinline__ int band_start(const StageArgs& a, int& hi) {
   return a.row_lo + by * a.rows;
 }
 
+// the stage's dt (Eq. (36) via the step's clock; see StageArgs::dtrole).  The
+// same arithmetic as k_dt: lam of the last completed step (lam[0] if that step
+// advanced, else lam[1]), dt = cfl*h / lam clipped to t_end - t.
+__device__ __forceinline__ double stage_dt(const StageArgs& a) {
+  if (!a.dt) return 1.0;
+  const bool lead = blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0;
+  if (a.dtrole == 1) {
+    const double* c = a.clk;
+    const unsigned long long lb = c[3] != 0.0 ? a.lamdt[0] : a.lamdt[1];
+    double dt = a.cflh / __longlong_as_double((long long)lb);
+    const double rem = c[4] - c[0];
+    if (!(rem > 0.0)) dt = 0.0;
+    else if (dt > rem) dt = rem;
+    if (lead) a.clk[1] = dt;
+    return dt;
+  }
+  const double dt = *a.dt;
+  if (a.dtrole == 2 && lead) {
+    double* c = a.clk;
+    if (c[3] != 0.0) a.lamdt[1] = a.lamdt[0];
+    a.lamdt[0] = 0ull;
+    if (dt != 0.0) {
+      c[0] = c[0] + dt;
+      c[2] += 1.0;
+      c[3] = 1.0;
+    } else {
+      c[3] = 0.0;
+    }
+  }
+  return dt;
+}
+
 struct Prim {
   double ri, u, v, p;  // 1/rho, velocities, pressure
 };

@@ -59,11 +59,8 @@ __global__ void __launch_bounds__(OI_NT) dgoi_stage_kernel(const StageArgs a, co
   double* const sred = oi_smem + 8 * np * OI_NT;
   pdl_wait();
   pdl_launch();
-  double dtv = 1.0;
-  if (a.dt) {
-    dtv = *a.dt;
-    if (dtv == 0.0) return;
-  }
+  const double dtv = stage_dt(a);  // (stage 1 / 2 of a fused-dt step: publishes / commits the clock)
+  if (dtv == 0.0) return;
   const int tid = threadIdx.x;
   const long long n1 = (long long)a.nx * (a.row_hi - a.row_lo);
   const long long nel = n1 + (long long)a.nx * (a.row_hi2 > a.row_lo2 ? a.row_hi2 - a.row_lo2 : 0);

@@ -67,11 +67,8 @@ __global__ void __launch_bounds__(FTX, H2D_FV_MINB) fv_stage_kernel(const StageA
   __shared__ double sred[32];
   pdl_wait();
   pdl_launch();
-  double dtv = 1.0;
-  if (a.dt) {
-    dtv = *a.dt;
-    if (dtv == 0.0) return;
-  }
+  const double dtv = stage_dt(a);  // (stage 1 / 2 of a fused-dt step: publishes / commits the clock)
+  if (dtv == 0.0) return;
   const int tid = threadIdx.x;
   int bhi;
   const int i0 = blockIdx.x * FTX, jb = band_start(a, bhi);
@@ -351,11 +348,8 @@ __global__ void __launch_bounds__(WPC * 32, H2D_FVW_MINB) fv_warp_kernel(const S
   double* const sred = fv_smem + WPC * WRING + (HQ0 ? WPC * WQ : 0);
   pdl_wait();
   pdl_launch();
-  double dtv = 1.0;
-  if (a.dt) {
-    dtv = *a.dt;
-    if (dtv == 0.0) return;
-  }
+  const double dtv = stage_dt(a);  // (stage 1 / 2 of a fused-dt step: publishes / commits the clock)
+  if (dtv == 0.0) return;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   int bhi;
   const int i0 = (blockIdx.x * WPC + wid) * WS, jb = band_start(a, bhi);

@@ -251,11 +251,9 @@ __global__ void __launch_bounds__(L<M, K>::NT, LTile<M, K>::MINB) gl_stage_kerne
   __syncthreads();
   pdl_wait();  // everything above touched only shared memory and kernel parameters
   pdl_launch();
-  double dtv = 1.0;  // (read after pdl_wait)
-  if (a.dt) {
-    dtv = *a.dt;
-    if (dtv == 0.0) return;
-  }
+  // (read after pdl_wait; stage 1 / 2 of a fused-dt step publish / commit the clock)
+  const double dtv = stage_dt(a);
+  if (dtv == 0.0) return;  // clipped-out step (t == t_end): uniform across the grid
 
   auto issue_row = [&](int Lr) {
     if (tid != 0) return;

@@ -32,6 +32,8 @@ struct hom2d {
   long long glaunch[7] = {};
   bool graph_off = false;
   long long eager_steps = 0;
+  bool dtfuse = true;                      // dt computed by stage 1 / committed by stage 2 (no k_dt)
+  int dtrole = 0;                          // role of the next run_stage (StageArgs::dtrole)
   long long graph_after = 2048;            // eager steps before batches run as graphs (their capture sits
                                            // in the device timeline: ~2 ms, repaid after ~2-4k steps;
                                            // profiles/round2_small_grids.md)
@@ -307,6 +309,10 @@ hom2d_status run_stage(hom2d* h, const double* q, const double* q0, double* out,
   s.qbar = qbar;
   s.laml = lamfuse ? h->laml : nullptr;
   s.badl = lamfuse ? h->badl : nullptr;
+  s.dtrole = dt ? h->dtrole : 0;
+  s.clk = h->clock;
+  s.lamdt = h->lam;
+  s.cflh = h->cfg.cfl * fmin((h->cfg.xmax - h->cfg.xmin) / h->cfg.nx, (h->cfg.ymax - h->cfg.ymin) / h->cfg.ny);
   s.fv_unlimited = h->cfg.fv_unlimited;
   int e = 0;
   if (!split) {
@@ -324,6 +330,7 @@ hom2d_status run_stage(hom2d* h, const double* q, const double* q0, double* out,
     bd.row_lo = 0; bd.row_hi = G;
     bd.row_lo2 = h->nrows - G; bd.row_hi2 = h->nrows;
     bd.no_pdl = async ? 1 : 0;  // it follows the wait on the exchange stream's event
+    if (bd.dtrole == 2) bd.dtrole = 0;  // the clock is committed once (by the interior launch)
     if (!e) e = launch_stage(h, bd);
     h->launches += 2;
   }
@@ -441,6 +448,8 @@ hom2d_status hom2d_create(const hom2d_config* cfg, const hom2d_dist* dist, void*
   {
     const char* ng = getenv("HOM2D_NO_GRAPH");  // A/B: eager launches instead of CUDA graphs
     h->graph_off = ng && ng[0] == '1';
+    const char* nd = getenv("HOM2D_NO_DTFUSE");  // A/B: k_dt launch instead of the fused dt
+    h->dtfuse = !(nd && nd[0] == '1');
     const char* gm = getenv("HOM2D_GRAPH_AFTER");  // A/B: eager steps before graph batches (default 2048)
     if (gm && *gm) h->graph_after = atoll(gm);
     const char* gb = getenv("HOM2D_GRAPH_MIN_BATCH");  // A/B: smallest graphed batch (default 64)
@@ -600,17 +609,24 @@ hom2d_status enqueue_step(hom2d* h) {
   const double dx = (h->cfg.xmax - h->cfg.xmin) / h->cfg.nx, dy = (h->cfg.ymax - h->cfg.ymin) / h->cfg.ny;
   const bool lim = h->cfg.limiter && h->cfg.method != HOM2D_FV;
   hom2d_status st;
-  launch_dt(h->clock, h->lam, h->cfg.cfl, fmin(dx, dy), h->stream);
-  h->launches++;
+  // dt of the step: computed by every CTA of stage 1 and committed by stage 2
+  // (StageArgs::dtrole; no k_dt launch in the chain), or by k_dt (HOM2D_NO_DTFUSE=1)
+  if (!h->dtfuse) {
+    launch_dt(h->clock, h->lam, h->cfg.cfl, fmin(dx, dy), h->stream);
+    h->launches++;
+  }
   const double* dt = h->clock + 1;
   // limiter runs: the stage kernels also write the element averages of their output;
   // limiter_per_step (f3): only after stage 3
   const bool lim12 = lim && !h->cfg.limiter_per_step;
   double* qb = lim ? h->qbar : nullptr;
   double* qb12 = lim12 ? h->qbar : nullptr;
+  h->dtrole = h->dtfuse ? 1 : 0;
   if ((st = run_stage(h, h->Qn, nullptr, h->Q1, 0.0, 1.0, 1.0, dt, nullptr, nullptr, qb12))) return st;
+  h->dtrole = h->dtfuse ? 2 : 0;
   if (lim12 && (st = run_limiter(h, h->Q1, dt, true))) return st;
   if ((st = run_stage(h, h->Q1, h->Qn, h->Q2, 0.75, 0.25, 0.25, dt, nullptr, nullptr, qb12))) return st;
+  h->dtrole = 0;
   if (lim12 && (st = run_limiter(h, h->Q2, dt, true))) return st;
   if (!lim) {
     if ((st = run_stage(h, h->Q2, h->Qn, h->Qn, 1.0 / 3.0, 2.0 / 3.0, 2.0 / 3.0, dt, h->lam, h->bad))) return st;

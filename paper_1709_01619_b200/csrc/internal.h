@@ -85,6 +85,13 @@ struct StageArgs {
   int nb1;                 // row blocks of the first band (set by the launcher)
   double* laml;            // optional (limiter runs, stage 3): per element line, the largest
   unsigned long long* badl;  // max(|u|,|v|)+c of `out` and its first non-physical point (LamFuse)
+  // dt of the step without a k_dt launch (dtrole 1: stage 1 computes dt = cflh / lam from the
+  // clock and the wave speed, thread (0,0,0) publishes it to clk[1]; dtrole 2: stage 2 reads it
+  // and thread (0,0,0) commits the clock {t += dt, steps++, stepped} and recycles lam)
+  int dtrole;
+  double* clk;
+  unsigned long long* lamdt;
+  double cflh;
 };
 
 // ring-stage stride of the marching HO kernels (doubles): the 128-B-swizzled P3

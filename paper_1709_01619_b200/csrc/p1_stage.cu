@@ -91,11 +91,8 @@ __global__ void __launch_bounds__(PWPC * 32, H2D_P1W_MINB) p1_warp_kernel(const 
   double* const sred = p1_smem_ + PWPC * PRING + (HQ0 ? PWPC * PQR : 0);
   pdl_wait();
   pdl_launch();
-  double dtv = 1.0;
-  if (a.dt) {
-    dtv = *a.dt;
-    if (dtv == 0.0) return;
-  }
+  const double dtv = stage_dt(a);  // (stage 1 / 2 of a fused-dt step: publishes / commits the clock)
+  if (dtv == 0.0) return;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int i0 = (blockIdx.x * PWPC + wid) * PWS;
   int bhi;

@@ -178,3 +178,27 @@ def test_dg_overintegration_self_exchange_bitwise(orc, P, monkeypatch):
         s.close()
     np.testing.assert_array_equal(outs[0], outs[1])
     np.testing.assert_array_equal(outs[0], outs[2])
+
+
+@pytest.mark.parametrize("method,k,limiter,sx", [("cpr", 3, 0, "0"), ("fv", 2, 0, "0"), ("dg", 1, 1, "0"),
+                                                 ("sd", 2, 0, "1"), ("cpr", 1, 1, "2"), ("fv", 1, 0, "1")])
+def test_fused_dt_bitwise_equals_kdt(orc, P, monkeypatch, method, k, limiter, sx):
+    """The step's dt computed by every CTA of stage 1 and committed by stage 2
+    (no k_dt launch) gives bitwise the state, t and step count of the k_dt chain
+    (HOM2D_NO_DTFUSE=1) -- over a t_end-clipped run, with the limiter, and on the
+    split (interior + boundary-band) multi-GPU stage path (HOM2D_SELF_EXCHANGE)."""
+    monkeypatch.setenv("HOM2D_SELF_EXCHANGE", sx)
+    box, bc, case, cfl = ((-1.0, 1.0, -1.0, 1.0), 1, P.SHOCK, 0.2) if limiter else ((-5.0, 5.0, -5.0, 5.0), 0,
+                                                                                   P.VORTEX, 0.08)
+    out = []
+    for nofuse in ("0", "1"):
+        monkeypatch.setenv("HOM2D_NO_DTFUSE", nofuse)
+        s = P.Solver(P.make_config(24, 18, method=method, k=k, bc=bc, box=box, cfl=cfl, limiter=limiter))
+        s.init_case(case)
+        t1, n1 = s.step(37)
+        t2, n2 = s.step(10 ** 6, t1 + 0.05)  # clipped at t_end
+        out.append((s.get_state(), t1, n1, t2, n2))
+        s.close()
+    (qa, *ra), (qb, *rb) = out
+    np.testing.assert_array_equal(qa, qb)
+    assert ra == rb
