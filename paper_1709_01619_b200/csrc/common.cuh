@@ -38,9 +38,12 @@ __device__ __forceinline__ double stage_dt(const StageArgs& a) {
   const bool lead = blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0;
   if (a.dtrole == 1) {
     const double* c = a.clk;
-    const unsigned long long lb = c[3] != 0.0 ? a.lamdt[0] : a.lamdt[1];
+    // five independent loads (one L2 round trip, not a dependent chain)
+    const unsigned long long l0 = a.lamdt[0], l1 = a.lamdt[1];
+    const double c0 = c[0], c3 = c[3], c4 = c[4];
+    const unsigned long long lb = c3 != 0.0 ? l0 : l1;
     double dt = a.cflh / __longlong_as_double((long long)lb);
-    const double rem = c[4] - c[0];
+    const double rem = c4 - c0;
     if (!(rem > 0.0)) dt = 0.0;
     else if (dt > rem) dt = rem;
     if (lead) a.clk[1] = dt;

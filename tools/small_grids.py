@@ -5,10 +5,11 @@ hom2d_step against the launch floor.
     python tools/small_grids.py [--out gpurun_out/small_grids.json]
 
 For each (method, k): the per-step time on a 2x2-element grid (the kernels do
-next to no work: the floor of the step's launch chain -- k_dt + 3 stage kernels
-with programmatic dependent launch), on the paper's grids (20^2, P3/P4 also
+next to no work: the floor of the step's launch chain -- 3 stage kernels with
+programmatic dependent launch, the dt fused into stages 1-2; HOM2D_NO_DTFUSE=1
+for the k_dt chain), on the paper's grids (20^2, P3/P4 also
 8^2; FV NDoF-matched) and on 80^2, each in three launch modes: eager launches,
-CUDA graphs after 256 eager steps (the default), graphs from the first step
+CUDA graphs after 2048 eager steps (the default), graphs from the first step
 (HOM2D_GRAPH_AFTER=0, HOM2D_GRAPH_MIN_BATCH=1).  Runs of 512 steps after a
 64-step warm-up; CUDA events on the library's stream.  Profiling aid only.
 """
