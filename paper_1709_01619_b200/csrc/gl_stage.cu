@@ -59,6 +59,16 @@ enum { LM_DG = 2, LM_SD = 4 };
 #ifndef H2D_WSQRT
 #define H2D_WSQRT fsqrt_ws  // Rusanov dissipation speed (common.cuh; A/B: fsqrt)
 #endif
+// y work by column: the thread of line b also owns column b of its element for
+// the y direction (the column's fluxes, its S / N face fluxes -- the S one
+// carried in registers from the row below -- and the y derivative at the
+// column's points) and hands the y part of the residual to the line owners
+// through shared memory: N points per thread cross shared memory instead of
+// the N^2 column fluxes (DG g, SD interior flux points) and the 2N face fluxes
+// every line thread read (0: the round-2 layout, A/B)
+#ifndef H2D_GL_COLY
+#define H2D_GL_COLY 1
+#endif
 template <int M, int K> struct LTile {
   static constexpr int TX = K == 1 ? 64 : K == 2 ? (M == LM_DG ? H2D_DG_TX2 : H2D_LTX2) : (M == LM_DG ? H2D_DG_TX : H2D_SD_TX),
                        RB = 64;
@@ -124,6 +134,17 @@ struct L {
   static constexpr int STGA = H2D_STGA(STG);  // stage stride (see H2D_STGA)
   static constexpr int OR_ = 0;
   static constexpr int OFW = OR_ + NSTG * STGA;            // W-face fluxes [TX+1][N][4]
+#if H2D_GL_COLY
+  // y part of the residual of every point, written by the thread that owns the
+  // point's column, read by the one that owns its line: element lx, point
+  // (row a, column x) at lx * RES + x * RCS + a * 4.  The column stride is 2 mod
+  // 4 doubles (a column's writes by the N column threads fall into different
+  // 16-B bank groups) and RES is 8 mod 16 doubles (the two elements of a
+  // quarter warp 64 B apart)
+  static constexpr int RCS = N * 4 + 2, RES = N * RCS + ((8 - (N * RCS) % 16) + 16) % 16;
+  static constexpr int ORY = OFW + (TX + 1) * N * 4;
+  static constexpr int OT = ORY + TX * RES;
+#else
   static constexpr int OFN = OFW + (TX + 1) * N * 4;       // N-face fluxes, double-buffered [2][TX][N][4]
   static constexpr int OG = OFN + 2 * TX * N * 4;          // DG: g at points [TX][NP][4]
   // per-element strides padded to 2 mod 4 doubles: the column reads of 8
@@ -131,6 +152,7 @@ struct L {
   static constexpr int GS = NP * 4 + 2, PYS = N * (N - 1) * 4 + 2;
   static constexpr int OPY = OG + (M == LM_DG ? TX * GS : 0);        // SD: column interior fluxes [TX][N][N-1][4]
   static constexpr int OT = OPY + (M == LM_SD ? TX * PYS : 0);
+#endif
   static constexpr int ORD = OT + ((LOps<K>::TOT + 1) & ~1);
   static constexpr int OB = ORD + 32;
   static constexpr int OQ0 = OB + ((NSTG + 1) & ~1);  // q^n prefetch [4][N][NT], thread-private
@@ -219,9 +241,13 @@ __global__ void __launch_bounds__(L<M, K>::NT, LTile<M, K>::MINB) gl_stage_kerne
   double* sm = reinterpret_cast<double*>(smem4);
   double* ring = sm + H::OR_;
   double* sFW = sm + H::OFW;
+#if H2D_GL_COLY
+  double* sRY = sm + H::ORY;
+#else
   double* sFN = sm + H::OFN;
   double* sG = sm + H::OG;
   double* sPY = sm + H::OPY;
+#endif
   double* sT = sm + H::OT;
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + H::OB);
   double* sQ0 = sm + H::OQ0;
@@ -371,12 +397,17 @@ __global__ void __launch_bounds__(L<M, K>::NT, LTile<M, K>::MINB) gl_stage_kerne
   const double* SI0 = tab.v + T::SI;               // flux point 0 row of sd_I (== eL)
   const double* SIN = tab.v + T::SI + N * N;       // flux point n row (== eR)
 
+#if H2D_GL_COLY
+  double FSr[4] = {0.0, 0.0, 0.0, 0.0};  // S-face flux of this thread's column (the row below's N face)
+#endif
   for (int Lr = 0; Lr <= RBv; ++Lr) {
     mbar_wait(&bar[Lr % NSTG], (Lr / NSTG) & 1);
     mbar_wait(&bar[(Lr + 1) % NSTG], ((Lr + 1) / NSTG) & 1);
     const RowView vc = view(Lr), vn = view(Lr + 1);
+#if !H2D_GL_COLY
     double* FNc = sFN + (Lr & 1) * TX * N * 4;        // N-face fluxes of this row (written now)
     double* FSc = sFN + ((Lr + 1) & 1) * TX * N * 4;  // S-face fluxes of this row (written in step Lr-1)
+#endif
     const long long jr = jb - 1 + Lr;
 
     double q[4][N];
@@ -392,6 +423,27 @@ __global__ void __launch_bounds__(L<M, K>::NT, LTile<M, K>::MINB) gl_stage_kerne
       const double* wl = (M == LM_DG) ? EL : SI0;
       const double* wr = (M == LM_DG) ? ER : SIN;
       double qd[4], qu[4];
+#if H2D_GL_COLY
+      // column b of the element, read once: its N trace here, its fluxes below
+      // (the prologue row's slot may hold no row: its values are then unused)
+      double colv[4][N];
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int l = 0; l < N; ++l) colv[c][l] = own_at(vc, c, lx + 1, l * N + b);
+      {
+        double u[4];
+        interp(vn, lx + 1, 1, b, wl, u, false);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          double s = wr[0] * colv[c][0];
+#pragma unroll
+          for (int l = 1; l < N; ++l) s = fma(wr[l], colv[c][l], s);
+          qd[c] = vc.have ? s : u[c];
+          qu[c] = vn.have ? u[c] : s;
+        }
+      }
+#else
       {
         double d[4], u[4];
         interp(vc, lx + 1, 1, b, wr, d, false);
@@ -402,6 +454,7 @@ __global__ void __launch_bounds__(L<M, K>::NT, LTile<M, K>::MINB) gl_stage_kerne
           qu[c] = vn.have ? u[c] : d[c];
         }
       }
+#endif
       if (Lr > 0) {
 #pragma unroll
         for (int c = 0; c < 4; ++c)
@@ -459,7 +512,16 @@ __global__ void __launch_bounds__(L<M, K>::NT, LTile<M, K>::MINB) gl_stage_kerne
         node_eval<0>(ql, gm1, gam, flf, sl);
         node_eval<1>(qd, gm1, gam, gd, sd);
         node_eval<1>(qu, gm1, gam, gu, su);
-        if (M == LM_DG) {  // f (registers) and g (smem, for the columns) at every point of the line
+        if (M == LM_DG) {
+#if H2D_GL_COLY  // f at every point of the line (registers); g at the column's points below
+#pragma unroll
+          for (int x = 0; x < N; ++x) {
+            double v[4] = {q[0][x], q[1][x], q[2][x], q[3][x]}, f[4];
+            flux<0>(v, prims(v, gm1), f);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) fl[c][x] = f[c];
+          }
+#else  // f (registers) and g (smem, for the columns) at every point of the line
 #pragma unroll
           for (int x = 0; x < N; ++x) {
             double v[4] = {q[0][x], q[1][x], q[2][x], q[3][x]}, f[4], g[4];
@@ -470,6 +532,7 @@ __global__ void __launch_bounds__(L<M, K>::NT, LTile<M, K>::MINB) gl_stage_kerne
             for (int c = 0; c < 4; ++c) fl[c][x] = f[c];
             st4(sG + lx * H::GS + (b * N + x) * 4, g);
           }
+#endif
         } else {  // SD: interior x flux points of the line, interior y flux points of column b
 #pragma unroll
           for (int r = 1; r < N; ++r) {
@@ -483,6 +546,7 @@ __global__ void __launch_bounds__(L<M, K>::NT, LTile<M, K>::MINB) gl_stage_kerne
             }
             flux<0>(v, prims(v, gm1), phi[r]);
           }
+#if !H2D_GL_COLY
           // column b of the element, read once for its N-1 interior flux points
           double colv[4][N];
 #pragma unroll
@@ -502,12 +566,60 @@ __global__ void __launch_bounds__(L<M, K>::NT, LTile<M, K>::MINB) gl_stage_kerne
             flux<1>(v, prims(v, gm1), g);
             st4(sPY + lx * H::PYS + (b * (N - 1) + (r - 1)) * 4, g);
           }
+#endif
         }
         double F[4], G[4];
         rus(ql, flf, sl, qw, fW, sw, F);
         rus(qd, gd, sd, qu, gu, su, G);
         st4(sFW + (lx * N + b) * 4, F);
+#if H2D_GL_COLY
+        {  // y part of the residual at the points (a, b) of column b, to their line owners
+          double gc[N + 1][4];  // DG: g at the column's points; SD: g at its interior flux points 1..N-1
+          if (M == LM_DG) {
+#pragma unroll
+            for (int l = 0; l < N; ++l) {
+              double v[4] = {colv[0][l], colv[1][l], colv[2][l], colv[3][l]};
+              flux<1>(v, prims(v, gm1), gc[l]);
+            }
+          } else {
+#pragma unroll
+            for (int r = 1; r < N; ++r) {
+              double v[4];
+#pragma unroll
+              for (int c = 0; c < 4; ++c) {
+                double sv = tab.v[T::SI + r * N] * colv[c][0];
+#pragma unroll
+                for (int l = 1; l < N; ++l) sv = fma(tab.v[T::SI + r * N + l], colv[c][l], sv);
+                v[c] = sv;
+              }
+              flux<1>(v, prims(v, gm1), gc[r]);
+            }
+          }
+#pragma unroll
+          for (int aa = 0; aa < N; ++aa) {
+            double gy[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              if (M == LM_DG) {  // sum_l (w_l/w_a) l'_a(eta_l) g_l + (l_a(-1) F^S - l_a(1) F^N) / w_a
+                double s = tab.v[T::DV + aa * N] * gc[0][c];
+#pragma unroll
+                for (int l = 1; l < N; ++l) s = fma(tab.v[T::DV + aa * N + l], gc[l][c], s);
+                gy[c] = s + tab.v[T::SL + aa] * FSr[c] - tab.v[T::SR + aa] * G[c];
+              } else {  // sum_r D_ar g_r over the flux points, the end ones the face fluxes
+                double s = tab.v[T::SD + aa * (N + 1)] * FSr[c] + tab.v[T::SD + aa * (N + 1) + N] * G[c];
+#pragma unroll
+                for (int r = 1; r < N; ++r) s += tab.v[T::SD + aa * (N + 1) + r] * gc[r][c];
+                gy[c] = s;
+              }
+            }
+            st4(sRY + lx * H::RES + b * H::RCS + aa * 4, gy);
+          }
+#pragma unroll
+          for (int c = 0; c < 4; ++c) FSr[c] = G[c];
+        }
+#else
         st4(FNc + (lx * N + b) * 4, G);
+#endif
 #pragma unroll
         for (int c = 0; c < 4; ++c) phi[0][c] = F[c];
         if (lx == TXv - 1) {  // the strip's last E face
@@ -526,7 +638,12 @@ __global__ void __launch_bounds__(L<M, K>::NT, LTile<M, K>::MINB) gl_stage_kerne
         node_eval<1>(qd, gm1, gam, gd, sd);
         node_eval<1>(qu, gm1, gam, gu, su);
         rus(qd, gd, sd, qu, gu, su, G);
+#if H2D_GL_COLY
+#pragma unroll
+        for (int c = 0; c < 4; ++c) FSr[c] = G[c];
+#else
         st4(FNc + (lx * N + b) * 4, G);
+#endif
       }
     }
     __syncthreads();
@@ -551,7 +668,31 @@ __global__ void __launch_bounds__(L<M, K>::NT, LTile<M, K>::MINB) gl_stage_kerne
 #pragma unroll
       for (int x = 0; x < N; ++x) {
         double v[4] = {q[0][x], q[1][x], q[2][x], q[3][x]};
-        double R[4], FS[4], FN[4];
+        double R[4];
+#if H2D_GL_COLY
+        double gy[4];  // y part of the residual at (b, x), from the owner of column x
+        ld4(sRY + lx * H::RES + x * H::RCS + b * 4, gy);
+        if (M == LM_DG) {
+          const double sRa = tab.v[T::SR + x], sLa = tab.v[T::SL + x];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            double fx = tab.v[T::DV + x * N] * fl[c][0];
+#pragma unroll
+            for (int l = 1; l < N; ++l) fx = fma(tab.v[T::DV + x * N + l], fl[c][l], fx);
+            fx += sLa * FW[c] - sRa * FE[c];
+            R[c] = fma(cx, fx, cy * gy[c]);  // bdt R, R = (2/dx) fx + (2/dy) gy (weak form signs)
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            double fx = tab.v[T::SD + x * (N + 1)] * phi[0][c];
+#pragma unroll
+            for (int r = 1; r <= N; ++r) fx = fma(tab.v[T::SD + x * (N + 1) + r], phi[r][c], fx);
+            R[c] = fma(-cx, fx, -cy * gy[c]);  // bdt R, R = -(2/dx) fx - (2/dy) gy
+          }
+        }
+#else
+        double FS[4], FN[4];
         ld4(FSc + (lx * N + x) * 4, FS);
         ld4(FNc + (lx * N + x) * 4, FN);
         if (M == LM_DG) {
@@ -597,6 +738,7 @@ __global__ void __launch_bounds__(L<M, K>::NT, LTile<M, K>::MINB) gl_stage_kerne
             R[c] = fma(-cx, fx, -cy * gy[c]);  // bdt R, R = -(2/dx) fx - (2/dy) gy
           }
         }
+#endif
 #pragma unroll
         for (int c = 0; c < 4; ++c) ov[c][x] = HQ0 ? fma(a.a0, q0v[c][x], fma(a.a1, v[c], R[c])) : fma(a.a1, v[c], R[c]);
       }
