@@ -43,6 +43,9 @@ namespace {
 #endif
 // A/B on 8192^2 / 4096^2 (round 1): P1 at 4 CTAs/SM (<= 128 registers; SD +7 %),
 // P2 32-element strips at 4 CTAs/SM (DG +20 %, SD +36 % over 16 at 1)
+#ifndef H2D_LMINB4
+#define H2D_LMINB4 H2D_LMINB
+#endif
 #ifndef H2D_LMINB1
 #define H2D_LMINB1 4
 #endif
@@ -72,7 +75,7 @@ enum { LM_DG = 2, LM_SD = 4 };
 template <int M, int K> struct LTile {
   static constexpr int TX = K == 1 ? 64 : K == 2 ? (M == LM_DG ? H2D_DG_TX2 : H2D_LTX2) : (M == LM_DG ? H2D_DG_TX : H2D_SD_TX),
                        RB = 64;
-  static constexpr int MINB = K == 1 ? H2D_LMINB1 : K == 2 ? H2D_LMINB2 : H2D_LMINB;
+  static constexpr int MINB = K == 1 ? H2D_LMINB1 : K == 2 ? H2D_LMINB2 : K == 3 ? H2D_LMINB : H2D_LMINB4;
 };
 
 constexpr int NSTG = 3;

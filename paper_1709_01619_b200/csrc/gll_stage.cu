@@ -80,6 +80,18 @@ enum { GM_CPR = 1, GM_NDG = 3 };
 #define H2D_NDG_TX4 H2D_TX4
 #endif
 constexpr int NSTG = 3;  // ring depth (rows): current, N neighbour, one in flight
+// NDG: y work by column (as gl_stage.cu's H2D_GL_COLY): the thread of line b
+// also owns column b of its element for the y direction -- g at the column's
+// points, D g, its S / N jumps (the S one carried in registers from the row
+// below) and their lift -- and hands the N points' y residual to the line
+// owners (0: the round-2 layout, A/B; A/B on 4096^2 NDG P2 / P3 / P4: 63.3 /
+// 60.7 / 59.6 -> 67.2 / 69.7 / 60.8 % of HBM).  CPR keeps the line layout: its
+// column owner would need the column points' primitives for B(q) (one more
+// reciprocal chain per point) and the larger buffer costs it a CTA per SM
+// (CPR P2 / P3 / P4: 71 / 68 / 63 -> 63 / 63 / 56 %)
+#ifndef H2D_GLL_COLY
+#define H2D_GLL_COLY 1
+#endif
 
 struct GMaps {   // P3: 3-D tensor maps {16 points, TX+2 elements, 4 components}
   CUtensorMap q, lo, hi;
@@ -109,16 +121,24 @@ struct G {
   static constexpr int STGA = H2D_STGA(STG);          // stage stride (see H2D_STGA)
   static constexpr int OR_ = 0;
   static constexpr int OFW = OR_ + NSTG * STGA;       // W-face fluxes [TX+1][N][4]
+  static constexpr bool CY = H2D_GLL_COLY && M == GM_NDG;  // y work by column (NDG)
   static constexpr int OJN = OFW + (TX + 1) * N * 4;  // N jumps of the current row [TX][N][4]
-  static constexpr int OJS = OJN + TX * N * 4;        // S jumps, double-buffered [2][TX][N][4]
-  static constexpr int OG = OJS + 2 * TX * N * 4;     // NDG: g at every point [TX][NP][4]
+  static constexpr int OJS = OJN + (CY ? 0 : TX * N * 4);      // S jumps, double-buffered [2][TX][N][4]
+  static constexpr int OG = OJS + (CY ? 0 : 2 * TX * N * 4);   // NDG (!CY): g at every point [TX][NP][4]
   static constexpr int GS = NP * 4 + 2;  // padded element stride (conflict-free column reads)
-  static constexpr int OT = OG + (M == GM_NDG ? TX * GS : 0);
+  // CY: y part of the residual of every point (written by the point's column
+  // owner): element lx, point (row a, column x) at lx * RES + x * RCS + a * 4
+  // (strides as gl_stage.cu: conflict-free column writes, 2-way line reads)
+  // (odd N: no element padding -- the lane groups of an element do not align
+  // with quarter warps anyway, and it keeps NDG P2 / P4 at 4 CTAs/SM)
+  static constexpr int RCS = N * 4 + 2, RES = N % 2 ? N * RCS : N * RCS + ((8 - (N * RCS) % 16) + 16) % 16;
+  static constexpr int ORY = OG + (M == GM_NDG && !CY ? TX * GS : 0);
+  static constexpr int OT = ORY + (CY ? TX * RES : 0);
   static constexpr int ORD = OT + ((N * N + 3 * N + 1) & ~1);
   static constexpr int OB = ORD + 32;                 // mbarriers (as doubles)
   static constexpr int LP = (N + 1) & ~1;             // q^n line slot (16-B multiple)
-  static constexpr int OQ0 = OB + ((NSTG + 1) & ~1);  // q^n prefetch [4][NT][LP], thread-private
-  static constexpr int TOTAL = OQ0 + 4 * NT * LP;
+  static constexpr int OQ0 = OB + ((NSTG + 1) & ~1);  // q^n prefetch [4][N][NT], thread-private
+  static constexpr int TOTAL = OQ0 + 4 * N * NT;
   static_assert(OQ0 % 2 == 0, "16-B cp.async slots");
   static constexpr size_t SMEM = TOTAL * sizeof(double);
 };
@@ -233,6 +253,7 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
   double* sm = reinterpret_cast<double*>(smem4);
   double* ring = sm + H::OR_;
   double* sFW = sm + H::OFW;
+  double* sRY = sm + H::ORY;
   double* sJN = sm + H::OJN;
   double* sJS = sm + H::OJS;
   double* sG = sm + H::OG;
@@ -373,12 +394,13 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
   if (HQ0 && own)  // q^n of the first own row (step L = 1)
     q0_prefetch<N, NT, H::LP>(sQ0, a.q0, a.cs, ((long long)jb * a.nx + i0 + lx) * NP + b * N, tid, vec);
 
-  const double* D = sT;
-  const double gLb = sT[N * N + b], gRb = sT[N * N + N + b];
+  [[maybe_unused]] const double* D = sT;
+  [[maybe_unused]] const double gLb = sT[N * N + b], gRb = sT[N * N + N + b];
   double lam = 0.0;
   const double bdt = a.bcoef * dtv;
   const double cx = -bdt * a.rdx2, cy = -bdt * a.rdy2;
 
+  double JSr[4] = {0.0, 0.0, 0.0, 0.0};  // CY: S jump of this thread's column (from the row below's N face)
   for (int L = 0; L <= RBv; ++L) {
     mbar_wait(&bar[L % NSTG], (L / NSTG) & 1);
     mbar_wait(&bar[(L + 1) % NSTG], ((L + 1) / NSTG) & 1);
@@ -398,9 +420,17 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
     // element above is carried to the next step); transmissive ends by selects.
     if (own) {
       double qd[4], qu[4];  // column b: own top point, next row's bottom point
+      double colv[4][N];  // CY: column b of the element (the prologue row's slot may hold no row: then unused)
+      if constexpr (H::CY) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+#pragma unroll
+          for (int l = 0; l < N; ++l) colv[c][l] = own_at(vc, c, lx + 1, l * N + b);
+      }
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        const double d = own_at(vc, c, lx + 1, (N - 1) * N + b), u = own_at(vn, c, lx + 1, b);
+        const double d = H::CY ? colv[c][N - 1] : own_at(vc, c, lx + 1, (N - 1) * N + b),
+                     u = own_at(vn, c, lx + 1, b);
         qd[c] = vc.have ? d : u;
         qu[c] = vn.have ? u : d;
       }
@@ -453,10 +483,34 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
         for (int c = 0; c < 4; ++c) jW[c] = F[c] - fW[c];
 #pragma unroll
         for (int c = 0; c < 4; ++c) j[c] = Gf[c] - gd[c];
-        st4(sJN + (lx * N + b) * 4, j);
+        if constexpr (H::CY) {  // y part of the residual at the points (a, b) of column b, to their line owners
+          double gc[N][4];  // g at the column's points
 #pragma unroll
-        for (int c = 0; c < 4; ++c) j[c] = Gf[c] - gu[c];
-        st4(jSn + (lx * N + b) * 4, j);
+          for (int l = 0; l < N; ++l) {
+            double v[4] = {colv[0][l], colv[1][l], colv[2][l], colv[3][l]};
+            flux<1>(v, prims(v, gm1), gc[l]);
+          }
+#pragma unroll
+          for (int aa = 0; aa < N; ++aa) {  // D g + the lift of the S / N jumps at (a, b)
+            const double gLa = tab.v[N * N + aa], gRa = tab.v[N * N + N + aa];
+            double gy[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              double sv = tab.v[aa * N] * gc[0][c];
+#pragma unroll
+              for (int l = 1; l < N; ++l) sv = fma(tab.v[aa * N + l], gc[l][c], sv);
+              gy[c] = sv + gLa * JSr[c] + gRa * j[c];
+            }
+            st4(sRY + lx * H::RES + b * H::RCS + aa * 4, gy);
+          }
+#pragma unroll
+          for (int c = 0; c < 4; ++c) JSr[c] = Gf[c] - gu[c];
+        } else {
+          st4(sJN + (lx * N + b) * 4, j);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) j[c] = Gf[c] - gu[c];
+          st4(jSn + (lx * N + b) * 4, j);
+        }
         if (lx == TXv - 1) {  // the strip's last E face
           if (mirE) {
             rus(qe, fE, se, qe, fE, se, F);
@@ -472,13 +526,16 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
         if (M == GM_NDG) {  // eta operands: g at the points of the line (smem); f kept in registers
 #pragma unroll
           for (int x = 0; x < N; ++x) {
-            double v[4] = {q[0][x], q[1][x], q[2][x], q[3][x]}, f[4], g[4];
+            double v[4] = {q[0][x], q[1][x], q[2][x], q[3][x]}, f[4];
             const Prim w = (x == 0) ? pW : (x == N - 1) ? pE : prims(v, gm1);
             flux<0>(v, w, f);
-            flux<1>(v, w, g);
 #pragma unroll
             for (int c = 0; c < 4; ++c) fxl[c][x] = f[c];
-            st4(sG + lx * H::GS + (b * N + x) * 4, g);
+            if constexpr (!H::CY) {
+              double g[4];
+              flux<1>(v, w, g);
+              st4(sG + lx * H::GS + (b * N + x) * 4, g);
+            }
           }
         }
       } else {  // prologue row (below the march): only its N face, as the first row's S face
@@ -488,7 +545,12 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
         rus(qd, gd, sd, qu, gu, su, Gf);
 #pragma unroll
         for (int c = 0; c < 4; ++c) j[c] = Gf[c] - gu[c];
-        st4(jSn + (lx * N + b) * 4, j);
+        if constexpr (H::CY) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) JSr[c] = j[c];
+        } else {
+          st4(jSn + (lx * N + b) * 4, j);
+        }
       }
     }
     __syncthreads();
@@ -506,7 +568,7 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
       // CPR P3: eta-derivatives of all points of the line at once, two points per
       // 16-B swizzled chunk (half the shared-memory loads of a per-point loop)
       double dyall[N][4];
-      if constexpr (M == GM_CPR && H::SWZ) {
+      if constexpr (M == GM_CPR && H::SWZ && !H::CY) {
         // (sums start from their first product: no zero-initialised accumulators)
 #pragma unroll
         for (int l = 0; l < N; ++l) {
@@ -530,7 +592,7 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
       // CPR P1 (1-D path, aligned): eta-derivatives of both points of the line
       // from the element's rows as 16-B pairs (same operation order as below)
       double dy2[N][4];
-      if constexpr (M == GM_CPR && N == 2 && !H::SWZ) {
+      if constexpr (M == GM_CPR && N == 2 && !H::SWZ && !H::CY) {
         if (vc.v2) {
 #pragma unroll
           for (int l = 0; l < N; ++l) {
@@ -552,6 +614,21 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
 #pragma unroll
       for (int x = 0; x < N; ++x) {
         double v[4] = {q[0][x], q[1][x], q[2][x], q[3][x]};
+        if constexpr (H::CY) {  // NDG: D[F] + the y part from the owner of column x
+          double gy[4];
+          ld4(sRY + lx * H::RES + x * H::RCS + b * 4, gy);
+          const double gLa = tab.v[N * N + x], gRa = tab.v[N * N + N + x];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            double sv = tab.v[x * N] * fxl[c][0];
+#pragma unroll
+            for (int l = 1; l < N; ++l) sv = fma(tab.v[x * N + l], fxl[c][l], sv);
+            const double fx = sv + gLa * jW[c] + gRa * jE[c];
+            // out = a0 q^n + a1 q + bdt R,  R = -(2/dx) fx - (2/dy) gy  (metric folded into cx, cy)
+            const double rk = fma(a.a1, v[c], fma(cx, fx, cy * gy[c]));
+            ov[c][x] = HQ0 ? fma(a.a0, q0v[c][x], rk) : rk;
+          }
+        } else {
         double Fx[4], Gy[4], dy[4];
 #pragma unroll
         for (int l = 0; l < N; ++l) {  // column x of the element (broadcast over its lines)
@@ -610,6 +687,7 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
           // out = a0 q^n + a1 q + bdt R,  R = -(2/dx) fx - (2/dy) gy  (metric folded into cx, cy)
           const double rk = fma(a.a1, v[c], fma(cx, fx, cy * gy));
           ov[c][x] = HQ0 ? fma(a.a0, q0v[c][x], rk) : rk;
+        }
         }
       }
       if (HLAM) {  // dt wave speed and non-physical check share one reciprocal (straight-line)
