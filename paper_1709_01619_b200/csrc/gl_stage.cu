@@ -32,11 +32,12 @@ namespace {
 // smem, so narrower strips keep 2+ CTAs per SM (A/B on 4096^2: DG 16 > 32 by
 // 37 % at P3, 3-6 % at P2/P4; SD 32 > 16 by 10 % at P3, 16 > 32 by 13 % at P4)
 #ifndef H2D_DG_TX
-#define H2D_DG_TX (K == 3 ? 14 : 11)  // P3: 14-element strips = 16-slot TMA rows, 4 CTAs/SM (+7.5 % over 16);
-                                     // P4: 11 (55 threads; 4 CTAs/SM with the 16-B stage stride: +2.7 % over 12)
+#define H2D_DG_TX (K == 3 ? 14 : 12)  // P3: 14-element strips = 16-slot TMA rows, 4 CTAs/SM (+7.5 % over 16);
+                                     // P4: 12 (60 threads) at 4 CTAs/SM since the by-column layout and the
+                                     // 5-entry table copy shrank shared memory (+3.3 % over 11)
 #endif
 #ifndef H2D_SD_TX
-#define H2D_SD_TX (K == 3 ? 14 : 11)  // A/B: P3 14 +2.5 % over 32; P4 11 +4.9 % over 12 (4 vs 3 CTAs/SM)
+#define H2D_SD_TX (K == 3 ? 14 : 12)  // A/B: P3 14 +2.5 % over 32; P4 12 (4 CTAs/SM, +4.2 % over 11)
 #endif
 #ifndef H2D_LMINB
 #define H2D_LMINB 1
@@ -71,6 +72,9 @@ enum { LM_DG = 2, LM_SD = 4 };
 // every line thread read (0: the round-2 layout, A/B)
 #ifndef H2D_GL_COLY
 #define H2D_GL_COLY 1
+#endif
+#ifndef H2D_GL_RESPAD
+#define H2D_GL_RESPAD 0
 #endif
 template <int M, int K> struct LTile {
   static constexpr int TX = K == 1 ? 64 : K == 2 ? (M == LM_DG ? H2D_DG_TX2 : H2D_LTX2) : (M == LM_DG ? H2D_DG_TX : H2D_SD_TX),
@@ -143,8 +147,10 @@ struct L {
   // (row a, column x) at lx * RES + x * RCS + a * 4.  The column stride is 2 mod
   // 4 doubles (a column's writes by the N column threads fall into different
   // 16-B bank groups) and RES is 8 mod 16 doubles (the two elements of a
-  // quarter warp 64 B apart)
-  static constexpr int RCS = N * 4 + 2, RES = N * RCS + ((8 - (N * RCS) % 16) + 16) % 16;
+  // quarter warp 64 B apart; odd N: no element padding -- the lane groups of
+  // an element do not align with quarter warps anyway)
+  static constexpr int RCS = N * 4 + 2,
+                       RES = (N % 2 && !H2D_GL_RESPAD) ? N * RCS : N * RCS + ((8 - (N * RCS) % 16) + 16) % 16;
   static constexpr int ORY = OFW + (TX + 1) * N * 4;
   static constexpr int OT = ORY + TX * RES;
 #else
@@ -156,7 +162,10 @@ struct L {
   static constexpr int OPY = OG + (M == LM_DG ? TX * GS : 0);        // SD: column interior fluxes [TX][N][N-1][4]
   static constexpr int OT = OPY + (M == LM_SD ? TX * PYS : 0);
 #endif
-  static constexpr int ORD = OT + ((LOps<K>::TOT + 1) & ~1);
+  // operator table copy for run-time (line-dependent) indices: by column only
+  // the weights of the element averages are indexed by the line
+  static constexpr int TOFF = H2D_GL_COLY ? LOps<K>::W : 0, TSZ = H2D_GL_COLY ? N : LOps<K>::TOT;
+  static constexpr int ORD = OT + ((TSZ + 1) & ~1);
   static constexpr int OB = ORD + 32;
   static constexpr int OQ0 = OB + ((NSTG + 1) & ~1);  // q^n prefetch [4][N][NT], thread-private
   static constexpr int TOTAL = OQ0 + 4 * N * NT;
@@ -272,7 +281,7 @@ __global__ void __launch_bounds__(L<M, K>::NT, LTile<M, K>::MINB) gl_stage_kerne
   const int ie = i0 + TXv < a.nx ? i0 + TXv : 0;
   const int nload = RBv + 2;
 
-  for (int i = tid; i < T::TOT; i += NT) sT[i] = tab.v[i];
+  for (int i = tid; i < H::TSZ; i += NT) sT[i] = tab.v[H::TOFF + i];
   if (tid == 0) {
     for (int s = 0; s < NSTG; ++s) mbar_init(&bar[s], 1);
     mbar_fence_init();
@@ -795,7 +804,7 @@ __global__ void __launch_bounds__(L<M, K>::NT, LTile<M, K>::MINB) gl_stage_kerne
           double sx = 0.0;
 #pragma unroll
           for (int x = 0; x < N; ++x) sx += tab.v[T::W + x] * ov[c][x];
-          lpart[c] = sT[T::W + b] * sx;
+          lpart[c] = sT[T::W - H::TOFF + b] * sx;
         }
       }
     }
