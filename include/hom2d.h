@@ -122,6 +122,30 @@ hom2d_status hom2d_workspace_bytes(const hom2d_config* cfg, const hom2d_dist* di
 /* Fill out[128] with a fresh ncclUniqueId (call on rank 0, broadcast the bytes). */
 hom2d_status hom2d_nccl_unique_id(void* out128);
 
+/* Peer-memory halo (SURVEY 8(e) "Stretch" / 8(f) f4: the strip halo by device
+ * loads from the neighbours' memory over NVLink instead of NCCL send/recv; the
+ * per-stage exchange of P:866-874's explicit scheme is the same data).  Every
+ * rank exports its workspace allocation (CUDA IPC handle + the workspace's
+ * offset in it) with hom2d_peer_id, the ids are exchanged by the caller (e.g.
+ * torch.distributed all_gather), and each rank calls hom2d_peer_connect with
+ * the ids of its strip neighbours (hom2d_strip_plan peer_lo / peer_hi; an id of
+ * this process's own allocation is used without a mapping).  From then on every
+ * halo exchange is: a signal kernel that publishes a sequence number into each
+ * neighbour's flag after the kernels that produced the exchanged array, and a
+ * pull kernel on the exchange stream that waits for both neighbours' numbers and
+ * copies their boundary rows into the local ghost buffers (traps after 60 s if a
+ * neighbour never signals).  NCCL still carries the allreduces (dt, errors).
+ * Both: handles with nranks > 1 created with an NCCL id, the same config on
+ * every rank; HOM2D_ERR_STATE otherwise, HOM2D_ERR_CUDA if a mapping fails.
+ * The id is plain bytes (copyable between processes of one node). */
+typedef struct {
+  uint8_t ipc[64];            /* cudaIpcMemHandle_t of the allocation holding the workspace */
+  uint64_t offset;            /* workspace start within that allocation (bytes) */
+  int32_t rank, device;       /* informational */
+} hom2d_peer_id_t;
+hom2d_status hom2d_peer_id(hom2d* h, hom2d_peer_id_t* out);
+hom2d_status hom2d_peer_connect(hom2d* h, const hom2d_peer_id_t* lo, const hom2d_peer_id_t* hi);
+
 /* Create a solver.  dist == NULL means one GPU (current device, default stream).
  * workspace: caller-owned device memory of >= hom2d_workspace_bytes, 256-B aligned. */
 hom2d_status hom2d_create(const hom2d_config* cfg, const hom2d_dist* dist, void* workspace,

@@ -29,7 +29,8 @@ STATUS = {0: "OK", 1: "ERR_ARG", 2: "ERR_MESH", 3: "ERR_ORDER", 4: "ERR_NONPHYSI
 EXPORTS = ["hom2d_strip_plan", "hom2d_workspace_bytes", "hom2d_nccl_unique_id", "hom2d_create", "hom2d_local_extent",
            "hom2d_set_state", "hom2d_get_state", "hom2d_init_case", "hom2d_residual", "hom2d_residual_strip", "hom2d_limit",
            "hom2d_compute_dt", "hom2d_step", "hom2d_error", "hom2d_time", "hom2d_decisions", "hom2d_decision_map",
-           "hom2d_launch_count", "hom2d_stage_timing", "hom2d_stage_time", "hom2d_last_error", "hom2d_destroy"]
+           "hom2d_launch_count", "hom2d_stage_timing", "hom2d_stage_time", "hom2d_last_error", "hom2d_destroy",
+           "hom2d_peer_id", "hom2d_peer_connect"]
 
 
 class Hom2dError(RuntimeError):
@@ -59,6 +60,10 @@ class StripPlan(C.Structure):
     _fields_ = [("row0", C.c_int32), ("nrows", C.c_int32), ("ghost_rows", C.c_int32),
                 ("peer_lo", C.c_int32), ("peer_hi", C.c_int32), ("has_lo", C.c_int32), ("has_hi", C.c_int32),
                 ("row_values", C.c_int64)]
+
+
+class PeerId(C.Structure):
+    _fields_ = [("ipc", C.c_uint8 * 64), ("offset", C.c_uint64), ("rank", C.c_int32), ("device", C.c_int32)]
 
 
 class Dist(C.Structure):
@@ -102,6 +107,8 @@ def load(path: str = LIB_PATH):
     L.hom2d_stage_time.argtypes = [vp, P(d), P(i64)]
     L.hom2d_last_error.argtypes = [vp]
     L.hom2d_last_error.restype = C.c_char_p
+    L.hom2d_peer_id.argtypes = [vp, P(PeerId)]
+    L.hom2d_peer_connect.argtypes = [vp, P(PeerId), P(PeerId)]
     L.hom2d_destroy.argtypes = [vp]
     L.hom2d_destroy.restype = None
     for name in EXPORTS:
@@ -267,6 +274,17 @@ class Solver:
         self._check(self._L.hom2d_stage_time(self.h, C.byref(ms), C.byref(n)))
         return ms.value, n.value
 
+    def peer_id(self) -> bytes:
+        """This rank's peer-memory halo id (hom2d_peer_id): plain bytes to exchange."""
+        out = PeerId()
+        self._check(self._L.hom2d_peer_id(self.h, C.byref(out)))
+        return bytes(out)
+
+    def peer_connect(self, lo: bytes, hi: bytes):
+        """Map the strip neighbours' workspaces (hom2d_peer_connect): halos by peer memory from now on."""
+        a, b = PeerId.from_buffer_copy(lo), PeerId.from_buffer_copy(hi)
+        self._check(self._L.hom2d_peer_connect(self.h, C.byref(a), C.byref(b)))
+
     def close(self):
         if getattr(self, "h", None):
             self._L.hom2d_destroy(self.h)
@@ -277,3 +295,21 @@ class Solver:
             self.close()
         except Exception:
             pass
+
+
+def peer_neighbours(rank: int, nranks: int):
+    """Ranks whose workspaces a rank maps for the peer-memory halo: its strip
+    neighbours (hom2d_strip_plan peer_lo, peer_hi; periodic in y)."""
+    return (rank + nranks - 1) % nranks, (rank + 1) % nranks
+
+
+def connect_peers(solver: "Solver", group=None):
+    """Peer-memory halo for a multi-rank solver: all-gather the ids over
+    torch.distributed (host bytes), connect to the strip neighbours.  Argument
+    marshalling only; the exchange itself runs in the library's kernels."""
+    import torch.distributed as dist
+    ids = [None] * dist.get_world_size(group)
+    dist.all_gather_object(ids, solver.peer_id(), group=group)
+    lo, hi = peer_neighbours(dist.get_rank(group), len(ids))
+    solver.peer_connect(ids[lo], ids[hi])
+    return ids

@@ -24,6 +24,13 @@ struct hom2d {
   cudaStream_t xstream = nullptr;          // nranks > 1: halo exchange stream (highest priority)
   bool self_x = false;                     // HOM2D_SELF_EXCHANGE test mode (see self_exchange_env)
   bool self_nccl = false;                  // HOM2D_SELF_EXCHANGE=2: the same through a 1-rank NCCL communicator
+  // peer-memory halo (hom2d_peer_connect; HOM2D_SELF_EXCHANGE=3: with itself as both neighbours)
+  char* ws = nullptr;                      // the caller's workspace (same carve on every rank)
+  bool peer = false;
+  char *pws_lo = nullptr, *pws_hi = nullptr;  // the neighbours' workspaces, mapped
+  void* ipc_mapped[2] = {nullptr, nullptr};   // IPC mappings to close
+  unsigned long long peer_seq = 0;         // exchanges so far (the same count on every rank)
+  unsigned long long* pflag = nullptr;     // [2]: last exchange signalled by the lo / hi neighbour
   cudaEvent_t ev_in = nullptr, ev_halo = nullptr;
   // CUDA graphs of 2^i steps (single GPU, untimed): launch-bound small grids
   cudaStream_t gstream = nullptr;
@@ -111,11 +118,13 @@ int points_per_elem(const hom2d_config& c) { return c.method == HOM2D_FV ? 1 : (
 // GPU, bitwise against the plain path.  HOM2D_SELF_EXCHANGE=1: the NCCL send/recv
 // replaced by device copies of the strip's own wrap rows; =2: the real NCCL data
 // plane on a 1-rank communicator (ncclCommInitRank, the grouped ncclSend/ncclRecv
-// of exchange() with rank 0 as both strip neighbours, every ncclAllReduce).
+// of exchange() with rank 0 as both strip neighbours, every ncclAllReduce); =3:
+// the peer-memory halo (peer.cu) with the handle's own workspace as both
+// neighbours' (signal + flag-gated pull kernels; no IPC mapping).
 int self_exchange_env(const hom2d_config& c, int nranks) {
   const char* v = getenv("HOM2D_SELF_EXCHANGE");
   if (nranks != 1 || c.bc != HOM2D_PERIODIC || !v) return 0;
-  return v[0] == '1' ? 1 : v[0] == '2' ? 2 : 0;
+  return v[0] == '1' ? 1 : v[0] == '2' ? 2 : v[0] == '3' ? 3 : 0;
 }
 
 hom2d_status check_cfg(const hom2d_config* c, int nranks) {
@@ -171,7 +180,9 @@ size_t carve(hom2d* h, const hom2d_config& c, int nranks, char* base) {
   auto* badl = lim ? cv.take<unsigned long long>(nl) : nullptr;
   long long* dmap = (c.record_decisions && nranks == 1) ? cv.take<long long>((size_t)c.nx * nrows) : nullptr;
   double *glo = nullptr, *ghi = nullptr, *qblo = nullptr, *qbhi = nullptr;
+  unsigned long long* pflag = nullptr;
   if (nranks > 1 || self_exchange_env(c, nranks)) {
+    pflag = cv.take<unsigned long long>(2);  // (same offset on every rank: peer-memory halo flags)
     glo = cv.take<double>(4 * (size_t)G * c.nx * np);
     ghi = cv.take<double>(4 * (size_t)G * c.nx * np);
     if (c.method != HOM2D_FV) {
@@ -183,7 +194,7 @@ size_t carve(hom2d* h, const hom2d_config& c, int nranks, char* base) {
     h->Qn = Qn; h->Q1 = Q1; h->Q2 = Q2; h->clock = clk; h->lam = lam; h->bad = bad; h->dec = dec;
     h->part = part; h->max_part = max_part; h->err3 = err3; h->qbar = qbar; h->dmap = dmap;
     h->laml = laml; h->badl = badl;
-    h->glo = glo; h->ghi = ghi; h->qblo = qblo; h->qbhi = qbhi;
+    h->glo = glo; h->ghi = ghi; h->qblo = qblo; h->qbhi = qbhi; h->pflag = pflag;
   }
   return cv.off + 512;  // trailing guard
 }
@@ -221,6 +232,38 @@ hom2d_status exchange(hom2d* h, const double* X, long long comp_stride, long lon
     *gcs = (long long)G * row_vals;
     *lo = h->ovr_lo;
     *hi = h->ovr_hi;
+    return HOM2D_OK;
+  }
+  if (h->peer) {  // peer-memory halo (peer.cu): signal my X, pull the neighbours' rows of theirs
+    NvtxRange nv("hom2d halo exchange (peer memory)");
+    const hom2d_strip_plan_t P = plan_of(h->cfg, h->rank, R);
+    const unsigned long long seq = ++h->peer_seq;
+    const long long off = (const char*)X - h->ws, pf = (const char*)h->pflag - h->ws;
+    // my lo neighbour's flag [1] ("from hi") and my hi neighbour's flag [0] ("from lo")
+    unsigned long long* to_lo = P.has_lo ? reinterpret_cast<unsigned long long*>(h->pws_lo + pf) + 1 : nullptr;
+    unsigned long long* to_hi = P.has_hi ? reinterpret_cast<unsigned long long*>(h->pws_hi + pf) + 0 : nullptr;
+    int e = launch_peer_signal(to_lo, to_hi, seq, h->stream);  // after the kernels that produced X
+    if (e) return fail(h, HOM2D_ERR_CUDA, "peer signal: %s", cudaGetErrorString((cudaError_t)e));
+    h->launches++;
+    PeerPull pp;
+    pp.flag_lo = h->pflag + 0;
+    pp.flag_hi = h->pflag + 1;
+    pp.seq = seq;
+    pp.src_lo = P.has_lo ? reinterpret_cast<const double*>(h->pws_lo + off) + (long long)(h->nrows - G) * row_vals
+                         : nullptr;
+    pp.src_hi = P.has_hi ? reinterpret_cast<const double*>(h->pws_hi + off) : nullptr;
+    pp.src_cs = comp_stride;
+    pp.dst_lo = rlo;
+    pp.dst_hi = rhi;
+    pp.cnt = (long long)G * row_vals;
+    pp.vec = ((off | (long long)(h->nrows - G) * row_vals * 8 | comp_stride * 8 | pp.cnt * 8 |
+               (long long)(uintptr_t)rlo | (long long)(uintptr_t)rhi) & 15) == 0;
+    e = launch_peer_pull(pp, xs);
+    if (e) return fail(h, HOM2D_ERR_CUDA, "peer pull: %s", cudaGetErrorString((cudaError_t)e));
+    h->launches++;
+    *gcs = pp.cnt;
+    *lo = P.has_lo ? rlo : nullptr;
+    *hi = P.has_hi ? rhi : nullptr;
     return HOM2D_OK;
   }
   if (R == 1 && h->self_x && !h->comm) {  // test mode: the periodic wrap rows through the ghost buffers, on xs
@@ -423,6 +466,85 @@ hom2d_status hom2d_nccl_unique_id(void* out128) {
   return HOM2D_OK;
 }
 
+namespace {
+// the allocation holding p (CUDA IPC exports whole allocations)
+bool alloc_base(const void* p, char** base) {
+  typedef CUresult (*fn_t)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static fn_t fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return false;
+    fn = reinterpret_cast<fn_t>(f);
+  }
+  CUdeviceptr b = 0;
+  size_t sz = 0;
+  if (fn(&b, &sz, (CUdeviceptr)(uintptr_t)p) != CUDA_SUCCESS) return false;
+  *base = reinterpret_cast<char*>((uintptr_t)b);
+  return true;
+}
+hom2d_status own_peer_id(hom2d* h, hom2d_peer_id_t* out) {
+  memset(out, 0, sizeof(*out));
+  char* base = nullptr;
+  if (!alloc_base(h->ws, &base)) return fail(h, HOM2D_ERR_CUDA, "peer id: cuMemGetAddressRange failed");
+  cudaIpcMemHandle_t mh;
+  static_assert(sizeof(mh) == sizeof(out->ipc), "cudaIpcMemHandle_t size");
+  CU(h, cudaIpcGetMemHandle(&mh, base));
+  memcpy(out->ipc, &mh, sizeof(mh));
+  out->offset = (uint64_t)(h->ws - base);
+  out->rank = h->rank;
+  out->device = h->device;
+  return HOM2D_OK;
+}
+}  // namespace
+
+hom2d_status hom2d_peer_id(hom2d* h, hom2d_peer_id_t* out) {
+  GUARD(h);
+  if (!out) return fail(h, HOM2D_ERR_ARG, "peer id: null pointer");
+  if (!h->pflag) return fail(h, HOM2D_ERR_STATE, "peer id: a handle with nranks > 1 is needed");
+  return own_peer_id(h, out);
+}
+
+hom2d_status hom2d_peer_connect(hom2d* h, const hom2d_peer_id_t* lo, const hom2d_peer_id_t* hi) {
+  GUARD(h);
+  if (!lo || !hi) return fail(h, HOM2D_ERR_ARG, "peer connect: null id");
+  if (!h->pflag || !h->glo) return fail(h, HOM2D_ERR_STATE, "peer connect: a handle with nranks > 1 is needed");
+  if (h->peer) return fail(h, HOM2D_ERR_STATE, "peer connect: already connected");
+  if (h->nranks > 1 && !h->comm) return fail(h, HOM2D_ERR_STATE, "peer connect: strip-only handle (no NCCL id)");
+  hom2d_peer_id_t me;
+  hom2d_status st = own_peer_id(h, &me);
+  if (st) return st;
+  const hom2d_peer_id_t* ids[2] = {lo, hi};
+  char* mapped[2] = {nullptr, nullptr};
+  for (int side = 0; side < 2; ++side) {
+    const hom2d_peer_id_t* id = ids[side];
+    if (!memcmp(id->ipc, me.ipc, sizeof(me.ipc))) {  // this process's own allocation (self / test)
+      mapped[side] = h->ws - me.offset;
+    } else if (side == 1 && !memcmp(ids[0]->ipc, id->ipc, sizeof(id->ipc)) && mapped[0]) {
+      mapped[1] = mapped[0];  // two ranks: both neighbours are the same peer (one mapping)
+    } else {
+      cudaIpcMemHandle_t mh;
+      memcpy(&mh, id->ipc, sizeof(mh));
+      void* p = nullptr;
+      const cudaError_t e = cudaIpcOpenMemHandle(&p, mh, cudaIpcMemLazyEnablePeerAccess);
+      if (e != cudaSuccess) {
+        for (void*& m : h->ipc_mapped)
+          if (m) { cudaIpcCloseMemHandle(m); m = nullptr; }
+        return fail(h, HOM2D_ERR_CUDA, "peer connect: cudaIpcOpenMemHandle (rank %d): %s", id->rank,
+                    cudaGetErrorString(e));
+      }
+      h->ipc_mapped[side] = p;
+      mapped[side] = (char*)p;
+    }
+  }
+  h->pws_lo = mapped[0] + lo->offset;
+  h->pws_hi = mapped[1] + hi->offset;
+  h->peer = true;
+  return HOM2D_OK;
+}
+
 hom2d_status hom2d_create(const hom2d_config* cfg, const hom2d_dist* dist, void* workspace, size_t ws_bytes,
                           hom2d** out) {
   if (!out) return HOM2D_ERR_ARG;
@@ -463,6 +585,16 @@ hom2d_status hom2d_create(const hom2d_config* cfg, const hom2d_dist* dist, void*
   const int sxm = self_exchange_env(*cfg, R);
   h->self_x = sxm != 0;
   h->self_nccl = sxm == 2;
+  h->ws = (char*)workspace;
+  if (h->pflag && cudaMemset(h->pflag, 0, 2 * sizeof(unsigned long long)) != cudaSuccess) {
+    cudaFreeHost(h->t_host);
+    delete h;
+    return HOM2D_ERR_CUDA;
+  }
+  if (sxm == 3) {  // peer-memory halo with itself as both neighbours
+    h->peer = true;
+    h->pws_lo = h->pws_hi = h->ws;
+  }
   if ((R > 1 && dist->nccl_id) || h->self_x) {  // (no id: strip-only handle, see hom2d_residual_strip)
     if (R > 1 || h->self_nccl) {
       ncclUniqueId id;
@@ -851,7 +983,11 @@ const char* hom2d_last_error(const hom2d* h) { return h ? h->msg : "null handle"
 
 void hom2d_destroy(hom2d* h) {
   if (!h) return;
+  cudaSetDevice(h->device);
   if (h->stream) cudaStreamSynchronize(h->stream); else cudaDeviceSynchronize();
+  if (h->xstream) cudaStreamSynchronize(h->xstream);
+  for (void*& m : h->ipc_mapped)
+    if (m) { cudaIpcCloseMemHandle(m); m = nullptr; }
   for (cudaEvent_t e : h->ev) cudaEventDestroy(e);
   if (h->xstream) cudaStreamSynchronize(h->xstream);
   if (h->gstream) cudaStreamSynchronize(h->gstream);

@@ -133,6 +133,22 @@ int launch_dgoi_stage(int k, const StageArgs& a, cudaStream_t s);
 int launch_p1_stage(int method, const StageArgs& a, cudaStream_t s);
 int march_rows_waves(int nrows, int strips, int rb_max, int ctas_per_sm);  // DG, (k+2)-point over-integration (f3)
 
+// peer-memory halo (peer.cu): signal "my X is complete" into the neighbours'
+// flags; pull the neighbours' G boundary rows of X (their memory, mapped) into
+// the local ghost buffers once both have signalled exchange `seq`
+struct PeerPull {
+  const unsigned long long *flag_lo, *flag_hi;  // own flags, written by the lo / hi neighbour
+  unsigned long long seq;
+  const double *src_lo, *src_hi;  // neighbour rows (mapped); nullptr = no neighbour on that side
+  long long src_cs;               // their component stride
+  double *dst_lo, *dst_hi;        // ghost buffers [4][cnt]
+  long long cnt;                  // values per component (G rows)
+  int vec;                        // every run 16-B aligned and cnt even: 16-B copies
+};
+int launch_peer_signal(unsigned long long* to_lo, unsigned long long* to_hi, unsigned long long seq,
+                       cudaStream_t s);
+int launch_peer_pull(const PeerPull& p, cudaStream_t s);
+
 struct AuxArgs {
   int method, k, nx, nrows, row0, ny_global;
   double xmin, xmax, ymin, ymax, gamma;

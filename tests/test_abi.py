@@ -56,6 +56,7 @@ int main(void) {
          offsetof(hom2d_config, limiter_per_step), offsetof(hom2d_config, limiter_characteristic),
          sizeof(hom2d_dist), offsetof(hom2d_dist, cuda_stream));
   printf("%zu %zu\n", offsetof(hom2d_config, fv_error_recon), offsetof(hom2d_config, dg_overintegrate));
+  printf("%zu %zu %zu\n", sizeof(hom2d_peer_id_t), offsetof(hom2d_peer_id_t, offset), offsetof(hom2d_peer_id_t, rank));
   return 0;
 }
 '''
@@ -70,7 +71,8 @@ int main(void) {
     D = P.Dist
     assert vals == [ctypes.sizeof(C), C.gamma.offset, C.limiter_eps.offset, C.record_decisions.offset,
                     C.limiter_per_step.offset, C.limiter_characteristic.offset, ctypes.sizeof(D), D.cuda_stream.offset,
-                    C.fv_error_recon.offset, C.dg_overintegrate.offset]
+                    C.fv_error_recon.offset, C.dg_overintegrate.offset,
+                    ctypes.sizeof(P.PeerId), P.PeerId.offset.offset, P.PeerId.rank.offset]
 
 
 def test_product_does_not_import_oracle():

@@ -116,3 +116,54 @@ def test_strip_plan_covers_grid():
         P.strip_plan(P.make_config(16, 10, method="cpr", k=3), 0, 4)   # ny % nranks != 0
     with pytest.raises(P.Hom2dError):
         P.strip_plan(P.make_config(16, 8, method="fv", k=1), 0, 8)     # FV needs 2 ghost rows
+
+
+class _FakeSolver:
+    """stands in for Solver in connect_peers: ids are bytes naming the rank"""
+    def __init__(self, rank):
+        self.rank = rank
+        self.got = None
+
+    def peer_id(self):
+        return b"rank%03d" % self.rank + bytes(73)
+
+    def peer_connect(self, lo, hi):
+        self.got = (lo, hi)
+
+
+def _peer_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_1709_01619_b200 as P
+    try:
+        s = _FakeSolver(rank)
+        ids = P.connect_peers(s)
+        assert [i[:7] for i in ids] == [b"rank%03d" % r for r in range(world)]
+        lo, hi = s.got
+        # the strip neighbours of hom2d_strip_plan (periodic in y)
+        plan = P.strip_plan(P.make_config(6, 4 * world), rank, world)
+        assert lo[:7] == b"rank%03d" % plan.peer_lo and hi[:7] == b"rank%03d" % plan.peer_hi
+        q.put((rank, "ok"))
+    except Exception as e:  # pragma: no cover - reported to the parent
+        q.put((rank, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_peer_id_exchange_gloo(world):
+    """The peer-memory halo's host plumbing (connect_peers): every rank gets all
+    ids by all_gather and connects to the ids of its strip-plan neighbours."""
+    from paper_1709_01619_b200 import build
+    build.build()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_peer_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(r[1] == "ok" for r in res), res

@@ -74,9 +74,11 @@ def test_overlapped_stage_path_bitwise(P, monkeypatch, method, k, limiter):
     that writes its source or the ghost buffers would break this.  =2: the same
     through NCCL itself -- a 1-rank communicator (ncclCommInitRank), the grouped
     ncclSend/ncclRecv of every stage with rank 0 as both neighbours, the lambda /
-    non-physical-flag ncclAllReduce of every step."""
+    non-physical-flag ncclAllReduce of every step.  =3: the peer-memory halo
+    (peer.cu) with the handle's own workspace as both neighbours': the signal
+    kernel, the flag-gated pull kernel on the exchange stream, the ghost rows."""
     out = []
-    for sx in ("0", "1", "2"):
+    for sx in ("0", "1", "2", "3"):
         monkeypatch.setenv("HOM2D_SELF_EXCHANGE", sx)
         cfg = P.make_config(23, 14, method=method, k=k, cfl=0.05, limiter=limiter)
         s = P.Solver(cfg)
@@ -86,6 +88,43 @@ def test_overlapped_stage_path_bitwise(P, monkeypatch, method, k, limiter):
         s.close()
     np.testing.assert_array_equal(out[0], out[1])
     np.testing.assert_array_equal(out[0], out[2])
+    np.testing.assert_array_equal(out[0], out[3])
+
+
+@pytest.mark.parametrize("method,k,limiter", [("cpr", 3, 0), ("fv", 2, 0), ("dg", 1, 1)])
+def test_peer_connect_self_bitwise(P, monkeypatch, method, k, limiter):
+    """The public peer-memory API on one GPU: hom2d_peer_id exports the
+    workspace allocation (cuMemGetAddressRange + cudaIpcGetMemHandle), and
+    hom2d_peer_connect with the handle's own id as both neighbours' (recognised
+    as this process's allocation: no IPC mapping) switches the overlapped strip
+    path to the peer-memory halo; 20 steps equal the plain path bitwise, and the
+    error query's exchange (FV reconstructed error) takes the same route."""
+    out = []
+    for mode in ("plain", "peer"):
+        monkeypatch.setenv("HOM2D_SELF_EXCHANGE", "1" if mode == "peer" else "0")
+        cfg = P.make_config(21, 12, method=method, k=k, cfl=0.05, limiter=limiter,
+                            fv_error_recon=1 if method == "fv" else 0)
+        s = P.Solver(cfg)
+        if mode == "peer":
+            pid = s.peer_id()
+            assert len(pid) == 80 and pid[:64] != bytes(64)
+            s.peer_connect(pid, pid)
+            with pytest.raises(P.Hom2dError):
+                s.peer_connect(pid, pid)  # already connected
+        s.init_case(P.VORTEX)
+        s.step(20)
+        out.append((s.get_state(), s.error(P.VORTEX, 0)))
+        s.close()
+    np.testing.assert_array_equal(out[0][0], out[1][0])
+    assert out[0][1] == out[1][1]
+
+
+def test_peer_id_needs_strip_handle(P):
+    """hom2d_peer_id / hom2d_peer_connect on a plain one-GPU handle: HOM2D_ERR_STATE."""
+    s = P.Solver(P.make_config(8, 8, method="cpr", k=1))
+    with pytest.raises(P.Hom2dError):
+        s.peer_id()
+    s.close()
 
 
 @pytest.mark.parametrize("method,k", [("cpr", 2), ("fv", 2)])

@@ -57,7 +57,7 @@ def main():
     s.init_case(P.VORTEX)
     s.error(P.VORTEX, 1)
     s.close()
-    for sx in ("1", "2"):  # the multi-GPU stage path on one GPU
+    for sx in ("1", "2", "3"):  # the multi-GPU stage path on one GPU (3: peer-memory halo)
         os.environ["HOM2D_SELF_EXCHANGE"] = sx
         for method, k in (("cpr", 3), ("fv", 1), ("dg", 2)):
             s = P.Solver(P.make_config(23, 14, method=method, k=k, cfl=0.05, limiter=1 if method == "dg" else 0))
