@@ -287,6 +287,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-tte", action="store_true", help="skip the time-to-error ladder")
     ap.add_argument("--no-weak", action="store_true", help="skip the weak-scaling workloads (configs[4])")
+    ap.add_argument("--halo", default="nccl", choices=["nccl", "peer"],
+                    help="N > 1: strip halo by NCCL send/recv (default) or by the peer-memory pull (hom2d_peer_connect)")
     args = ap.parse_args()
     assert args.warmup >= 3, "timing rules: W >= 3"
     wl = args.workload
@@ -328,6 +330,8 @@ def main():
     else:
         cfg = P.make_config(nx, ny, method=method, k=k, cfl=cfl)
     s = P.Solver(cfg, rank=rank, nranks=world, device=local, stream=stream, nccl_id=nid)
+    if world > 1 and args.halo == "peer":
+        P.connect_peers(s)
     s.init_case(P.SHOCK if case == "shock" else P.VORTEX)
     npe = 1 if method == "fv" else (k + 1) ** 2
     ndof_global = nx * ny * npe
@@ -432,6 +436,8 @@ def main():
                 wid = obj[0]
             ws = P.Solver(P.make_config(wnx, wny, method=wm, k=wk, cfl=wcfl), rank=rank, nranks=world, device=local,
                           stream=stream, nccl_id=wid)
+            if world > 1 and args.halo == "peer":
+                P.connect_peers(ws)
             ws.init_case(P.VORTEX)
             ws.step(args.warmup)
             barrier_sync()
@@ -458,6 +464,7 @@ def main():
                            "case": ("isentropic vortex, periodic" if case == "vortex" else
                                     "radial shock tube, transmissive, minmod limiter every stage"),
                            "cfl": cfl, "parallelism": f"ystrip{world}",
+                           "halo": (args.halo if world > 1 else "none (1 GPU: periodic wrap in place)"),
                            "l2_flush": f"none needed: {4 * ndof_global * 8 / 1e9:.2f} GB/state array >> 126 MB L2"},
                 "e2e": e2e, "gpu_launches": gpu_launches, "roofline": roofline, "cpu_baseline": cpu,
                 "time_to_error": tte,
