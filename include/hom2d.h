@@ -31,8 +31,9 @@
  * y-strips (rank r owns element rows [r*ny/G, (r+1)*ny/G)); every rank calls
  * every function with the same arguments; arrays passed to set/get_state are
  * the LOCAL strip in the layout above.  Boundary element rows are exchanged with
- * ncclSend/ncclRecv once per RK stage; the dt wave-speed max and the error sums
- * are ncclAllReduce'd.  ny % nranks == 0 is required.
+ * ncclSend/ncclRecv once per RK stage (or pulled from the neighbours' memory
+ * after hom2d_peer_connect); the dt wave-speed max and the error sums are
+ * ncclAllReduce'd.  ny % nranks == 0 is required.
  */
 #ifndef HOM2D_H
 #define HOM2D_H
@@ -137,7 +138,11 @@ hom2d_status hom2d_nccl_unique_id(void* out128);
  * neighbour never signals).  NCCL still carries the allreduces (dt, errors).
  * Both: handles with nranks > 1 created with an NCCL id, the same config on
  * every rank; HOM2D_ERR_STATE otherwise, HOM2D_ERR_CUDA if a mapping fails.
- * The id is plain bytes (copyable between processes of one node). */
+ * The id is plain bytes (copyable between processes of one node).  A
+ * neighbour may read this rank's rows until it returns from its own last
+ * hom2d_step / hom2d_limit / hom2d_error: every rank must have returned from
+ * those (e.g. a host barrier) before any rank destroys its handle and frees its
+ * workspace (the Python binding's close() does the barrier). */
 typedef struct {
   uint8_t ipc[64];            /* cudaIpcMemHandle_t of the allocation holding the workspace */
   uint64_t offset;            /* workspace start within that allocation (bytes) */

@@ -287,11 +287,20 @@ class Solver:
 
     def close(self):
         if getattr(self, "h", None):
+            grp = getattr(self, "_peer_group", False)
+            if grp is not False:
+                # peer-memory halo: a neighbour may still be pulling rows of this
+                # workspace until every rank has returned from its last step
+                import torch.distributed as dist
+                if dist.is_initialized():
+                    dist.barrier(group=grp)
+                self._peer_group = False
             self._L.hom2d_destroy(self.h)
             self.h = None
 
     def __del__(self):
         try:
+            self._peer_group = False  # (no collective from a finaliser)
             self.close()
         except Exception:
             pass
@@ -312,4 +321,5 @@ def connect_peers(solver: "Solver", group=None):
     dist.all_gather_object(ids, solver.peer_id(), group=group)
     lo, hi = peer_neighbours(dist.get_rank(group), len(ids))
     solver.peer_connect(ids[lo], ids[hi])
+    solver._peer_group = group  # close() then waits for every rank before the workspace goes
     return ids
