@@ -209,7 +209,8 @@ def test_determinism_bitwise(orc, P):
 
 @pytest.mark.parametrize("method,k,n", [("cpr", 3, 4096), ("cpr", 2, 1024), ("fv", 1, 2048), ("ndg", 3, 2048),
                                           ("dg", 3, 2048), ("sd", 3, 2048), ("cpr", 1, 2048), ("cpr", 4, 1024),
-                                          ("dg", 4, 1024), ("sd", 2, 1024), ("fv", 2, 2048)])
+                                          ("dg", 4, 1024), ("sd", 2, 1024), ("fv", 2, 2048), ("sd", 4, 1024),
+                                          ("ndg", 4, 1024), ("ndg", 2, 1024), ("dg", 2, 1024)])
 def test_full_size_tiled_patch(orc, P, method, k, n):
     """At BASELINE sizes, in the bench's launch configuration (CPR P3 at 4096^2 is
     the north-star bench launch itself): a state that repeats a seeded 16x16-element
@@ -288,6 +289,39 @@ def test_full_size_tiled_patch_limited_step(orc, P, method, k, n, cfl):
     err = np.abs(out - ref).max(axis=(1, 2, 3, 4, 5)) / np.maximum(np.abs(ref).reshape(4, -1).max(1), 1e-300)
     assert err.max() < 1e-10
     assert s.decisions()[0] == cnt[0] * (n // pn) ** 2
+    s.close()
+
+
+@pytest.mark.parametrize("method,k,n", [("cpr", 3, 2048), ("dg", 3, 2048), ("sd", 4, 1024), ("ndg", 4, 1024),
+                                          ("sd", 2, 1024), ("fv", 2, 2048)])
+def test_full_size_tiled_patch_step(orc, P, method, k, n):
+    """Every stage variant at bench sizes (stage 1 without q^n, stage 2 with it,
+    stage 3 with the dt wave speed / non-physical epilogue; the fused dt): two
+    SSP-RK3 steps of a periodic state that repeats a seeded 16x16 patch equal the
+    oracle's two steps of the patch on its own periodic grid, tiled (dt agrees:
+    same element size, same max wave speed)."""
+    import torch
+    pn = 16
+    box_small = (-5.0, -5.0 + 10.0 * pn / n, -5.0, -5.0 + 10.0 * pn / n)
+    cfl = CFL[(method, k)]
+    oc = orc.config(nx=pn, ny=pn, method=method, k=k, box=box_small, cfl=cfl)
+    from paper_1709_01619_b200.inputs import perturb
+    qp = perturb(orc.init_case(oc), seed=29, amp=1e-3)
+    q2, t2, n2 = orc.run(oc, qp, 2)
+    npe = 1 if method == "fv" else (k + 1) ** 2
+    patch = torch.from_numpy(qp.reshape(4, pn, 1, pn, npe)).cuda()
+    big = patch.repeat(1, n // pn, 1, n // pn, 1).reshape(-1).contiguous()
+    s = P.Solver(P.make_config(n, n, method=method, k=k, cfl=cfl, box=(-5.0, 5.0, -5.0, 5.0)))
+    s.set_state(big)
+    del big
+    t, steps = s.step(2)
+    assert steps == n2 == 2 and abs(t - t2) <= 1e-12 * t2
+    out = torch.empty(4 * n * n * npe, dtype=torch.float64, device="cuda")
+    s.get_state(out)
+    out = out.view(4, n // pn, pn, n // pn, pn, npe)
+    ref = torch.from_numpy(q2.reshape(4, 1, pn, 1, pn, npe)).cuda()
+    err = max(float((out[c] - ref[c]).abs().max() / ref[c].abs().max().clamp_min(1e-300)) for c in range(4))
+    assert err <= 1e-10
     s.close()
 
 
