@@ -60,6 +60,9 @@ namespace {
 #define H2D_DG_TX2 30  // DG P2: 90 threads, 4 CTAs/SM (its g buffer: 32 fits 3; +2.7 %)
 #endif
 enum { LM_DG = 2, LM_SD = 4 };
+#ifndef H2D_Q0LATE
+#define H2D_Q0LATE 1
+#endif
 #ifndef H2D_WSQRT
 #define H2D_WSQRT fsqrt_ws  // Rusanov dissipation speed (common.cuh; A/B: fsqrt)
 #endif
@@ -796,7 +799,7 @@ __global__ void __launch_bounds__(L<M, K>::NT, LTile<M, K>::MINB) gl_stage_kerne
           for (int x = 0; x < N; ++x) o[x] = ov[c][x];
         }
       }
-      if (HQ0 && Lr < RBv)  // q^n of the next row into the consumed private slots
+      if (HQ0 && Lr < RBv && !H2D_Q0LATE)  // q^n of the next row into the consumed private slots
         q0_prefetch<N, NT>(sQ0, a.q0, a.cs, base + (long long)a.nx * NP, tid, vec);
       if (HAVG) {  // this line's share of the element average: w_b sum_x w_x q
 #pragma unroll
@@ -839,6 +842,12 @@ __global__ void __launch_bounds__(L<M, K>::NT, LTile<M, K>::MINB) gl_stage_kerne
       if (tid == 0) fence_proxy_async_smem();
       issue_row(Lr + NSTG);
     }
+    // q^n of the next row into the consumed private slots -- after the proxy
+    // fence of the TMA issue: the fence waits for this thread's in-flight
+    // cp.async writes, so a prefetch issued before it stalled warp 0 for a
+    // global-memory round trip every row (H2D_Q0LATE=0: the round-2 order)
+    if (H2D_Q0LATE && HQ0 && own && Lr > 0 && Lr < RBv)
+      q0_prefetch<N, NT>(sQ0, a.q0, a.cs, ((long long)(jb + Lr) * a.nx + i0 + lx) * NP + b * N, tid, vec);
   }
   if (HLAM && a.lam) block_max_to(lam, a.lam, sm + H::ORD);
 }

@@ -195,6 +195,9 @@ __device__ __forceinline__ void ld4(const double* p, double v[4]) {
   v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
 }
 
+#ifndef H2D_Q0LATE
+#define H2D_Q0LATE 1
+#endif
 #ifndef H2D_WSQRT
 #define H2D_WSQRT fsqrt_ws  // Rusanov dissipation speed (common.cuh; A/B: fsqrt)
 #endif
@@ -731,7 +734,7 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
           for (int x = 0; x < N; ++x) o[x] = ov[c][x];
         }
       }
-      if (HQ0 && L < RBv)  // q^n of the next row into the (now consumed) private slots
+      if (HQ0 && L < RBv && !H2D_Q0LATE)  // q^n of the next row into the (now consumed) private slots
         q0_prefetch<N, NT, H::LP>(sQ0, a.q0, a.cs, base + (long long)a.nx * NP, tid, vec);
       if (HAVG) {  // this line's share of the element average: w_b sum_x w_x q
 #pragma unroll
@@ -774,6 +777,12 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
       if (tid == 0) fence_proxy_async_smem();
       issue_row(L + NSTG);
     }
+    // q^n of the next row into the consumed private slots -- after the proxy
+    // fence of the TMA issue: the fence waits for this thread's in-flight
+    // cp.async writes, so a prefetch issued before it stalled warp 0 for a
+    // global-memory round trip every row (H2D_Q0LATE=0: the round-2 order)
+    if (H2D_Q0LATE && HQ0 && own && L > 0 && L < RBv)
+      q0_prefetch<N, NT, H::LP>(sQ0, a.q0, a.cs, ((long long)(jb + L) * a.nx + i0 + lx) * NP + b * N, tid, vec);
   }
   if (HLAM && a.lam) block_max_to(lam, a.lam, sm + H::ORD);
 }
