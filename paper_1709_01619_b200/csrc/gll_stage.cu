@@ -80,6 +80,9 @@ enum { GM_CPR = 1, GM_NDG = 3 };
 #define H2D_NDG_TX4 H2D_TX4
 #endif
 constexpr int NSTG = 3;  // ring depth (rows): current, N neighbour, one in flight
+#ifndef H2D_SWZ_CONTIG
+#define H2D_SWZ_CONTIG 1
+#endif
 // NDG: y work by column (as gl_stage.cu's H2D_GL_COLY): the thread of line b
 // also owns column b of its element for the y direction -- g at the column's
 // points, D g, its S / N jumps (the S one carried in registers from the row
@@ -115,7 +118,12 @@ struct G {
   // per stage (doubles): SWZ: 4 components x RSW rows of 16, each component at a
   // 1024-B boundary so the swizzle phase of a slot is (slot & 7) for every
   // component (+ 8 unswizzled fix-up rows); else 4 * CREG
-  static constexpr int RSW = (NSL + 7) & ~7;
+  // CONTIG (NDG): the 4 components of a row as ONE 3-D box {16, NSL, 4} (rows of
+  // 16 doubles contiguous over components, no padding to whole 1024-B blocks;
+  // the swizzle phase of row r = c NSL + e of the box is r & 7).  A/B (round
+  // 2b): NDG P3 +1 %, CPR P3 -1 % (it keeps four per-component boxes)
+  static constexpr bool CONTIG = H2D_SWZ_CONTIG && M == GM_NDG;
+  static constexpr int RSW = CONTIG ? NSL : (NSL + 7) & ~7;
   static constexpr int FIXO = 4 * RSW * 16;
   static constexpr int STG = SWZ ? FIXO + 8 * 16 : 4 * CREG;
   static constexpr int STGA = H2D_STGA(STG);          // stage stride (see H2D_STGA)
@@ -309,7 +317,9 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
       if (wrapW) tx += 4u * 128u;
       if (wrapE) tx += 4u * 128u;
       mbar_arrive_expect_tx(br, tx);
-      for (int c = 0; c < 4; ++c) tma_load_3d(st + c * H::RSW * 16, mp, 0, y0, c, br);
+      if (H::CONTIG) tma_load_3d(st, mp, 0, y0, 0, br);
+      else
+        for (int c = 0; c < 4; ++c) tma_load_3d(st + c * H::RSW * 16, mp, 0, y0, c, br);
       double* fix = st + H::FIXO;
       for (int c = 0; c < 4; ++c) {
         if (wrapW) tma_load_1d(fix + (0 * 4 + c) * 16, rb + c * cs + (long long)iw * NP, NP * 8, br);
@@ -372,7 +382,8 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
   // value (c, p) of own element slot e = lx + 1 (hot path: no branches)
   auto own_at = [&](const RowView& v, int c, int e, int p) -> double {
     if constexpr (H::SWZ) {  // 128-B swizzle: 16-B chunk (p >> 1) of row e sits at chunk (p >> 1) ^ (e & 7)
-      return v.st[(c * H::RSW + e) * 16 + ((((p >> 1) ^ (e & 7)) << 1) | (p & 1))];
+      const int r = c * H::RSW + e;
+      return v.st[r * 16 + ((((p >> 1) ^ ((H::CONTIG ? r : e) & 7)) << 1) | (p & 1))];
     } else {
       return v.st[c * CREG + CW + (v.dM ^ (c & v.csodd)) + (e - 1) * NP + p];
     }
@@ -382,7 +393,8 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
   auto any_at = [&](const RowView& v, int c, int e, int p) -> double {
     if constexpr (H::SWZ) {
       const bool fw = (e == 0 && wrapW), fe = (e == TXv + 1 && wrapE);
-      const int iS = (c * H::RSW + e) * 16 + ((((p >> 1) ^ (e & 7)) << 1) | (p & 1));
+      const int r = c * H::RSW + e;
+      const int iS = r * 16 + ((((p >> 1) ^ ((H::CONTIG ? r : e) & 7)) << 1) | (p & 1));
       const int iF = H::FIXO + ((fe ? 4 : 0) + c) * 16 + p;
       return v.st[(fw || fe) ? iF : iS];
     } else {
@@ -445,7 +457,8 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
             if constexpr (H::SWZ) {  // 16-B chunks: points (4b + 2h, 4b + 2h + 1)
               if ((x & 1) == 0) {
                 const double2 u = *reinterpret_cast<const double2*>(
-                    vc.st + (c * H::RSW + lx + 1) * 16 + (((2 * b + (x >> 1)) ^ ((lx + 1) & 7)) << 1));
+                    vc.st + (c * H::RSW + lx + 1) * 16 +
+                    (((2 * b + (x >> 1)) ^ ((H::CONTIG ? c * H::RSW + lx + 1 : lx + 1) & 7)) << 1));
                 q[c][x] = u.x;
                 q[c][x + 1] = u.y;
               }
@@ -581,7 +594,8 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
 #pragma unroll
             for (int h = 0; h < N / 2; ++h) {
               const double2 u = *reinterpret_cast<const double2*>(
-                  vc.st + (c * H::RSW + lx + 1) * 16 + (((2 * l + h) ^ ((lx + 1) & 7)) << 1));
+                  vc.st + (c * H::RSW + lx + 1) * 16 +
+                  (((2 * l + h) ^ ((H::CONTIG ? c * H::RSW + lx + 1 : lx + 1) & 7)) << 1));
               if (l == 0) {
                 dyall[2 * h][c] = db * u.x;
                 dyall[2 * h + 1][c] = db * u.y;
@@ -802,15 +816,15 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 }  // namespace
 
-// {16 points, nelem elements, 4 components} fp64, box {16, box_e, 1}, 128-byte swizzle
-bool make_map(CUtensorMap* m, const double* base, long long nelem, long long cs, int box_e) {
+// {16 points, nelem elements, 4 components} fp64, box {16, box_e, box_c}, 128-byte swizzle
+bool make_map(CUtensorMap* m, const double* base, long long nelem, long long cs, int box_e, int box_c) {
   memset(m, 0, sizeof(*m));
   if (!base) return true;  // transmissive boundary: never used
   auto fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[3] = {16, (cuuint64_t)nelem, 4};
   cuuint64_t strides[2] = {16 * sizeof(double), (cuuint64_t)cs * sizeof(double)};
-  cuuint32_t box[3] = {16, (cuuint32_t)box_e, 1};  // one component per copy
+  cuuint32_t box[3] = {16, (cuuint32_t)box_e, (cuuint32_t)box_c};  // one component or all four per copy
   cuuint32_t es[3] = {1, 1, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(base), dims, strides, box, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -834,8 +848,9 @@ static int launch_g(const StageArgs& a, cudaStream_t s) {
   memset(&maps, 0, sizeof(maps));
   if (H::SWZ) {
     const long long nel = (long long)a.nx * a.nrows;
-    if (!make_map(&maps.q, a.q, nel, a.cs, H::NSL) || !make_map(&maps.lo, a.ghost_lo, a.nx, a.gcs, H::NSL) ||
-        !make_map(&maps.hi, a.ghost_hi, a.nx, a.gcs, H::NSL))
+    const int bc = H::CONTIG ? 4 : 1;
+    if (!make_map(&maps.q, a.q, nel, a.cs, H::NSL, bc) || !make_map(&maps.lo, a.ghost_lo, a.nx, a.gcs, H::NSL, bc) ||
+        !make_map(&maps.hi, a.ghost_hi, a.nx, a.gcs, H::NSL, bc))
       return (int)cudaErrorInvalidValue;
   }
   StageArgs b = a;

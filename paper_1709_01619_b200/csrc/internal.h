@@ -121,9 +121,9 @@ inline int band_blocks(StageArgs& a) {
 int march_rows(int nrows, int strips, int rb_max, int ctas_per_sm = 4);
 
 // host: 3-D TMA tensor map {16 points, nelem elements, 4 components} (fp64,
-// box {16, box_e, 1}, 128-B swizzle) over an element-row array; base == nullptr
+// box {16, box_e, box_c}, 128-B swizzle) over an element-row array; base == nullptr
 // gives an unused zero map (transmissive boundary)
-bool make_map(CUtensorMap* m, const double* base, long long nelem, long long cs, int box_e);
+bool make_map(CUtensorMap* m, const double* base, long long nelem, long long cs, int box_e, int box_c = 1);
 
 int launch_gl_stage(int method, int k, const StageArgs& a, cudaStream_t s);   // DG, SD (marching)
 int launch_gll_stage(int method, int k, const StageArgs& a, cudaStream_t s);  // CPR, NDG
