@@ -83,6 +83,9 @@ constexpr int NSTG = 3;  // ring depth (rows): current, N neighbour, one in flig
 #ifndef H2D_SWZ_CONTIG
 #define H2D_SWZ_CONTIG 1
 #endif
+#ifndef H2D_Q0TMA
+#define H2D_Q0TMA 1
+#endif
 // NDG: y work by column (as gl_stage.cu's H2D_GL_COLY): the thread of line b
 // also owns column b of its element for the y direction -- g at the column's
 // points, D g, its S / N jumps (the S one carried in registers from the row
@@ -98,6 +101,7 @@ constexpr int NSTG = 3;  // ring depth (rows): current, N neighbour, one in flig
 
 struct GMaps {   // P3: 3-D tensor maps {16 points, TX+2 elements, 4 components}
   CUtensorMap q, lo, hi;
+  CUtensorMap q0;  // (Q0T) q^n, box {16, TX, 4}
 };
 
 template <int M, int K>
@@ -122,13 +126,19 @@ struct G {
   // 16 doubles contiguous over components, no padding to whole 1024-B blocks;
   // the swizzle phase of row r = c NSL + e of the box is r & 7).  A/B (round
   // 2b): NDG P3 +1 %, CPR P3 -1 % (it keeps four per-component boxes)
-  static constexpr bool CONTIG = H2D_SWZ_CONTIG && M == GM_NDG;
+  // Q0T (CPR P3): q^n of a row by TMA into a 2-row swizzled ring, issued two rows
+  // ahead (instead of one row ahead by per-thread cp.async); the contiguous
+  // box below pays for its shared memory
+  static constexpr bool Q0T = H2D_Q0TMA && SWZ && M == GM_CPR;
+  static constexpr bool CONTIG = H2D_SWZ_CONTIG && (M == GM_NDG || Q0T);
   static constexpr int RSW = CONTIG ? NSL : (NSL + 7) & ~7;
   static constexpr int FIXO = 4 * RSW * 16;
   static constexpr int STG = SWZ ? FIXO + 8 * 16 : 4 * CREG;
   static constexpr int STGA = H2D_STGA(STG);          // stage stride (see H2D_STGA)
   static constexpr int OR_ = 0;
-  static constexpr int OFW = OR_ + NSTG * STGA;       // W-face fluxes [TX+1][N][4]
+  static constexpr int QSTG = 4 * TX * 16;            // (Q0T) one q^n row: [4 x TX rows of 16], 1024-B multiple
+  static constexpr int OQT = OR_ + NSTG * STGA;       // (Q0T) q^n ring [2][QSTG]
+  static constexpr int OFW = OQT + (Q0T ? 2 * QSTG : 0);  // W-face fluxes [TX+1][N][4]
   static constexpr bool CY = H2D_GLL_COLY && M == GM_NDG;  // y work by column (NDG)
   static constexpr int OJN = OFW + (TX + 1) * N * 4;  // N jumps of the current row [TX][N][4]
   static constexpr int OJS = OJN + (CY ? 0 : TX * N * 4);      // S jumps, double-buffered [2][TX][N][4]
@@ -145,8 +155,9 @@ struct G {
   static constexpr int ORD = OT + ((N * N + 3 * N + 1) & ~1);
   static constexpr int OB = ORD + 32;                 // mbarriers (as doubles)
   static constexpr int LP = (N + 1) & ~1;             // q^n line slot (16-B multiple)
-  static constexpr int OQ0 = OB + ((NSTG + 1) & ~1);  // q^n prefetch [4][N][NT], thread-private
-  static constexpr int TOTAL = OQ0 + 4 * N * NT;
+  static constexpr int OQ0 = OB + ((NSTG + 2 + 1) & ~1);  // q^n prefetch [4][N][NT], thread-private (!Q0T)
+  static constexpr int TOTAL = OQ0 + (Q0T ? 0 : 4 * N * NT);
+  static_assert(!Q0T || (QSTG % 128 == 0 && OQT % 128 == 0), "1024-B aligned q^n stages");
   static_assert(OQ0 % 2 == 0, "16-B cp.async slots");
   static constexpr size_t SMEM = TOTAL * sizeof(double);
 };
@@ -271,6 +282,8 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
   double* sT = sm + H::OT;
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + H::OB);
   double* sQ0 = sm + H::OQ0;
+  double* sQT = sm + H::OQT;                  // (Q0T) q^n ring
+  uint64_t* qbar = bar + NSTG;                // (Q0T) its mbarriers
 
   const int tid = threadIdx.x;
   int bhi;
@@ -291,7 +304,7 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
 
   for (int i = tid; i < N * N + 3 * N; i += NT) sT[i] = tab.v[i];
   if (tid == 0) {
-    for (int s = 0; s < NSTG; ++s) mbar_init(&bar[s], 1);
+    for (int s = 0; s < NSTG + (H::Q0T ? 2 : 0); ++s) mbar_init(&bar[s], 1);
     mbar_fence_init();
   }
   __syncthreads();
@@ -406,8 +419,21 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
   };
 
   for (int L = 0; L < NSTG && L < nload; ++L) issue_row(L);
-  if (HQ0 && own)  // q^n of the first own row (step L = 1)
+  // (Q0T) q^n of own row jb + m into ring slot m & 1, by one TMA box
+  auto issue_q0 = [&](int m) {
+    if (tid != 0) return;
+    uint64_t* bq = &qbar[m & 1];
+    mbar_arrive_expect_tx(bq, 4u * TX * 128u);
+    tma_load_3d(sQT + (m & 1) * H::QSTG, &maps.q0, 0, (jb + m) * a.nx + i0, 0, bq);
+  };
+  if (H::Q0T) {
+    if (HQ0) {  // the first two own rows
+      issue_q0(0);
+      if (RBv > 1) issue_q0(1);
+    }
+  } else if (HQ0 && own) {  // q^n of the first own row (step L = 1)
     q0_prefetch<N, NT, H::LP>(sQ0, a.q0, a.cs, ((long long)jb * a.nx + i0 + lx) * NP + b * N, tid, vec);
+  }
 
   [[maybe_unused]] const double* D = sT;
   [[maybe_unused]] const double gLb = sT[N * N + b], gRb = sT[N * N + N + b];
@@ -574,9 +600,16 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
     if (L > 0 && own) {
       const long long base = (jr * a.nx + i0 + lx) * NP + b * N;
       // q^n of the line: prefetched by cp.async one row ahead into thread-private smem
-      if (HQ0) asm volatile("cp.async.wait_group 0;" ::: "memory");
-#define Q0V(c, x) (N % 2 == 0 && vec ? sQ0[((c) * N + ((x) & ~1)) * NT + 2 * tid + ((x) & 1)] \
-                                     : sQ0[((c) * N + (x)) * NT + tid])
+      if (HQ0) {
+        if (H::Q0T) mbar_wait(&qbar[(L - 1) & 1], ((L - 1) >> 1) & 1);
+        else asm volatile("cp.async.wait_group 0;" ::: "memory");
+      }
+      const double* q0s = sQT + ((L - 1) & 1) * H::QSTG;  // (Q0T) this row's q^n slot
+#define Q0V(c, x)                                                                                           \
+  (H::Q0T ? q0s[((c) * TX + lx) * 16 +                                                                      \
+                ((((2 * b + ((x) >> 1)) ^ (((c) * TX + lx) & 7)) << 1) | ((x) & 1))]                        \
+   : (N % 2 == 0 && vec ? sQ0[((c) * N + ((x) & ~1)) * NT + 2 * tid + ((x) & 1)]                             \
+                        : sQ0[((c) * N + (x)) * NT + tid]))
       double F[4], jE[4];
       ld4(sFW + ((lx + 1) * N + b) * 4, F);
 #pragma unroll
@@ -748,7 +781,7 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
           for (int x = 0; x < N; ++x) o[x] = ov[c][x];
         }
       }
-      if (HQ0 && L < RBv && !H2D_Q0LATE)  // q^n of the next row into the (now consumed) private slots
+      if (!H::Q0T && HQ0 && L < RBv && !H2D_Q0LATE)  // q^n of the next row into the (now consumed) private slots
         q0_prefetch<N, NT, H::LP>(sQ0, a.q0, a.cs, base + (long long)a.nx * NP, tid, vec);
       if (HAVG) {  // this line's share of the element average: w_b sum_x w_x q
 #pragma unroll
@@ -795,8 +828,12 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
     // fence of the TMA issue: the fence waits for this thread's in-flight
     // cp.async writes, so a prefetch issued before it stalled warp 0 for a
     // global-memory round trip every row (H2D_Q0LATE=0: the round-2 order)
-    if (H2D_Q0LATE && HQ0 && own && L > 0 && L < RBv)
+    if (!H::Q0T && H2D_Q0LATE && HQ0 && own && L > 0 && L < RBv)
       q0_prefetch<N, NT, H::LP>(sQ0, a.q0, a.cs, ((long long)(jb + L) * a.nx + i0 + lx) * NP + b * N, tid, vec);
+    if (H::Q0T && HQ0 && L > 0 && L + 1 < RBv) {  // q^n two rows ahead into the slot this row consumed
+      if (tid == 0) fence_proxy_async_smem();
+      issue_q0(L + 1);
+    }
   }
   if (HLAM && a.lam) block_max_to(lam, a.lam, sm + H::ORD);
 }
@@ -850,7 +887,8 @@ static int launch_g(const StageArgs& a, cudaStream_t s) {
     const long long nel = (long long)a.nx * a.nrows;
     const int bc = H::CONTIG ? 4 : 1;
     if (!make_map(&maps.q, a.q, nel, a.cs, H::NSL, bc) || !make_map(&maps.lo, a.ghost_lo, a.nx, a.gcs, H::NSL, bc) ||
-        !make_map(&maps.hi, a.ghost_hi, a.nx, a.gcs, H::NSL, bc))
+        !make_map(&maps.hi, a.ghost_hi, a.nx, a.gcs, H::NSL, bc) ||
+        (H::Q0T && !make_map(&maps.q0, a.q0, nel, a.cs, H::TX, 4)))
       return (int)cudaErrorInvalidValue;
   }
   StageArgs b = a;
