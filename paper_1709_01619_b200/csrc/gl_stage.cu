@@ -63,6 +63,9 @@ enum { LM_DG = 2, LM_SD = 4 };
 #ifndef H2D_Q0LATE
 #define H2D_Q0LATE 1
 #endif
+#ifndef H2D_Q0TMA
+#define H2D_Q0TMA 1
+#endif
 #ifndef H2D_WSQRT
 #define H2D_WSQRT fsqrt_ws  // Rusanov dissipation speed (common.cuh; A/B: fsqrt)
 #endif
@@ -89,6 +92,7 @@ constexpr int NSTG = 3;
 
 struct LMaps {
   CUtensorMap q, lo, hi;
+  CUtensorMap q0;  // (Q0T) q^n, box {16, TX, 4}
 };
 
 // operator table (kernel parameter: compile-time indices become constant-bank operands)
@@ -143,7 +147,11 @@ struct L {
   static constexpr int STG = SWZ ? FIXO + 8 * 16 : 4 * CREG;
   static constexpr int STGA = H2D_STGA(STG);  // stage stride (see H2D_STGA)
   static constexpr int OR_ = 0;
-  static constexpr int OFW = OR_ + NSTG * STGA;            // W-face fluxes [TX+1][N][4]
+  // Q0T (P3): q^n of a row by TMA into a 2-row swizzled ring two rows ahead (as gll_stage.cu)
+  static constexpr bool Q0T = H2D_Q0TMA && SWZ;
+  static constexpr int QSTG = 4 * TX * 16;                  // one q^n row: [4 x TX rows of 16]
+  static constexpr int OQT = OR_ + NSTG * STGA;             // (Q0T) q^n ring [2][QSTG]
+  static constexpr int OFW = OQT + (Q0T ? 2 * QSTG : 0);    // W-face fluxes [TX+1][N][4]
 #if H2D_GL_COLY
   // y part of the residual of every point, written by the thread that owns the
   // point's column, read by the one that owns its line: element lx, point
@@ -170,8 +178,9 @@ struct L {
   static constexpr int TOFF = H2D_GL_COLY ? LOps<K>::W : 0, TSZ = H2D_GL_COLY ? N : LOps<K>::TOT;
   static constexpr int ORD = OT + ((TSZ + 1) & ~1);
   static constexpr int OB = ORD + 32;
-  static constexpr int OQ0 = OB + ((NSTG + 1) & ~1);  // q^n prefetch [4][N][NT], thread-private
-  static constexpr int TOTAL = OQ0 + 4 * N * NT;
+  static constexpr int OQ0 = OB + ((NSTG + 2 + 1) & ~1);  // q^n prefetch [4][N][NT], thread-private (!Q0T)
+  static constexpr int TOTAL = OQ0 + (Q0T ? 0 : 4 * N * NT);
+  static_assert(!Q0T || (QSTG % 128 == 0 && OQT % 128 == 0), "1024-B aligned q^n stages");
   static constexpr size_t SMEM = TOTAL * sizeof(double);
 };
 
@@ -266,6 +275,8 @@ __global__ void __launch_bounds__(L<M, K>::NT, LTile<M, K>::MINB) gl_stage_kerne
   double* sT = sm + H::OT;
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + H::OB);
   double* sQ0 = sm + H::OQ0;
+  double* sQT = sm + H::OQT;                  // (Q0T) q^n ring
+  uint64_t* qbar = bar + NSTG;                // (Q0T) its mbarriers
 
   const int tid = threadIdx.x;
   int bhi;
@@ -286,7 +297,7 @@ __global__ void __launch_bounds__(L<M, K>::NT, LTile<M, K>::MINB) gl_stage_kerne
 
   for (int i = tid; i < H::TSZ; i += NT) sT[i] = tab.v[H::TOFF + i];
   if (tid == 0) {
-    for (int s = 0; s < NSTG; ++s) mbar_init(&bar[s], 1);
+    for (int s = 0; s < NSTG + (H::Q0T ? 2 : 0); ++s) mbar_init(&bar[s], 1);
     mbar_fence_init();
   }
   __syncthreads();
@@ -401,8 +412,21 @@ __global__ void __launch_bounds__(L<M, K>::NT, LTile<M, K>::MINB) gl_stage_kerne
   };
 
   for (int Lr = 0; Lr < NSTG && Lr < nload; ++Lr) issue_row(Lr);
-  if (HQ0 && own)  // q^n of the first own row
+  // (Q0T) q^n of own row jb + m into ring slot m & 1, by one TMA box
+  auto issue_q0 = [&](int m) {
+    if (tid != 0) return;
+    uint64_t* bq = &qbar[m & 1];
+    mbar_arrive_expect_tx(bq, 4u * TX * 128u);
+    tma_load_3d(sQT + (m & 1) * H::QSTG, &maps.q0, 0, (jb + m) * a.nx + i0, 0, bq);
+  };
+  if (H::Q0T) {
+    if (HQ0) {  // the first two own rows
+      issue_q0(0);
+      if (RBv > 1) issue_q0(1);
+    }
+  } else if (HQ0 && own) {  // q^n of the first own row
     q0_prefetch<N, NT>(sQ0, a.q0, a.cs, ((long long)jb * a.nx + i0 + lx) * NP + b * N, tid, vec);
+  }
 
   double lam = 0.0;
   const double bdt = a.bcoef * dtv;
@@ -665,9 +689,16 @@ __global__ void __launch_bounds__(L<M, K>::NT, LTile<M, K>::MINB) gl_stage_kerne
 
     if (Lr > 0 && own) {
       const long long base = (jr * a.nx + i0 + lx) * NP + b * N;
-      if (HQ0) asm volatile("cp.async.wait_group 0;" ::: "memory");
-#define Q0V(c, x) (N % 2 == 0 && vec ? sQ0[((c) * N + ((x) & ~1)) * NT + 2 * tid + ((x) & 1)] \
-                                     : sQ0[((c) * N + (x)) * NT + tid])
+      if (HQ0) {
+        if (H::Q0T) mbar_wait(&qbar[(Lr - 1) & 1], ((Lr - 1) >> 1) & 1);
+        else asm volatile("cp.async.wait_group 0;" ::: "memory");
+      }
+      const double* q0s = sQT + ((Lr - 1) & 1) * H::QSTG;  // (Q0T) this row's q^n slot
+#define Q0V(c, x)                                                                                           \
+  (H::Q0T ? q0s[((c) * TX + lx) * 16 +                                                                      \
+                ((((2 * b + ((x) >> 1)) ^ (((c) * TX + lx) & 7)) << 1) | ((x) & 1))]                        \
+   : (N % 2 == 0 && vec ? sQ0[((c) * N + ((x) & ~1)) * NT + 2 * tid + ((x) & 1)]                             \
+                        : sQ0[((c) * N + (x)) * NT + tid]))
       double FW[4], FE[4];
       ld4(sFW + (lx * N + b) * 4, FW);
       ld4(sFW + ((lx + 1) * N + b) * 4, FE);
@@ -799,7 +830,7 @@ __global__ void __launch_bounds__(L<M, K>::NT, LTile<M, K>::MINB) gl_stage_kerne
           for (int x = 0; x < N; ++x) o[x] = ov[c][x];
         }
       }
-      if (HQ0 && Lr < RBv && !H2D_Q0LATE)  // q^n of the next row into the consumed private slots
+      if (!H::Q0T && HQ0 && Lr < RBv && !H2D_Q0LATE)  // q^n of the next row into the consumed private slots
         q0_prefetch<N, NT>(sQ0, a.q0, a.cs, base + (long long)a.nx * NP, tid, vec);
       if (HAVG) {  // this line's share of the element average: w_b sum_x w_x q
 #pragma unroll
@@ -846,8 +877,12 @@ __global__ void __launch_bounds__(L<M, K>::NT, LTile<M, K>::MINB) gl_stage_kerne
     // fence of the TMA issue: the fence waits for this thread's in-flight
     // cp.async writes, so a prefetch issued before it stalled warp 0 for a
     // global-memory round trip every row (H2D_Q0LATE=0: the round-2 order)
-    if (H2D_Q0LATE && HQ0 && own && Lr > 0 && Lr < RBv)
+    if (!H::Q0T && H2D_Q0LATE && HQ0 && own && Lr > 0 && Lr < RBv)
       q0_prefetch<N, NT>(sQ0, a.q0, a.cs, ((long long)(jb + Lr) * a.nx + i0 + lx) * NP + b * N, tid, vec);
+    if (H::Q0T && HQ0 && Lr > 0 && Lr + 1 < RBv) {  // q^n two rows ahead into the slot this row consumed
+      if (tid == 0) fence_proxy_async_smem();
+      issue_q0(Lr + 1);
+    }
   }
   if (HLAM && a.lam) block_max_to(lam, a.lam, sm + H::ORD);
 }
@@ -870,7 +905,8 @@ static int launch_l(const StageArgs& a, cudaStream_t s) {
   if (H::SWZ) {
     const long long nel = (long long)a.nx * a.nrows;
     if (!make_map(&maps.q, a.q, nel, a.cs, H::NSL) || !make_map(&maps.lo, a.ghost_lo, a.nx, a.gcs, H::NSL) ||
-        !make_map(&maps.hi, a.ghost_hi, a.nx, a.gcs, H::NSL))
+        !make_map(&maps.hi, a.ghost_hi, a.nx, a.gcs, H::NSL) ||
+        (H::Q0T && !make_map(&maps.q0, a.q0, nel, a.cs, H::TX, 4)))
       return (int)cudaErrorInvalidValue;
   }
   StageArgs b = a;

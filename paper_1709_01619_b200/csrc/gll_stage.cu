@@ -126,10 +126,10 @@ struct G {
   // 16 doubles contiguous over components, no padding to whole 1024-B blocks;
   // the swizzle phase of row r = c NSL + e of the box is r & 7).  A/B (round
   // 2b): NDG P3 +1 %, CPR P3 -1 % (it keeps four per-component boxes)
-  // Q0T (CPR P3): q^n of a row by TMA into a 2-row swizzled ring, issued two rows
+  // Q0T (P3): q^n of a row by TMA into a 2-row swizzled ring, issued two rows
   // ahead (instead of one row ahead by per-thread cp.async); the contiguous
   // box below pays for its shared memory
-  static constexpr bool Q0T = H2D_Q0TMA && SWZ && M == GM_CPR;
+  static constexpr bool Q0T = H2D_Q0TMA && SWZ;
   static constexpr bool CONTIG = H2D_SWZ_CONTIG && (M == GM_NDG || Q0T);
   static constexpr int RSW = CONTIG ? NSL : (NSL + 7) & ~7;
   static constexpr int FIXO = 4 * RSW * 16;
