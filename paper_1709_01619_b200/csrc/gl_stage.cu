@@ -63,6 +63,9 @@ enum { LM_DG = 2, LM_SD = 4 };
 #ifndef H2D_Q0LATE
 #define H2D_Q0LATE 1
 #endif
+#ifndef H2D_VIEWCARRY
+#define H2D_VIEWCARRY 1  // a row's view of the ring (source, piece offsets) computed once, carried to the next row
+#endif
 #ifndef H2D_Q0TMA
 #define H2D_Q0TMA 1
 #endif
@@ -439,10 +442,12 @@ __global__ void __launch_bounds__(L<M, K>::NT, LTile<M, K>::MINB) gl_stage_kerne
 #if H2D_GL_COLY
   double FSr[4] = {0.0, 0.0, 0.0, 0.0};  // S-face flux of this thread's column (the row below's N face)
 #endif
+  RowView vcar = view(0);  // (H2D_VIEWCARRY) the next row's view, carried
   for (int Lr = 0; Lr <= RBv; ++Lr) {
     mbar_wait(&bar[Lr % NSTG], (Lr / NSTG) & 1);
     mbar_wait(&bar[(Lr + 1) % NSTG], ((Lr + 1) / NSTG) & 1);
-    const RowView vc = view(Lr), vn = view(Lr + 1);
+    const RowView vc = H2D_VIEWCARRY ? vcar : view(Lr), vn = view(Lr + 1);
+    vcar = vn;
 #if !H2D_GL_COLY
     double* FNc = sFN + (Lr & 1) * TX * N * 4;        // N-face fluxes of this row (written now)
     double* FSc = sFN + ((Lr + 1) & 1) * TX * N * 4;  // S-face fluxes of this row (written in step Lr-1)

@@ -217,6 +217,9 @@ __device__ __forceinline__ void ld4(const double* p, double v[4]) {
 #ifndef H2D_Q0LATE
 #define H2D_Q0LATE 1
 #endif
+#ifndef H2D_VIEWCARRY
+#define H2D_VIEWCARRY 1  // a row's view of the ring (source, piece offsets) computed once, carried to the next row
+#endif
 #ifndef H2D_WSQRT
 #define H2D_WSQRT fsqrt_ws  // Rusanov dissipation speed (common.cuh; A/B: fsqrt)
 #endif
@@ -442,10 +445,12 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
   const double cx = -bdt * a.rdx2, cy = -bdt * a.rdy2;
 
   double JSr[4] = {0.0, 0.0, 0.0, 0.0};  // CY: S jump of this thread's column (from the row below's N face)
+  RowView vcar = view(0);  // (H2D_VIEWCARRY) the next row's view, carried
   for (int L = 0; L <= RBv; ++L) {
     mbar_wait(&bar[L % NSTG], (L / NSTG) & 1);
     mbar_wait(&bar[(L + 1) % NSTG], ((L + 1) / NSTG) & 1);
-    const RowView vc = view(L), vn = view(L + 1);
+    const RowView vc = H2D_VIEWCARRY ? vcar : view(L), vn = view(L + 1);
+    vcar = vn;
     double* jSc = sJS + (L & 1) * TX * N * 4;        // S jumps of row L (written in step L-1)
     double* jSn = sJS + ((L + 1) & 1) * TX * N * 4;  // S jumps of row L+1 (written now)
     const long long jr = jb - 1 + L;                 // local strip row of this step
