@@ -361,13 +361,20 @@ __global__ void __launch_bounds__(L<M, K>::NT, LTile<M, K>::MINB) gl_stage_kerne
     int dW, dM, dE, csodd;
     bool have;
   };
+  const bool has_glo = a.ghost_lo != nullptr, has_ghi = a.ghost_hi != nullptr;
   auto view = [&](int Lr) {
     RowView v;
+    v.st = ring + (Lr % NSTG) * STGA;
+    v.dW = v.dM = v.dE = 0;
+    v.csodd = 0;
+    if constexpr (H::SWZ) {  // (the 128-B rows need no piece offsets: only whether the row exists)
+      const int jr = jb - 1 + Lr;
+      v.have = jr < 0 ? has_glo : (jr >= a.nrows ? has_ghi : true);
+      return v;
+    }
     long long cs;
     const double* rb = row_src(a, jb - 1 + Lr, NP, cs);
-    v.st = ring + (Lr % NSTG) * STGA;
     v.have = rb != nullptr;
-    v.dW = v.dM = v.dE = 0;
     v.csodd = (int)(cs & 1);
     if (!H::SWZ && rb) {
       v.dM = piece_off(rb + (long long)i0 * NP);

@@ -375,13 +375,21 @@ __global__ void __launch_bounds__(G<M, K>::NT, GTile<K>::MINB)
     bool have;
     bool v2;  // 1-D path: every component's own piece 16-B aligned (P1 pairs load as double2)
   };
+  const bool has_glo = a.ghost_lo != nullptr, has_ghi = a.ghost_hi != nullptr;
   auto view = [&](int L) {
     RowView v;
+    v.st = ring + (L % NSTG) * STGA;
+    v.dW = v.dM = v.dE = 0;
+    v.csodd = 0;
+    v.v2 = false;
+    if constexpr (H::SWZ) {  // (the 128-B rows need no piece offsets: only whether the row exists)
+      const int jr = jb - 1 + L;
+      v.have = jr < 0 ? has_glo : (jr >= a.nrows ? has_ghi : true);
+      return v;
+    }
     long long cs;
     const double* rb = row_src(a, jb - 1 + L, NP, cs);
-    v.st = ring + (L % NSTG) * STGA;
     v.have = rb != nullptr;
-    v.dW = v.dM = v.dE = 0;
     v.csodd = (int)(cs & 1);
     if (!H::SWZ && rb) {
       v.dM = piece_off(rb + (long long)i0 * NP);
