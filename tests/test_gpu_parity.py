@@ -325,6 +325,26 @@ def test_full_size_tiled_patch_step(orc, P, method, k, n):
     s.close()
 
 
+@pytest.mark.parametrize("method,k", [("cpr", 3), ("ndg", 3), ("dg", 3), ("sd", 3), ("sd", 4), ("ndg", 4),
+                                      ("cpr", 2), ("fv", 2)])
+def test_multi_row_march_transmissive(orc, P, method, k):
+    """Transmissive x and y (the mirrored end faces, the missing ghost rows of the
+    strip's first and last marches, the q^n ring's first and last rows) on grids
+    where every CTA marches several element rows and strips are ragged: 10
+    SSP-RK3 steps against the oracle on seeded perturbed input."""
+    nx, ny = (200, 163) if method != "fv" else (700, 523)
+    oc = orc.config(nx=nx, ny=ny, method=method, k=k, cfl=CFL[(method, k)], bc=1)
+    from paper_1709_01619_b200.inputs import perturb
+    q = perturb(orc.init_case(oc), seed=43, amp=1e-3)
+    s = P.Solver(P.make_config(nx, ny, method=method, k=k, cfl=CFL[(method, k)], bc=P.TRANSMISSIVE))
+    s.set_state(q)
+    _, n_g = s.step(10)
+    q_o, _, n_o = orc.run(oc, q, 10)
+    assert n_g == n_o == 10
+    assert rel_linf(s.get_state(), q_o) <= 1e-10
+    s.close()
+
+
 @pytest.mark.parametrize("method,k", [("cpr", 3), ("ndg", 3), ("dg", 2), ("sd", 3), ("fv", 2)])
 def test_multi_row_march_parity(orc, P, method, k):
     """Grids big enough that each CTA marches several element rows (and strips are
